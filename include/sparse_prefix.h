@@ -1,0 +1,148 @@
+/*
+ * include/sparse_prefix.h -- C ABI of libsparseprefix.so, the B200 (sm_100a) hot path of
+ * sparse prefix caching (arXiv 2605.05219, "PAPER.md"; "P:L" = PAPER.md line L).
+ *
+ * The method: for each retained cache entry (a cached prefix of length <= N), estimate the law
+ * of the overlap depth T of future requests from observed requests, and place at
+ * most M recurrent-state checkpoints 1 <= c_1 < ... < c_M <= N so that the expected
+ * recomputation E[r(T;C)] = sum_t p_t (t - l(t;C)) is minimal, via the exact dynamic
+ * program of Thm 2.
+ *
+ * General conventions (every call):
+ *   - Pointers are DEVICE pointers unless a parameter says "host".  The caller owns every
+ *     buffer; the library never allocates on these paths (the DP's scratch is a caller-provided
+ *     workspace).  Calls are stateless and thread-safe.
+ *   - Calls are asynchronous and stream-ordered on `stream` (0 = legacy default stream).
+ *   - Shape / argument errors are detected on the host and returned synchronously, with nothing
+ *     enqueued.  Per-entry data errors that can only be seen on the device (overflow guard,
+ *     malformed positions) are reported in the per-entry outputs as documented below.
+ *   - Counts: histograms are integer counts c_t of observed overlap depths, row-major
+ *     [n_entries][N+1]; bin 0 counts misses and is ignored by the objective (T in {1..N},
+ *     P:169; hits only).  Probabilities p = c / n are never formed: the argmin is
+ *     scale invariant, and costs are returned as integer numerators n * E[r].
+ *   - Canonical output ("rule B", reading R3): among optimal placements the library
+ *     returns the colex-minimal one: per DP cell the lowest-index argmin, backtracked from
+ *     (M, N) and stopped as soon as no mass remains at or below the current depth.
+ */
+#ifndef SPARSE_PREFIX_H
+#define SPARSE_PREFIX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sp_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  SP_OK = 0,
+  SP_ERR_BAD_LENGTH = 1,       /* N < 1, n_entries < 0, n_requests < 0, N > SP_MAX_N            */
+  SP_ERR_BUDGET_TOO_LARGE = 2, /* M < 0 or M > N                                                */
+  SP_ERR_BAD_ARGUMENT = 3,     /* NULL required pointer, bad enum, misaligned buffer            */
+  SP_ERR_OVERFLOW = 4,         /* per entry: 2 * n * N does not fit the cost type               */
+  SP_ERR_BAD_POSITIONS = 5,    /* per set: positions not strictly increasing in [1, N]          */
+  SP_ERR_WORKSPACE = 6,        /* workspace NULL or smaller than *_workspace_bytes()            */
+  SP_ERR_CUDA = 7,             /* launch / runtime error; see sp_last_error_string()            */
+  SP_ERR_INTERNAL = 8          /* per entry: a D&C bracket came out empty (never expected)      */
+} sp_status;
+
+typedef enum {
+  SP_W_COUNTS_I32 = 0, /* int32_t c[E][N+1]                                                    */
+  SP_W_COUNTS_I64 = 1, /* int64_t c[E][N+1]                                                    */
+  SP_W_PROB_F64 = 2    /* double  w[E][N+1], w_t >= 0 finite (fp64 variant; costs are double)  */
+} sp_weight_type;
+
+#define SP_MAX_N 65535 /* positions are stored as uint16 in the argmin table */
+
+/* ------------------------------------------------------------------------------------------
+ * a1 + a2 -- overlap depths and the per-entry overlap-depth histogram.
+ * P:133-137 (overlap depth t of a request with the cached prefix), P:169 (T in {1..N}),
+ * P:189-190 (per-edge decomposition: each request is matched against the entry it hit).
+ *
+ * For request r (tokens req_tokens[req_off[r] .. req_off[r+1])) and its entry
+ * e = req_entry[r] (tokens entry_tokens[entry_off[e] .. entry_off[e+1])):
+ *     t_r = min(LCP(request, entry), N)          (depths beyond N clamp to N)
+ *     hist[e][t_r] += 1                          (ACCUMULATED: the caller zeroes hist)
+ *     lcp_out[r] = t_r                           (if lcp_out != NULL)
+ * Offsets are int64 token indices; rows with offsets that are multiples of 4 tokens take the
+ * 16-byte vector path, others a scalar path (same result).  Precondition (checked only by
+ * debug builds): 0 <= req_entry[r] < n_entries; requests with an out-of-range entry are
+ * skipped and get lcp_out[r] = -1.
+ * Errors: SP_ERR_BAD_LENGTH (N < 1 or N > SP_MAX_N, n_entries < 0, n_requests < 0),
+ *         SP_ERR_BAD_ARGUMENT (NULL required pointer), SP_ERR_CUDA.
+ * ---------------------------------------------------------------------------------------- */
+sp_status sp_overlap_hist(const int32_t* entry_tokens, const int64_t* entry_off,
+                          int32_t n_entries, const int32_t* req_tokens, const int64_t* req_off,
+                          const int32_t* req_entry, int64_t n_requests, int32_t N,
+                          int32_t* hist, int32_t* lcp_out, sp_stream_t stream);
+
+/* Multi-GPU merge helper (SURVEY 8(e) sparse variant): hist[e - e_begin][depth[i]] += 1 for
+ * every i with e_begin <= entry[i] < e_end and 0 <= depth[i] <= N (others ignored).
+ * hist is [e_end - e_begin][N+1], accumulated.  Errors: BAD_LENGTH, BAD_ARGUMENT, CUDA. */
+sp_status sp_accumulate_depths(const int32_t* entry, const int32_t* depth, int64_t n,
+                               int32_t e_begin, int32_t e_end, int32_t N, int32_t* hist,
+                               sp_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * a3 + a4 + a5 -- optimal checkpoint placement (Thm 2; proof P:755-774).
+ *   P_j = sum_{t<=j} c_t,  T_j = sum_{t<=j} t c_t
+ *   dp[0][j] = T_j,  dp[m][0] = 0 (at-most-m reading R1),
+ *   dp[m][j] = min_{1<=s<=j} dp[m-1][s-1] + (T_j - T_{s-1}) - s (P_j - P_{s-1})
+ * computed on the GPU as a divide-and-conquer monotone argmin per layer, exactly.
+ *
+ *   weights        [E][N+1] of type wtype (bin 0 ignored; not normalised)
+ *   positions      int32 [E][M]: the rule-B placement, ascending, unused slots 0
+ *   n_positions    int32 [E]: number of positions (0..min(M, #nonzero bins)), or a NEGATIVE
+ *                  sp_status for that entry (-SP_ERR_OVERFLOW if 2 * P_N * N >= 2^62 for the
+ *                  count types; -SP_ERR_INTERNAL never expected)
+ *   cost           [E]: V_M = dp[M][N] = n * E[r] -- int64 for count types, double for F64
+ *   cost_by_budget [E][M+1] V_0..V_M (same type as cost; V_0 = T_N = n * R_nc), or
+ *                  NULL.  (The DP computes every budget m <= M on the way.)
+ *   workspace      device scratch of >= sp_place_checkpoints_workspace_bytes(E, N, M) bytes
+ * M = 0 gives n_positions = 0 and cost = T_N.  An all-zero histogram gives 0 positions, cost 0.
+ * Errors (synchronous): BAD_LENGTH (N < 1, N > SP_MAX_N, E < 0), BUDGET_TOO_LARGE (M < 0 or
+ * M > N), BAD_ARGUMENT (NULL pointer, bad wtype), WORKSPACE, CUDA.
+ * ---------------------------------------------------------------------------------------- */
+size_t sp_place_checkpoints_workspace_bytes(int32_t n_entries, int32_t N, int32_t M);
+
+sp_status sp_place_checkpoints(const void* weights, sp_weight_type wtype, int32_t n_entries,
+                               int32_t N, int32_t M, int32_t* positions, int32_t* n_positions,
+                               void* cost, void* cost_by_budget, void* workspace,
+                               size_t workspace_bytes, sp_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * a6 -- expected recomputation and worst case of given placements (baseline evaluation).
+ * For checkpoint set C = {c_1 < ... < c_k} (c_0 = 0, c_{k+1} = N + 1):
+ *   cost  = sum_{t=1}^N c_t (t - l(t;C))                          (l from P:133-137)
+ *   worst = max_{0<=i<=k} (c_{i+1} - c_i) - 1 = max_t r(t;C)       (distribution-free)
+ * n_sets placements per entry.  broadcast != 0: positions [n_sets][max_pos] and
+ * n_positions [n_sets] are shared by every entry (e.g. balanced / block schedules, Table 1
+ * P:360-378); broadcast == 0: positions [E][n_sets][max_pos], n_positions [E][n_sets].
+ *   cost        [E][n_sets]: int64 (count types) or double (F64)
+ *   worst_case  int32 [E][n_sets] or NULL
+ * A malformed set (k < 0, k > max_pos, positions not strictly increasing in [1, N]) yields
+ * cost = -1 (count types) / NaN (F64) and worst = -SP_ERR_BAD_POSITIONS for that set.
+ * Errors (synchronous): BAD_LENGTH, BAD_ARGUMENT, CUDA.
+ * ---------------------------------------------------------------------------------------- */
+sp_status sp_expected_recompute(const void* weights, sp_weight_type wtype, int32_t n_entries,
+                                int32_t N, const int32_t* positions, const int32_t* n_positions,
+                                int32_t n_sets, int32_t max_pos, int32_t broadcast, void* cost,
+                                int32_t* worst_case, sp_stream_t stream);
+
+/* Host-side helpers for the Table 1 baselines.  out_host must hold M (resp.
+ * floor(N/B)) ints.  Return the number of positions written, or a negative sp_status. */
+int32_t sp_balanced_positions(int32_t N, int32_t M, int32_t* out_host);
+int32_t sp_block_positions(int32_t N, int32_t B, int32_t* out_host);
+
+const char* sp_status_string(sp_status status);
+/* Last CUDA error text seen by this thread (static storage, never NULL). */
+const char* sp_last_error_string(void);
+/* Library version string, e.g. "sparseprefix 0.1 sm_100a". */
+const char* sp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSE_PREFIX_H */

@@ -1,0 +1,211 @@
+// expected_recompute.cu -- a6: expected recomputation and worst case of given placements
+// (baseline evaluation: balanced / block schedules of Table 1; objective P:171-173).
+//
+// For C = {c_1 < ... < c_k}, c_0 = 0, c_{k+1} = N+1, segment i holds depths [c_i, c_{i+1}-1]
+// whose reusable depth is c_i, so
+//     cost = sum_i sum_{t in seg i} c_t (t - c_i) = T_N - sum_{i=1}^k c_i (P(c_{i+1}-1) - P(c_i-1))
+// (the w(s,j) decomposition of P:758 summed over the segments), and
+//     worst = max_i (c_{i+1} - c_i) - 1.
+// HBM-bound: one CTA per entry reads the histogram row once (coalesced) into 32-bin chunk
+// prefix sums kept in shared memory; each placement then needs k+1 prefix values
+// P(x) = chunk prefix + a <= 32-bin partial sum (L1/L2-resident row).  One warp per placement.
+// Count types are exact in int64; fp64 weights are accumulated in double-double.
+#include <cmath>
+
+#include "common.cuh"
+
+namespace sp {
+
+constexpr int EV_NT = 256;
+constexpr int EV_NW = EV_NT / 32;
+constexpr int EV_MAXCH = 2049;   // (SP_MAX_N + 1) / 32 + 1
+
+struct ddv {
+  double hi, lo;
+};
+__device__ __forceinline__ ddv add(ddv a, ddv b) {
+  double s = a.hi + b.hi;
+  double bb = s - a.hi;
+  double err = (a.hi - (s - bb)) + (b.hi - bb) + a.lo + b.lo;
+  double h = s + err;
+  return ddv{h, err - (h - s)};
+}
+__device__ __forceinline__ ddv neg(ddv a) { return ddv{-a.hi, -a.lo}; }
+__device__ __forceinline__ ddv mul_int(ddv a, int c) {
+  double p = a.hi * c;
+  double e = fma(a.hi, (double)c, -p) + a.lo * c;
+  double h = p + e;
+  return ddv{h, e - (h - p)};
+}
+__device__ __forceinline__ int64_t add(int64_t a, int64_t b) { return a + b; }
+__device__ __forceinline__ int64_t neg(int64_t a) { return -a; }
+__device__ __forceinline__ int64_t mul_int(int64_t a, int c) { return a * c; }
+
+template <typename WT>
+struct EvTraits {
+  using A = int64_t;
+  using CT = int64_t;
+  static __device__ __forceinline__ A from(WT x) { return (int64_t)x; }
+  static __device__ __forceinline__ A prod(int t, WT x) { return (int64_t)t * (int64_t)x; }
+  static __device__ __forceinline__ CT out(A a) { return a; }
+  static __device__ __forceinline__ CT bad() { return -1; }
+  static __device__ __forceinline__ A shfl_xor(A a, int o) { return __shfl_xor_sync(FULL, a, o); }
+  static __device__ __forceinline__ A shfl_up(A a, int o) { return __shfl_up_sync(FULL, a, o); }
+  static __device__ __forceinline__ A shfl_idx(A a, int l) { return __shfl_sync(FULL, a, l); }
+};
+template <>
+struct EvTraits<double> {
+  using A = ddv;
+  using CT = double;
+  static __device__ __forceinline__ A from(double x) { return ddv{x, 0.0}; }
+  static __device__ __forceinline__ A prod(int t, double x) {
+    double p = t * x;
+    return ddv{p, fma((double)t, x, -p)};
+  }
+  static __device__ __forceinline__ CT out(A a) { return a.hi + a.lo; }
+  static __device__ __forceinline__ CT bad() { return NAN; }
+  static __device__ __forceinline__ A shfl_xor(A a, int o) {
+    return ddv{__shfl_xor_sync(FULL, a.hi, o), __shfl_xor_sync(FULL, a.lo, o)};
+  }
+  static __device__ __forceinline__ A shfl_up(A a, int o) {
+    return ddv{__shfl_up_sync(FULL, a.hi, o), __shfl_up_sync(FULL, a.lo, o)};
+  }
+  static __device__ __forceinline__ A shfl_idx(A a, int l) {
+    return ddv{__shfl_sync(FULL, a.hi, l), __shfl_sync(FULL, a.lo, l)};
+  }
+};
+
+template <typename A, typename Tr>
+__device__ __forceinline__ A warp_reduce(A v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = add(v, Tr::shfl_xor(v, o));
+  return v;
+}
+
+template <typename WT>
+__global__ void __launch_bounds__(EV_NT)
+    eval_kernel(const WT* __restrict__ w, int E, int N, const int32_t* __restrict__ positions,
+                const int32_t* __restrict__ npos, int S, int max_pos, int broadcast,
+                typename EvTraits<WT>::CT* __restrict__ cost, int32_t* __restrict__ worst) {
+  using Tr = EvTraits<WT>;
+  using A = typename Tr::A;
+  __shared__ A chp[EV_MAXCH + 1];   // chp[c] = sum of bins < 32 c (bin 0 excluded)
+  __shared__ A wsum[EV_NW];
+  __shared__ A sh_TN;
+  const int lane = lane_id(), wid = warp_id();
+  const int nch = (N + 1 + 31) / 32;
+
+  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+    const WT* we = w + (int64_t)e * (N + 1);
+    // -- chunk sums (warp per chunk) and T_N ------------------------------------------------
+    A tpart = A{};
+    for (int c = wid; c < nch; c += EV_NW) {
+      const int t = 32 * c + lane;
+      const WT x = (t >= 1 && t <= N) ? we[t] : WT(0);
+      A s = warp_reduce<A, Tr>(Tr::from(x));
+      tpart = add(tpart, Tr::prod(t, x));
+      if (lane == 0) chp[c + 1] = s;
+    }
+    tpart = warp_reduce<A, Tr>(tpart);
+    if (lane == 0) wsum[wid] = tpart;
+    __syncthreads();
+    if (wid == 0) {   // warp scan of the chunk sums, 32 chunks per step
+      A run = A{};
+      if (lane == 0) chp[0] = run;
+      for (int base = 1; base <= nch; base += 32) {
+        const int c = base + lane;
+        A inc = c <= nch ? chp[c] : A{};
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const A y = Tr::shfl_up(inc, o);
+          if (lane >= o) inc = add(inc, y);
+        }
+        if (c <= nch) chp[c] = add(run, inc);
+        run = add(run, Tr::shfl_idx(inc, 31));
+      }
+      if (lane == 0) {
+        A tn = A{};
+        for (int q = 0; q < EV_NW; ++q) tn = add(tn, wsum[q]);
+        sh_TN = tn;
+      }
+    }
+    __syncthreads();
+    const A TN = sh_TN;
+
+    // P(x) = sum_{t=1}^x w_t
+    auto Pof = [&](int x) -> A {
+      const int c = x >> 5;
+      A s = chp[c];
+      for (int t = max(32 * c, 1); t <= x; ++t) s = add(s, Tr::from(we[t]));
+      return s;
+    };
+
+    // -- one warp per placement --------------------------------------------------------------
+    for (int q = wid; q < S; q += EV_NW) {
+      const int64_t set = broadcast ? q : (int64_t)e * S + q;
+      const int32_t* pc = positions + set * max_pos;
+      const int k = npos[set];
+      bool ok = k >= 0 && k <= max_pos;
+      A acc = A{};
+      int gmax = 0;
+      if (ok) {
+        for (int i = lane; i <= k; i += 32) {   // gap i: (c_i, c_{i+1})
+          const int ci = i == 0 ? 0 : pc[i - 1];
+          const int cn = i == k ? N + 1 : pc[i];
+          if (cn <= ci || cn > N + 1 || (i > 0 && ci < 1)) ok = false;
+          gmax = max(gmax, cn - ci);
+          if (i >= 1 && ok) {
+            // c_i (P(c_{i+1} - 1) - P(c_i - 1))
+            const A d = add(Pof(cn - 1), neg(Pof(ci - 1)));
+            acc = add(acc, mul_int(d, ci));
+          }
+        }
+      }
+      ok = __all_sync(FULL, ok);
+      acc = warp_reduce<A, Tr>(acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gmax = max(gmax, __shfl_xor_sync(FULL, gmax, o));
+      if (lane == 0) {
+        const int64_t oi = (int64_t)e * S + q;
+        cost[oi] = ok ? Tr::out(add(TN, neg(acc))) : Tr::bad();
+        if (worst) worst[oi] = ok ? gmax - 1 : -SP_ERR_BAD_POSITIONS;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace sp
+
+extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type wtype,
+                                           int32_t n_entries, int32_t N,
+                                           const int32_t* positions, const int32_t* n_positions,
+                                           int32_t n_sets, int32_t max_pos, int32_t broadcast,
+                                           void* cost, int32_t* worst_case, sp_stream_t stream) {
+  if (N < 1 || N > SP_MAX_N || n_entries < 0 || n_sets < 0 || max_pos < 0)
+    return SP_ERR_BAD_LENGTH;
+  if (wtype != SP_W_COUNTS_I32 && wtype != SP_W_COUNTS_I64 && wtype != SP_W_PROB_F64)
+    return SP_ERR_BAD_ARGUMENT;
+  if (n_entries == 0 || n_sets == 0) return SP_OK;
+  if (!weights || !n_positions || !cost || (max_pos > 0 && !positions))
+    return SP_ERR_BAD_ARGUMENT;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = n_entries < sms * 8 ? n_entries : sms * 8;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (wtype == SP_W_COUNTS_I32)
+    sp::eval_kernel<int32_t><<<grid, sp::EV_NT, 0, st>>>(
+        (const int32_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
+        broadcast, (int64_t*)cost, worst_case);
+  else if (wtype == SP_W_COUNTS_I64)
+    sp::eval_kernel<int64_t><<<grid, sp::EV_NT, 0, st>>>(
+        (const int64_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
+        broadcast, (int64_t*)cost, worst_case);
+  else
+    sp::eval_kernel<double><<<grid, sp::EV_NT, 0, st>>>(
+        (const double*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
+        broadcast, (double*)cost, worst_case);
+  SP_CHECK_LAUNCH();
+  return SP_OK;
+}

@@ -1,0 +1,230 @@
+"""Thin ctypes binding of libsparseprefix.so (include/sparse_prefix.h), same names as the C ABI.
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of the library.
+There is no CPU fallback -- if the library is missing or a tensor is not on a CUDA device, the
+call raises.  torch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsparseprefix.so")
+
+SP_OK = 0
+SP_ERR_BAD_LENGTH = 1
+SP_ERR_BUDGET_TOO_LARGE = 2
+SP_ERR_BAD_ARGUMENT = 3
+SP_ERR_OVERFLOW = 4
+SP_ERR_BAD_POSITIONS = 5
+SP_ERR_WORKSPACE = 6
+SP_ERR_CUDA = 7
+SP_ERR_INTERNAL = 8
+
+SP_W_COUNTS_I32 = 0
+SP_W_COUNTS_I64 = 1
+SP_W_PROB_F64 = 2
+SP_MAX_N = 65535
+
+_WTYPE = {torch.int32: SP_W_COUNTS_I32, torch.int64: SP_W_COUNTS_I64,
+          torch.float64: SP_W_PROB_F64}
+
+_lib = None
+_vp, _i32, _i64, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+
+SYMBOLS = {
+    # name: (restype, argtypes)
+    "sp_overlap_hist": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp]),
+    "sp_accumulate_depths": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "sp_place_checkpoints_workspace_bytes": (_sz, [_i32, _i32, _i32]),
+    "sp_place_checkpoints": (ctypes.c_int, [_vp, ctypes.c_int, _i32, _i32, _i32, _vp, _vp, _vp,
+                                            _vp, _vp, _sz, _vp]),
+    "sp_expected_recompute": (ctypes.c_int, [_vp, ctypes.c_int, _i32, _i32, _vp, _vp, _i32, _i32,
+                                             _i32, _vp, _vp, _vp]),
+    "sp_balanced_positions": (_i32, [_i32, _i32, _vp]),
+    "sp_block_positions": (_i32, [_i32, _i32, _vp]),
+    "sp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "sp_last_error_string": (ctypes.c_char_p, []),
+    "sp_version": (ctypes.c_char_p, []),
+}
+
+
+class SPError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = lib().sp_status_string(status).decode()
+        if status == SP_ERR_CUDA:
+            msg += " (" + lib().sp_last_error_string().decode() + ")"
+        super().__init__(f"{where}: {msg}")
+
+
+def lib():
+    """Load libsparseprefix.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2605_05219_b200.build`"
+                               " or __graft_entry__.build() first (there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SYMBOLS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int, where: str):
+    if st != SP_OK:
+        raise SPError(st, where)
+
+
+def _dev(t: torch.Tensor, dtype, name: str, ndim=None):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be on a CUDA device (no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must be {ndim}-D")
+    return t.data_ptr()
+
+
+def _stream(stream, device):
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def overlap_hist(entry_tokens, entry_off, req_tokens, req_off, req_entry, N, hist=None,
+                 lcp_out=None, n_entries=None, stream=None):
+    """a1 + a2.  Returns (hist [E][N+1] int32, accumulated in place; lcp_out [R] or None)."""
+    E = entry_off.numel() - 1 if n_entries is None else n_entries
+    R = req_off.numel() - 1
+    dev = req_tokens.device
+    if hist is None:
+        hist = torch.zeros(E, N + 1, dtype=torch.int32, device=dev)
+    st = lib().sp_overlap_hist(
+        _dev(entry_tokens, torch.int32, "entry_tokens"), _dev(entry_off, torch.int64, "entry_off"),
+        E, _dev(req_tokens, torch.int32, "req_tokens"), _dev(req_off, torch.int64, "req_off"),
+        _dev(req_entry, torch.int32, "req_entry"), R, N, _dev(hist, torch.int32, "hist"),
+        None if lcp_out is None else _dev(lcp_out, torch.int32, "lcp_out"), _stream(stream, dev))
+    _check(st, "sp_overlap_hist")
+    return hist, lcp_out
+
+
+def accumulate_depths(entry, depth, e_begin, e_end, N, hist, stream=None):
+    st = lib().sp_accumulate_depths(_dev(entry, torch.int32, "entry"),
+                                    _dev(depth, torch.int32, "depth"), entry.numel(), e_begin,
+                                    e_end, N, _dev(hist, torch.int32, "hist"),
+                                    _stream(stream, hist.device))
+    _check(st, "sp_accumulate_depths")
+    return hist
+
+
+def place_checkpoints_workspace_bytes(n_entries, N, M) -> int:
+    return int(lib().sp_place_checkpoints_workspace_bytes(n_entries, N, M))
+
+
+def place_checkpoints(weights, M, positions=None, n_positions=None, cost=None,
+                      cost_by_budget=False, workspace=None, stream=None):
+    """a3-a5 (+ a7 for float64 weights).  weights: [E][N+1] int32 / int64 counts or float64.
+    Returns (positions [E][M] int32, n_positions [E] int32, cost [E], cost_by_budget or None)."""
+    if weights.dim() != 2:
+        raise ValueError("weights must be [E][N+1]")
+    wtype = _WTYPE.get(weights.dtype)
+    if wtype is None:
+        raise TypeError("weights must be int32, int64 or float64")
+    E, N = weights.shape[0], weights.shape[1] - 1
+    dev = weights.device
+    cdt = torch.float64 if wtype == SP_W_PROB_F64 else torch.int64
+    if positions is None:
+        positions = torch.empty(E, max(M, 0), dtype=torch.int32, device=dev)
+    if n_positions is None:
+        n_positions = torch.empty(E, dtype=torch.int32, device=dev)
+    if cost is None:
+        cost = torch.empty(E, dtype=cdt, device=dev)
+    cbb = None
+    if cost_by_budget is True:
+        cbb = torch.empty(E, M + 1, dtype=cdt, device=dev)
+    elif isinstance(cost_by_budget, torch.Tensor):
+        cbb = cost_by_budget
+    need = place_checkpoints_workspace_bytes(E, N, M)
+    if workspace is None:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    st = lib().sp_place_checkpoints(
+        _dev(weights, weights.dtype, "weights"), wtype, E, N, M,
+        _dev(positions, torch.int32, "positions") if M > 0 else None,
+        _dev(n_positions, torch.int32, "n_positions"), _dev(cost, cdt, "cost"),
+        None if cbb is None else _dev(cbb, cdt, "cost_by_budget"),
+        _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream, dev))
+    _check(st, "sp_place_checkpoints")
+    return positions, n_positions, cost, cbb
+
+
+def expected_recompute(weights, positions, n_positions, broadcast=True, cost=None, worst=None,
+                       stream=None):
+    """a6.  broadcast: positions [S][max_pos] / n_positions [S] shared by all entries; else
+    [E][S][max_pos] / [E][S].  Returns (cost [E][S], worst [E][S])."""
+    wtype = _WTYPE.get(weights.dtype)
+    if wtype is None:
+        raise TypeError("weights must be int32, int64 or float64")
+    E, N = weights.shape[0], weights.shape[1] - 1
+    dev = weights.device
+    if broadcast:
+        S, max_pos = positions.shape[0], positions.shape[1]
+    else:
+        S, max_pos = positions.shape[1], positions.shape[2]
+    cdt = torch.float64 if wtype == SP_W_PROB_F64 else torch.int64
+    if cost is None:
+        cost = torch.empty(E, S, dtype=cdt, device=dev)
+    if worst is None:
+        worst = torch.empty(E, S, dtype=torch.int32, device=dev)
+    st = lib().sp_expected_recompute(
+        _dev(weights, weights.dtype, "weights"), wtype, E, N,
+        _dev(positions, torch.int32, "positions") if positions.numel() else None,
+        _dev(n_positions, torch.int32, "n_positions"), S, max_pos, 1 if broadcast else 0,
+        _dev(cost, cdt, "cost"), _dev(worst, torch.int32, "worst"), _stream(stream, dev))
+    _check(st, "sp_expected_recompute")
+    return cost, worst
+
+
+def balanced_positions(N, M):
+    buf = (ctypes.c_int32 * max(M, 1))()
+    k = lib().sp_balanced_positions(N, M, buf)
+    if k < 0:
+        raise SPError(-k, "sp_balanced_positions")
+    return list(buf[:k])
+
+
+def block_positions(N, B):
+    buf = (ctypes.c_int32 * max(N // max(B, 1), 1))()
+    k = lib().sp_block_positions(N, B, buf)
+    if k < 0:
+        raise SPError(-k, "sp_block_positions")
+    return list(buf[:k])
+
+
+def baseline_sets(N, budgets=(), blocks=(), device="cuda"):
+    """Pack balanced schedules (one per budget) and block schedules (one per B) as broadcast
+    placement sets for expected_recompute: returns (positions [S][max_pos], n_positions [S],
+    labels)."""
+    sets, labels = [], []
+    for m in budgets:
+        sets.append(balanced_positions(N, m))
+        labels.append(("balanced", m))
+    for B in blocks:
+        sets.append(block_positions(N, B))
+        labels.append(("block", B))
+    width = max([len(s) for s in sets] + [1])
+    pos = torch.zeros(len(sets), width, dtype=torch.int32)
+    for i, s in enumerate(sets):
+        if s:
+            pos[i, :len(s)] = torch.tensor(s, dtype=torch.int32)
+    npos = torch.tensor([len(s) for s in sets], dtype=torch.int32)
+    return pos.to(device), npos.to(device), labels

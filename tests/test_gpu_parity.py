@@ -1,0 +1,380 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact for every
+integer output (positions, counts, int64 costs, LCPs, histograms); fp64 variant within 1e-12
+relative error of the exact rational reference V_int / n (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2605_05219_b200 import sp
+from paper_2605_05219_b200 import workload as wl
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2605_05219_b200 import build
+    build.build()
+    sp.lib()
+    return torch.device("cuda:0")
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def run_lcp(tr, N, dev, E):
+    g = {k: v.to(dev) for k, v in tr.items() if isinstance(v, torch.Tensor)}
+    R = g["req_off"].numel() - 1
+    lcp = torch.full((R,), -7, dtype=torch.int32, device=dev)
+    hist, _ = sp.overlap_hist(g["entry_tokens"], g["entry_off"], g["req_tokens"], g["req_off"],
+                              g["req_entry"], N, lcp_out=lcp, n_entries=E)
+    torch.cuda.synchronize()
+    return np_(hist), np_(lcp)
+
+
+def oracle_lcp(tr, N, E):
+    return oracle.lcp_hist(np_(tr["entry_tokens"]), np_(tr["entry_off"]), np_(tr["req_tokens"]),
+                           np_(tr["req_off"]), np_(tr["req_entry"]), N, n_entries=E, nthreads=8)
+
+
+# ------------------------------------------------------------------------------------------
+# a1 + a2 : LCP + histogram
+# ------------------------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("name,E,align", [("W1", 1, 1), ("W2", 40, 4), ("W2", 40, 1),
+                                          ("W3", 12, 4), ("W3", 12, 1)])
+def test_lcp_hist_parity(dev, name, E, align):
+    cfg = wl.scaled(wl.CONFIGS[name], E)
+    cfg = wl.TraceConfig(**{**cfg.__dict__, "align": align, "miss_frac": 0.05})
+    tr = wl.make_trace(cfg, seed=3)
+    h_gpu, l_gpu = run_lcp(tr, cfg.N, dev, E)
+    h_ref, l_ref = oracle_lcp(tr, cfg.N, E)
+    assert (l_gpu == l_ref).all()
+    assert (h_gpu == h_ref).all()
+    # and the construction: LCP = drawn depth (clamped to N)
+    assert (l_gpu == np.minimum(np_(tr["depth"]), cfg.N)).all()
+
+
+def test_lcp_clamp_ragged_and_bad_entries(dev):
+    """N smaller than the overlaps (clamp), empty requests, out-of-range entry ids, and an
+    accumulate (+=) into a non-zero histogram."""
+    cfg = wl.scaled(wl.CONFIGS["W2"], 9)
+    tr = wl.make_trace(cfg, seed=4)
+    N = 300
+    tr["req_entry"][5] = 99          # out of range -> skipped, lcp = -1
+    tr["req_entry"][6] = -1
+    # make request 7 empty
+    off = tr["req_off"].clone()
+    L7 = int(off[8] - off[7])
+    keep = torch.ones(tr["req_tokens"].numel(), dtype=torch.bool)
+    keep[int(off[7]):int(off[8])] = False
+    tr["req_tokens"] = tr["req_tokens"][keep]
+    off[8:] -= L7
+    tr["req_off"] = off
+    g = {k: v.to(dev) for k, v in tr.items() if isinstance(v, torch.Tensor)}
+    R = off.numel() - 1
+    base = torch.randint(0, 5, (9, N + 1), dtype=torch.int32)
+    hist = base.clone().to(dev)
+    lcp = torch.zeros(R, dtype=torch.int32, device=dev)
+    sp.overlap_hist(g["entry_tokens"], g["entry_off"], g["req_tokens"], g["req_off"],
+                    g["req_entry"], N, hist=hist, lcp_out=lcp, n_entries=9)
+    torch.cuda.synchronize()
+    # the oracle rejects bad entry ids as an error: give those requests entry 0 there and
+    # remove their contribution afterwards
+    valid = np.ones(R, bool)
+    valid[[5, 6]] = False
+    ok_entry = np_(tr["req_entry"]).copy()
+    ok_entry[~valid] = 0
+    ref_h, ref_l = oracle.lcp_hist(np_(tr["entry_tokens"]), np_(tr["entry_off"]),
+                                   np_(tr["req_tokens"]), np_(off), ok_entry, N, n_entries=9)
+    got_l = np_(lcp)
+    assert (got_l[valid] == ref_l[valid]).all()
+    assert (got_l[~valid] == -1).all()
+    assert got_l[7] == 0
+    # remove the two substituted requests from the oracle histogram
+    for r in (5, 6):
+        ref_h[0, ref_l[r]] -= 1
+    assert (np_(hist) == np_(base) + ref_h).all()
+
+
+def test_accumulate_depths(dev):
+    rng = np.random.default_rng(5)
+    n, E, N = 20000, 50, 700
+    ent = rng.integers(-3, E + 3, n).astype(np.int32)
+    dep = rng.integers(-2, N + 3, n).astype(np.int32)
+    hist = torch.zeros(20, N + 1, dtype=torch.int32, device=dev)
+    sp.accumulate_depths(torch.from_numpy(ent).to(dev), torch.from_numpy(dep).to(dev), 10, 30, N,
+                         hist)
+    ref = np.zeros((20, N + 1), np.int64)
+    m = (ent >= 10) & (ent < 30) & (dep >= 0) & (dep <= N)
+    np.add.at(ref, (ent[m] - 10, dep[m]), 1)
+    assert (np_(hist) == ref).all()
+
+
+# ------------------------------------------------------------------------------------------
+# a3 - a5 : the DP
+# ------------------------------------------------------------------------------------------
+
+
+def gpu_place(H, M, dev, dtype=torch.int32):
+    w = torch.as_tensor(H).to(dtype).to(dev).contiguous()
+    pos, npos, cost, cbb = sp.place_checkpoints(w, M, cost_by_budget=True)
+    torch.cuda.synchronize()
+    return np_(pos), np_(npos), np_(cost), np_(cbb)
+
+
+def check_against_oracle(H, M, pos, npos, cost, cbb, algo="cht", rows=None):
+    rows = range(H.shape[0]) if rows is None else rows
+    for e in rows:
+        c = H[e].astype(np.int64)
+        rp, rc, rcbb = oracle.place(c, M, algo)
+        k = len(rp)
+        assert npos[e] == k, (e, npos[e], k)
+        assert pos[e, :k].tolist() == rp.tolist(), (e, pos[e, :k], rp)
+        assert (pos[e, k:] == 0).all()
+        assert cost[e] == rc, (e, cost[e], rc)
+        assert (cbb[e] == rcbb).all(), e
+
+
+def test_dp_small_exhaustive(dev):
+    """Every N <= 16, every M <= N, random sparse/dense histograms: GPU == naive oracle."""
+    for N in range(1, 17):
+        H = np.stack([wl.random_small_hist(21, N, max_count=6, zero_frac=z, key=k).numpy()
+                      for k, z in enumerate([0.0, 0.3, 0.6, 0.9] * 6)])
+        for M in range(0, N + 1):
+            pos, npos, cost, cbb = gpu_place(H, M, dev)
+            check_against_oracle(H, M, pos, npos, cost, cbb, algo="naive")
+
+
+def test_dp_w1(dev):
+    cfg = wl.CONFIGS["W1"]
+    tr = wl.make_trace(cfg, seed=0)
+    h, _ = oracle_lcp(tr, cfg.N, 1)
+    pos, npos, cost, cbb = gpu_place(h, cfg.M, dev)
+    bpos, bcost = oracle.brute_force(h[0].astype(np.int64), cfg.M)
+    assert cost[0] == bcost and pos[0, :npos[0]].tolist() == bpos.tolist()
+    check_against_oracle(h, cfg.M, pos, npos, cost, cbb, algo="naive")
+
+
+@pytest.mark.parametrize("N,M,E", [(97, 5, 33), (300, 20, 20), (1000, 8, 12), (2048, 8, 40),
+                                   (4097, 16, 10)])
+def test_dp_dense_random(dev, N, M, E):
+    cfg = wl.TraceConfig("t", E, N, M, 1, (N, N), (1, 1), "uniform", dense_n=(N // 2, 4 * N))
+    H = wl.make_dense_hist(cfg, seed=N).numpy()
+    pos, npos, cost, cbb = gpu_place(H, M, dev)
+    check_against_oracle(H, M, pos, npos, cost, cbb, algo="naive" if N <= 1000 else "cht")
+
+
+@pytest.mark.parametrize("name", ["W2", "W3"])
+def test_dp_from_lcp_traces(dev, name):
+    """W2/W3-shaped histograms from LCP traces (sparse: K <= requests/entry).  The input comes
+    from the oracle's LCP loop, never from the CUDA path."""
+    cfg = wl.scaled(wl.CONFIGS[name], 24)
+    tr = wl.make_trace(cfg, seed=6)
+    h, _ = oracle_lcp(tr, cfg.N, 24)
+    pos, npos, cost, cbb = gpu_place(h, cfg.M, dev)
+    check_against_oracle(h, cfg.M, pos, npos, cost, cbb)
+
+
+def test_dp_w4_budget_sweep_sample(dev):
+    cfg = wl.scaled(wl.CONFIGS["W4"], 64)
+    H = wl.make_dense_hist(cfg, seed=2).numpy()
+    pos, npos, cost, cbb = gpu_place(H, 64, dev)
+    check_against_oracle(H, 64, pos, npos, cost, cbb, rows=range(0, 64, 7))
+
+
+def thm1_value(N, M):
+    K = M + 1
+    q, rho = divmod(N + 1, K)
+    return (K - rho) * q * (q - 1) // 2 + rho * q * (q + 1) // 2
+
+
+def test_dp_uniform_thm1_full_size(dev):
+    """Thm 1 closed form and the F7 positions at W5's N, M (no oracle needed)."""
+    N, M = 32768, 64
+    H = wl.uniform_hist(8, N).numpy()
+    pos, npos, cost, cbb = gpu_place(H, M, dev)
+    K = M + 1
+    q, rho = divmod(N + 1, K)
+    f7 = [i * q + max(0, i - (K - rho)) for i in range(1, M + 1)]
+    for e in range(8):
+        assert cost[e] == thm1_value(N, M)
+        assert [int(x) for x in cbb[e]] == [thm1_value(N, m) for m in range(M + 1)]
+        assert npos[e] == M and pos[e].tolist() == f7
+
+
+def test_dp_w5_full_size_sampled(dev):
+    """BASELINE's scale config at full size (16384 x N=32768 x M=64) in the bench launch
+    configuration; a sample of entries checked one by one against the oracle's CHT DP."""
+    cfg = wl.CONFIGS["W5"]
+    H = wl.make_dense_hist(cfg, seed=0, device=dev)
+    pos, npos, cost, cbb = sp.place_checkpoints(H, cfg.M, cost_by_budget=True)
+    torch.cuda.synchronize()
+    pos, npos, cost, cbb = np_(pos), np_(npos), np_(cost), np_(cbb)
+    assert (npos == cfg.M).all()                      # dense histograms: every slot is used
+    rows = [0, 1, 2, 3, 4097, 8191, 12000, 16383]
+    Hs = np_(H[rows])
+    for i, e in enumerate(rows):
+        c = Hs[i].astype(np.int64)
+        rp, rc, rcbb = oracle.place(c, cfg.M, "cht")
+        assert pos[e, :npos[e]].tolist() == rp.tolist() and cost[e] == rc
+        assert (cbb[e] == rcbb).all()
+    # properties at every entry: V_m non-increasing, positions strictly increasing in [1, N]
+    assert (np.diff(cbb, axis=1) <= 0).all()
+    assert (np.diff(pos, axis=1) > 0).all() and pos.min() >= 1 and pos.max() <= cfg.N
+
+
+def test_dp_edge_cases(dev):
+    N = 50
+    H = np.zeros((8, N + 1), np.int64)
+    H[1, 50] = 5                     # point mass at N
+    H[2, 1] = 3                      # point mass at 1
+    H[3, [3, 10, 40]] = [2, 1, 7]    # K = 3 < M
+    H[4, 1:] = 1                     # uniform
+    H[5, 0] = 100                    # only misses -> like all-zero
+    H[6, 1:] = np.arange(1, N + 1)   # increasing
+    H[7, 25] = 1
+    for M in (0, 1, 4, 50):
+        pos, npos, cost, cbb = gpu_place(H, M, dev)
+        check_against_oracle(H, M, pos, npos, cost, cbb, algo="naive")
+    # N = 1
+    H1 = np.array([[0, 3], [2, 0]], np.int64)
+    for M in (0, 1):
+        pos, npos, cost, cbb = gpu_place(H1, M, dev)
+        check_against_oracle(H1, M, pos, npos, cost, cbb, algo="naive")
+
+
+def test_dp_wide_path_and_int64_weights(dev):
+    """Counts large enough that 2 n N >= 2^31 take the int64 path (still exact)."""
+    N, M, E = 3000, 12, 6
+    cfg = wl.TraceConfig("t", E, N, M, 1, (N, N), (1, 1), "uniform", dense_n=(N, 2 * N))
+    H = wl.make_dense_hist(cfg, seed=9).numpy().astype(np.int64) * 50000
+    assert (H.sum(1) * N * 2 >= 2 ** 31).all()
+    for dt in (torch.int32, torch.int64):
+        pos, npos, cost, cbb = gpu_place(H, M, dev, dtype=dt)
+        check_against_oracle(H, M, pos, npos, cost, cbb)
+    H64 = H.copy()
+    H64[0] *= 2 ** 20                 # int64 weights beyond int32
+    pos, npos, cost, cbb = gpu_place(H64, M, dev, dtype=torch.int64)
+    check_against_oracle(H64, M, pos, npos, cost, cbb, rows=[0])
+
+
+def test_dp_wide_path_large_N(dev):
+    """int64 path with N beyond the shared-memory limit (b in global/L2 scratch)."""
+    N, M, E = 32768, 8, 3
+    cfg = wl.TraceConfig("t", E, N, M, 1, (N, N), (1, 1), "mix", dense_n=(60000, 70000))
+    H = wl.make_dense_hist(cfg, seed=10).numpy()
+    assert (H.sum(1) * N * 2 >= 2 ** 31).all()
+    pos, npos, cost, cbb = gpu_place(H, M, dev)
+    check_against_oracle(H, M, pos, npos, cost, cbb)
+
+
+def test_dp_status_flags(dev):
+    N, M = 40, 3
+    H = np.ones((3, N + 1), np.int64)
+    H[1, 7] = -1                               # negative count -> BAD_ARGUMENT for that entry
+    H[2, 5] = 2 ** 62 // N                     # 2 n N >= 2^62 -> OVERFLOW for that entry
+    pos, npos, cost, cbb = gpu_place(H, M, dev, dtype=torch.int64)
+    assert npos[0] == 3
+    assert npos[1] == -sp.SP_ERR_BAD_ARGUMENT
+    assert npos[2] == -sp.SP_ERR_OVERFLOW
+    with pytest.raises(sp.SPError):
+        sp.place_checkpoints(torch.ones(2, 5, dtype=torch.int32, device=dev), 5)   # M > N
+
+
+def test_dp_workspace_too_small(dev):
+    w = torch.ones(4, 101, dtype=torch.int32, device=dev)
+    with pytest.raises(sp.SPError, match="WORKSPACE"):
+        sp.place_checkpoints(w, 4, workspace=torch.empty(16, dtype=torch.uint8, device=dev))
+
+
+# ------------------------------------------------------------------------------------------
+# a7 : fp64 variant
+# ------------------------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("N,M,E,dyadic", [(500, 7, 10, False), (2048, 8, 8, True),
+                                          (8192, 16, 4, False)])
+def test_dp_f64_relerr(dev, N, M, E, dyadic):
+    cfg = wl.TraceConfig("t", E, N, M, 1, (N, N), (1, 1), "mix",
+                         dense_n=(4096, 4096) if dyadic else (3000, 9000))
+    H = wl.make_dense_hist(cfg, seed=11).numpy().astype(np.int64)
+    n = H.sum(1, keepdims=True)
+    W = H / n
+    pos, npos, cost, cbb = gpu_place(W, M, dev, dtype=torch.float64)
+    for e in range(E):
+        _, vint, rcbb = oracle.place(H[e], M, "cht")
+        ref = vint / n[e, 0]
+        assert abs(cost[e] - ref) <= 1e-12 * ref, (e, cost[e], ref)
+        # the returned positions achieve it under the oracle's definitional fp64 walk
+        got = oracle.expected_cost_f64(W[e], pos[e, :npos[e]])
+        assert abs(got - ref) <= 1e-12 * ref
+        # DP-valued frontier V_0..V_M: looser documented bound (M N eps P_N)
+        assert np.allclose(cbb[e], rcbb / n[e, 0], rtol=0, atol=4 * M * N * 2.2e-16 * 1.0)
+
+
+def test_dp_f64_small_vs_f64_oracle(dev):
+    rng = np.random.default_rng(12)
+    W = rng.random((20, 41)) * (rng.random((20, 41)) < 0.5)
+    W[:, 0] = 0
+    pos, npos, cost, cbb = gpu_place(W, 5, dev, dtype=torch.float64)
+    for e in range(20):
+        D, O = oracle.dp_f64(W[e], 5)
+        ref = D[5, -1]
+        assert abs(cost[e] - ref) <= 1e-12 * max(ref, 1e-300) + 1e-15
+
+
+# ------------------------------------------------------------------------------------------
+# a6 : baseline evaluation
+# ------------------------------------------------------------------------------------------
+
+
+def test_expected_recompute_baselines(dev):
+    cfg = wl.scaled(wl.CONFIGS["W4"], 40)
+    H = wl.make_dense_hist(cfg, seed=13)
+    N = cfg.N
+    pos, npos, labels = sp.baseline_sets(N, budgets=range(0, 65), blocks=(64, 128), device=dev)
+    cost, worst = sp.expected_recompute(H.to(dev), pos, npos, broadcast=True)
+    torch.cuda.synchronize()
+    rc, rw = oracle.eval_batch(np_(H), np_(pos), np_(npos), broadcast=True, nthreads=8)
+    assert (np_(cost) == rc).all() and (np_(worst) == rw).all()
+    # Thm 1.2 / Table 1 tail for balanced: worst = ceil((N+1)/(M+1)) - 1
+    for i, (kind, m) in enumerate(labels):
+        if kind == "balanced":
+            assert (np_(worst)[:, i] == -(-(N + 1) // (m + 1)) - 1).all()
+
+
+def test_expected_recompute_dp_positions_and_bad_sets(dev):
+    """E[r](DP output) == V_M, per-entry (non-broadcast) sets, malformed sets flagged."""
+    cfg = wl.scaled(wl.CONFIGS["W3"], 16)
+    cfg = wl.TraceConfig(**{**cfg.__dict__, "dense_n": (2000, 5000)})
+    H = wl.make_dense_hist(cfg, seed=14).to(dev)
+    pos, npos, cost, _ = sp.place_checkpoints(H, 16)
+    E, S = 16, 2
+    P = torch.zeros(E, S, 16, dtype=torch.int32, device=dev)
+    K = torch.zeros(E, S, dtype=torch.int32, device=dev)
+    P[:, 0] = pos
+    K[:, 0] = npos
+    P[:, 1, :3] = torch.tensor([5, 5, 9], dtype=torch.int32)    # not strictly increasing
+    K[:, 1] = 3
+    c2, w2 = sp.expected_recompute(H, P, K, broadcast=False)
+    torch.cuda.synchronize()
+    assert (np_(c2)[:, 0] == np_(cost)).all()
+    assert (np_(c2)[:, 1] == -1).all() and (np_(w2)[:, 1] == -sp.SP_ERR_BAD_POSITIONS).all()
+
+
+def test_expected_recompute_f64(dev):
+    cfg = wl.scaled(wl.CONFIGS["W4"], 8)
+    H = wl.make_dense_hist(cfg, seed=15).numpy().astype(np.int64)
+    W = H / H.sum(1, keepdims=True)
+    pos, npos, _ = sp.baseline_sets(cfg.N, budgets=(1, 4, 16, 64), blocks=(64,), device=dev)
+    cost, worst = sp.expected_recompute(torch.from_numpy(W).to(dev), pos, npos)
+    torch.cuda.synchronize()
+    rc, _ = oracle.eval_batch(H.astype(np.int32), np_(pos), np_(npos), broadcast=True)
+    ref = rc / H.sum(1, keepdims=True)
+    assert np.allclose(np_(cost), ref, rtol=1e-13, atol=0)

@@ -1,0 +1,493 @@
+#!/usr/bin/env python3
+"""bench.py -- one step = one pass of the whole hot path over one batch.
+
+Per rank and step (W5 by default = BASELINE.json configs[4], 16384 entries x N=32768 x M=64 per
+GPU, weak scaling):
+  a1+a2  sp_overlap_hist   over this rank's batch of new requests (20 per entry, end-spike law);
+         the depths are merged into the resident per-entry histograms (1 GPU: accumulated in
+         place; N GPUs: (entry, depth) pairs all-gathered over NCCL and scatter-added by the
+         owner with sp_accumulate_depths, or --merge allreduce: dense int32 NCCL all-reduce)
+  a3-a5  sp_place_checkpoints on the owned histograms (dense depth-mode laws, n ~ U[8192,16384]
+         draws per entry plus the new requests), cost_by_budget for the V_0..V_M frontier
+  a6     sp_expected_recompute for the balanced (M) and block (B = 64, 128) baselines
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DP cells/s (entries*N*M)"
+UNIT = "cells/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="W5", choices=["W2", "W3", "W4", "W5"])
+    ap.add_argument("--entries", type=int, default=None, help="entries per GPU (default: config)")
+    ap.add_argument("--merge", default="sparse", choices=["sparse", "allreduce"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle wall time")
+    return ap.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+# ---------------------------------------------------------------------------------------------
+# clocks (B200_PROFILING.md "clocks DURING the timed region")
+# ---------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in out.strip().splitlines():
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------------------------
+# the CPU oracle as baseline (cpu_baseline leg and --impl reference)
+# ---------------------------------------------------------------------------------------------
+def oracle_sample_step(oracle, sample, nthreads):
+    """One oracle pass over a bounded sample: LCP loop + CHT DP + baseline evaluation."""
+    t0 = time.perf_counter()
+    hist = sample["hist"].copy()
+    oracle.lcp_hist(sample["entry_tokens"], sample["entry_off"], sample["req_tokens"],
+                    sample["req_off"], sample["req_entry"], sample["N"], n_entries=hist.shape[0],
+                    hist=hist, nthreads=nthreads)
+    t1 = time.perf_counter()
+    oracle.place_batch(hist, sample["M"], "cht", nthreads=nthreads)
+    t2 = time.perf_counter()
+    oracle.eval_batch(hist, sample["bpos"], sample["bnpos"], broadcast=True, nthreads=nthreads)
+    t3 = time.perf_counter()
+    return t3 - t0, (t1 - t0, t2 - t1, t3 - t2)
+
+
+def build_oracle_sample(args, n_entries):
+    """Host copy of a bounded sample of the workload (the generator's inputs, never CUDA
+    outputs): the first n_entries entries with their requests and dense histograms."""
+    import numpy as np
+    import torch
+    from paper_2605_05219_b200 import sp
+    from paper_2605_05219_b200 import workload as wl
+    cfg = wl.CONFIGS[args.workload]
+    scfg = wl.scaled(cfg, n_entries)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    tr = wl.make_trace(scfg, seed=args.seed, device=dev)
+    if cfg.dense_n:
+        hist = wl.make_dense_hist(scfg, seed=args.seed, device=dev)
+    else:
+        hist = torch.zeros(n_entries, cfg.N + 1, dtype=torch.int32, device=dev)
+    budgets = cfg.M_sweep if cfg.M_sweep else (cfg.M,)
+    sets = [sp_balanced(cfg.N, m) for m in budgets] + [sp_block(cfg.N, B) for B in (64, 128)]
+    width = max(len(s) for s in sets)
+    bpos = np.zeros((len(sets), width), np.int32)
+    for i, s in enumerate(sets):
+        bpos[i, :len(s)] = s
+    return dict(entry_tokens=tr["entry_tokens"].cpu().numpy(),
+                entry_off=tr["entry_off"].cpu().numpy(), req_tokens=tr["req_tokens"].cpu().numpy(),
+                req_off=tr["req_off"].cpu().numpy(), req_entry=tr["req_entry"].cpu().numpy(),
+                hist=hist.cpu().numpy(), N=cfg.N, M=cfg.M, bpos=bpos,
+                bnpos=np.array([len(s) for s in sets], np.int32), E=n_entries)
+
+
+def sp_balanced(N, M):
+    # Table 1 balanced schedule, generated on the host for the oracle sample
+    return [(i * (N + 1)) // (M + 1) for i in range(1, M + 1)]
+
+
+def sp_block(N, B):
+    return [B * i for i in range(1, N // B + 1)]
+
+
+def calibrate_sample(args, oracle, nthreads, target_s):
+    """Pick a sample size whose oracle step takes ~target_s seconds of wall time."""
+    cfg_E = (args.entries or __import__("paper_2605_05219_b200.workload",
+                                        fromlist=["CONFIGS"]).CONFIGS[args.workload].n_entries)
+    n = min(2 * nthreads, cfg_E)
+    s = build_oracle_sample(args, n)
+    dt, _ = oracle_sample_step(oracle, s, nthreads)
+    n2 = int(min(cfg_E, max(n, n * target_s / max(dt, 1e-3))))
+    n2 = max(nthreads, (n2 // nthreads) * nthreads) if n2 >= nthreads else n2
+    if n2 != n:
+        s = build_oracle_sample(args, n2)
+    return s
+
+
+def cpu_baseline(args, nthreads):
+    import oracle
+    oracle.build()
+    s = calibrate_sample(args, oracle, nthreads, args.cpu_seconds)
+    dt, parts = oracle_sample_step(oracle, s, nthreads)
+    cells = s["E"] * s["N"] * s["M"]
+    return {"value": cells / dt, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+            "sample": (f"first {s['E']} entries of {args.workload} (full N={s['N']}, M={s['M']}, "
+                       f"their {len(s['req_off']) - 1} requests): literal LCP loop + paper's "
+                       f"CHT DP (int64/__int128) + definitional baseline evaluation, "
+                       f"{nthreads} pthreads"),
+            "seconds": dt, "seconds_lcp_dp_eval": parts}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (the tier's reference arm) on the host cores."""
+    world, rank, _ = env_rank()
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    nthreads = os.cpu_count() or 1
+    per_step = max(2.0, min(20.0, 150.0 / max(args.steps + args.warmup, 1)))
+    s = calibrate_sample(args, oracle, nthreads, per_step)
+    for _ in range(args.warmup):
+        oracle_sample_step(oracle, s, nthreads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_sample_step(oracle, s, nthreads)
+    dt = time.perf_counter() - t0
+    cells = s["E"] * s["N"] * s["M"] * args.steps
+    v = cells / dt
+    cfg = workload_config(args, 1, None)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads, "kind": "oracle",
+                             "sample": f"first {s['E']} entries of {args.workload} per step"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world, extra):
+    from paper_2605_05219_b200 import workload as wl
+    cfg = wl.CONFIGS[args.workload]
+    E = args.entries or cfg.n_entries
+    d = {"workload": f"{args.workload}: {E} entries/GPU x N={cfg.N} x M={cfg.M}",
+         "entries_per_gpu": E, "entries_total": E * world, "N": cfg.N, "M": cfg.M,
+         "requests_per_entry": cfg.req_per_entry, "lcp_law": cfg.shape,
+         "dp_hist": (f"dense depth-mode, n~U{list(cfg.dense_n)} draws/entry, {cfg.dense_shape} "
+                     f"laws, + the step's requests" if cfg.dense_n else "from the LCP requests"),
+         "parallelism": f"entries sharded over {world} GPU(s)",
+         "merge": None if world == 1 else args.merge,
+         "l2": "inputs larger than L2 (request tokens and histograms >> 126 MB)"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ---------------------------------------------------------------------------------------------
+# the GPU arm
+# ---------------------------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_05219_b200 import build as bld
+    from paper_2605_05219_b200 import sp
+    from paper_2605_05219_b200 import workload as wl
+
+    world, rank, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        bld.build()
+    if world > 1:
+        dist.barrier()
+    sp.lib()
+
+    cfg = wl.CONFIGS[args.workload]
+    E_own = args.entries or cfg.n_entries
+    E_tot = E_own * world
+    e0, e1 = rank * E_own, (rank + 1) * E_own
+    N, M = cfg.N, cfg.M
+    tcfg = wl.scaled(cfg, E_tot)
+
+    # ---- inputs (resident in HBM before timing) ------------------------------------------------
+    tr = wl.make_trace(tcfg, seed=args.seed, device=dev, world=world, rank=rank)
+    R = tr["req_off"].numel() - 1
+    if cfg.dense_n:
+        hist = wl.make_dense_hist(tcfg, seed=args.seed, device=dev, entry_begin=e0,
+                                  n_entries=E_own)
+    else:
+        hist = torch.zeros(E_own, N + 1, dtype=torch.int32, device=dev)
+    budgets = cfg.M_sweep if cfg.M_sweep else (M,)
+    bpos, bnpos, labels = sp.baseline_sets(N, budgets=budgets, blocks=(64, 128), device=dev)
+    S = bpos.shape[0]
+    positions = torch.empty(E_own, M, dtype=torch.int32, device=dev)
+    npos = torch.empty(E_own, dtype=torch.int32, device=dev)
+    cost = torch.empty(E_own, dtype=torch.int64, device=dev)
+    cbb = torch.empty(E_own, M + 1, dtype=torch.int64, device=dev)
+    bcost = torch.empty(E_own, S, dtype=torch.int64, device=dev)
+    bworst = torch.empty(E_own, S, dtype=torch.int32, device=dev)
+    ws = torch.empty(sp.place_checkpoints_workspace_bytes(E_own, N, M), dtype=torch.uint8,
+                     device=dev)
+
+    # tokens examined by the LCP (generator depths): sum min(t+1, len, L_e)
+    d = torch.minimum(tr["depth"].to(torch.int64), torch.tensor(N, device=dev))
+    rlen = tr["req_off"][1:] - tr["req_off"][:-1]
+    Le = tr["L"][tr["req_entry"].long()]
+    lim = torch.minimum(torch.minimum(rlen, Le), torch.tensor(N, device=dev))
+    examined = torch.minimum(d + 1, lim)
+    tokens_examined = int(examined.sum())
+    # algorithmic HBM bytes of the LCP kernel: request + entry tokens examined (entry tokens
+    # once per entry: max over its requests), offsets/ids, one histogram update per request
+    ent_max = torch.zeros(E_tot, dtype=torch.int64, device=dev)
+    ent_max.scatter_reduce_(0, tr["req_entry"].long(), examined, reduce="amax")
+    lcp_bytes = 4 * tokens_examined + 4 * int(ent_max.sum()) + R * (4 + 16 + 16 + 4 + 4)
+
+    lcp = torch.full((max(R, 1),), -1, dtype=torch.int32, device=dev)
+    if world > 1:
+        Rmax_t = torch.tensor([R], device=dev)
+        dist.all_reduce(Rmax_t, op=dist.ReduceOp.MAX)
+        Rmax = int(Rmax_t)
+        ent_pad = torch.full((Rmax,), -1, dtype=torch.int32, device=dev)
+        ent_pad[:R] = tr["req_entry"]
+        lcp_pad = torch.full((Rmax,), -1, dtype=torch.int32, device=dev)
+        g_ent = torch.empty(world * Rmax, dtype=torch.int32, device=dev)
+        g_lcp = torch.empty(world * Rmax, dtype=torch.int32, device=dev)
+        dist.all_gather_into_tensor(g_ent, ent_pad)
+        if args.merge == "allreduce":
+            partial = torch.zeros(E_tot, N + 1, dtype=torch.int32, device=dev)
+
+    stream = torch.cuda.current_stream(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    req_tokens, req_off, req_entry = tr["req_tokens"], tr["req_off"], tr["req_entry"]
+
+    def step(marks=None):
+        if marks:
+            marks[0].record(stream)
+        # a1 + a2
+        if world == 1:
+            sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], req_tokens, req_off, req_entry,
+                            N, hist=hist, lcp_out=lcp, n_entries=E_tot, stream=stream)
+        elif args.merge == "sparse":
+            sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], req_tokens, req_off, req_entry,
+                            N, lcp_out=lcp_pad, n_entries=E_tot, stream=stream, with_hist=False)
+        else:
+            partial.zero_()
+            sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], req_tokens, req_off, req_entry,
+                            N, hist=partial, lcp_out=lcp, n_entries=E_tot, stream=stream)
+        if marks:
+            marks[1].record(stream)
+        # merge (the one exchange step)
+        if world > 1:
+            if args.merge == "sparse":
+                dist.all_gather_into_tensor(g_lcp, lcp_pad)
+                sp.accumulate_depths(g_ent, g_lcp, e0, e1, N, hist, stream=stream)
+            else:
+                dist.all_reduce(partial)
+                hist.add_(partial[e0:e1])
+        if marks:
+            marks[2].record(stream)
+        # a3 - a5
+        sp.place_checkpoints(hist, M, positions=positions, n_positions=npos, cost=cost,
+                             cost_by_budget=cbb, workspace=ws, stream=stream)
+        if marks:
+            marks[3].record(stream)
+        # a6
+        sp.expected_recompute(hist, bpos, bnpos, broadcast=True, cost=bcost, worst=bworst,
+                              stream=stream)
+        if marks:
+            marks[4].record(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- warm-up ---------------------------------------------------------------------------
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stats = sp.dp_stats(ws)
+    assert (npos >= 0).all(), "DP flagged an entry (negative n_positions)"
+
+    # ---- timed region (device-resident inputs) -----------------------------------------------
+    marks = [[ev() for _ in range(5)] for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t_start, t_end = ev(), ev()
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(marks[k])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = t_start.elapsed_time(t_end)
+    stage = np.array([[marks[k][i].elapsed_time(marks[k][i + 1]) for i in range(4)]
+                      for k in range(args.steps)])          # lcp, merge, dp, eval (ms)
+    t = torch.tensor([ms] + list(stage.sum(0)), dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, lcp_ms, merge_ms, dp_ms, eval_ms = [float(x) for x in t.cpu()]
+
+    # ---- e2e: through the C ABI with the step's inputs in pinned HOST memory -----------------
+    e2e = None
+    if not args.no_e2e:
+        h_tok = torch.empty(req_tokens.shape, dtype=torch.int32, pin_memory=True)
+        h_tok.copy_(req_tokens)
+        h_off = req_off.cpu().pin_memory()
+        h_ent = req_entry.cpu().pin_memory()
+        o_pos = torch.empty(positions.shape, dtype=torch.int32, pin_memory=True)
+        o_npos = torch.empty(npos.shape, dtype=torch.int32, pin_memory=True)
+        o_cost = torch.empty(cost.shape, dtype=torch.int64, pin_memory=True)
+        o_bcost = torch.empty(bcost.shape, dtype=torch.int64, pin_memory=True)
+        o_cbb = torch.empty(cbb.shape, dtype=torch.int64, pin_memory=True)
+        bi = (h_tok.numel() * 4 + h_off.numel() * 8 + h_ent.numel() * 4)
+        bo = (o_pos.numel() * 4 + o_npos.numel() * 4 + o_cost.numel() * 8 + o_bcost.numel() * 8
+              + o_cbb.numel() * 8)
+
+        def e2e_step():
+            req_tokens.copy_(h_tok, non_blocking=True)
+            req_off.copy_(h_off, non_blocking=True)
+            req_entry.copy_(h_ent, non_blocking=True)
+            step()
+            o_pos.copy_(positions, non_blocking=True)
+            o_npos.copy_(npos, non_blocking=True)
+            o_cost.copy_(cost, non_blocking=True)
+            o_bcost.copy_(bcost, non_blocking=True)
+            o_cbb.copy_(cbb, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        a, b = ev(), ev()
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e_ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_ms = float(e_ms)
+        e2e = {"value": E_tot * N * M * args.steps / (e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": bi * world, "d2h_bytes_per_step": bo * world,
+               "ms_per_step": e_ms / args.steps}
+
+    # ---- numbers -------------------------------------------------------------------------
+    tok_all = torch.tensor([tokens_examined, lcp_bytes], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tok_all)
+    tokens_all, lcp_bytes_all = [float(x) for x in tok_all.cpu()]
+    K = args.steps
+    value = E_tot * N * M * K / (ms_max / 1e3)
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    # DP roofline: INT-ALU pipe bound (min-plus, no tensor cores).  One candidate evaluation
+    # v = b_s - s P_j with a leftmost-argmin update is 1 IMAD (FMA pipe) + 3 ALU-pipe ops
+    # (ISETP + 2 SEL); the ALU pipe issues 64 lanes/clk/SM (16/clk/SMSP) => peak
+    # = SMs * f_max * 64 / 3 evaluations/s.
+    evals_per_launch = stats["evaluations"]          # exact, from the kernel's own counter
+    dp_launch_s = dp_ms / K / 1e3
+    achieved = evals_per_launch / dp_launch_s / 1e9
+    peak = sms * sm_max * 1e6 * 64 / 3 / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32-exact (int64 costs)",
+        "data": "synthetic (seeded; SURVEY 8(d) recipe)",
+        "config": workload_config(args, world, None),
+        "lcp_tokens_per_s": tokens_all * K / (lcp_ms / 1e3),
+        "stage_ms_per_step": {"lcp_hist": lcp_ms / K, "merge": merge_ms / K, "dp": dp_ms / K,
+                              "eval": eval_ms / K},
+        "roofline": {"bound": "alu", "kernel": "dp_place_kernel", "achieved": achieved,
+                     "peak": peak, "unit": "Geval/s", "frac": achieved / peak,
+                     "traffic": None,
+                     "work": f"{evals_per_launch} candidate evaluations per launch "
+                             f"({evals_per_launch / (E_own * N * M):.2f} per DP cell)",
+                     "peak_basis": f"{sms} SMs x {sm_max:.0f} MHz x 64 ALU lanes / 3 ops"},
+        "roofline_lcp": {"bound": "hbm", "kernel": "lcp_hist_kernel",
+                         "achieved": lcp_bytes_all * K / (lcp_ms / 1e3) / 1e9 / world,
+                         "peak": hbm_peak, "unit": "GB/s",
+                         "frac": lcp_bytes_all * K / (lcp_ms / 1e3) / 1e9 / world / hbm_peak,
+                         "traffic": None},
+        "dp_paths": {k: v for k, v in stats.items() if k != "evaluations"},
+        "gpu_launches": K * (3 + (1 if world > 1 and args.merge == "sparse" else 0)),
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, os.cpu_count() or 1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -66,6 +66,8 @@ typedef enum {
  *     t_r = min(LCP(request, entry), N)          (depths beyond N clamp to N)
  *     hist[e][t_r] += 1                          (ACCUMULATED: the caller zeroes hist)
  *     lcp_out[r] = t_r                           (if lcp_out != NULL)
+ * hist may be NULL when lcp_out is not (depths only, e.g. to ship (entry, depth) pairs to the
+ * entry's owner rank and merge there with sp_accumulate_depths).
  * Offsets are int64 token indices; rows with offsets that are multiples of 4 tokens take the
  * 16-byte vector path, others a scalar path (same result).  Precondition (checked only by
  * debug builds): 0 <= req_entry[r] < n_entries; requests with an out-of-range entry are
@@ -100,12 +102,24 @@ sp_status sp_accumulate_depths(const int32_t* entry, const int32_t* depth, int64
  *   cost           [E]: V_M = dp[M][N] = n * E[r] -- int64 for count types, double for F64
  *   cost_by_budget [E][M+1] V_0..V_M (same type as cost; V_0 = T_N = n * R_nc), or
  *                  NULL.  (The DP computes every budget m <= M on the way.)
- *   workspace      device scratch of >= sp_place_checkpoints_workspace_bytes(E, N, M) bytes
+ *   workspace      device scratch of >= sp_place_checkpoints_workspace_bytes(E, N, M) bytes.
+ *                  Its first SP_WS_STATS_BYTES bytes receive launch statistics
+ *                  (sp_dp_stats, see below); the rest is scratch.
  * M = 0 gives n_positions = 0 and cost = T_N.  An all-zero histogram gives 0 positions, cost 0.
  * Errors (synchronous): BAD_LENGTH (N < 1, N > SP_MAX_N, E < 0), BUDGET_TOO_LARGE (M < 0 or
  * M > N), BAD_ARGUMENT (NULL pointer, bad wtype), WORKSPACE, CUDA.
  * ---------------------------------------------------------------------------------------- */
 size_t sp_place_checkpoints_workspace_bytes(int32_t n_entries, int32_t N, int32_t M);
+
+/* Launch statistics written (stream-ordered) at the start of the workspace by every
+ * sp_place_checkpoints call: the exact number of candidate evaluations b_s - s P_j the
+ * divide-and-conquer performed (the DP's executed work; cells = E N M), and the entries solved
+ * on the exact-int32 / int64 / fp64 paths. */
+#define SP_WS_STATS_BYTES 256
+typedef struct {
+  unsigned long long evaluations;
+  unsigned long long entries_i32, entries_i64, entries_f64;
+} sp_dp_stats;
 
 sp_status sp_place_checkpoints(const void* weights, sp_weight_type wtype, int32_t n_entries,
                                int32_t N, int32_t M, int32_t* positions, int32_t* n_positions,

@@ -28,7 +28,11 @@ namespace sp {
 
 constexpr int DP_NT = 512;
 constexpr int DP_NW = DP_NT / 32;
-constexpr int DP_TPL = 8;   // target candidate evaluations per thread per row
+constexpr int T_INLINE = 8;   // rows with at most this many candidates: one thread solves it
+constexpr int PS = 32;        // candidates per piece of a queued (long) row
+constexpr int QMAX = 512;     // queued rows per level
+constexpr int PMAX = 2048;    // pieces per level
+constexpr int RB = 4;         // rows per thread per batch in the bracket pass
 
 // ------------------------------------------------------------------------------------------
 // value-type traits
@@ -96,9 +100,14 @@ __device__ __forceinline__ dd dd_shfl_xor(dd v, int o) {
 
 __host__ __device__ __forceinline__ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// workspace slot layout (bytes): P 8B[N+1] | bA 8B[N+1] | bB 8B[N+1] | opt uint16[M][N+1]
+// workspace slot layout (bytes):
+//   P 8B[N+1] | bA 8B[N+1] | bB 8B[N+1] | opt uint16[M][N+1] | P32 int32[N+1]
+__host__ __device__ __forceinline__ size_t slot_opt_off(int N) { return 3 * align256(8 * (size_t)(N + 1)); }
+__host__ __device__ __forceinline__ size_t slot_p32_off(int N, int M) {
+  return slot_opt_off(N) + align256(2 * (size_t)(M > 0 ? M : 1) * (N + 1));
+}
 __host__ __device__ __forceinline__ size_t slot_bytes(int N, int M) {
-  return 3 * align256(8 * (size_t)(N + 1)) + align256(2 * (size_t)(M > 0 ? M : 1) * (N + 1));
+  return slot_p32_off(N, M) + align256(4 * (size_t)(N + 1));
 }
 
 struct DpParams {
@@ -114,10 +123,13 @@ struct DpParams {
 };
 
 struct Shared {
+  uint64_t mbar;                  // TMA bulk-copy completion barrier
+  unsigned long long ctr[3];      // per-level queue counters (triple-buffered)
+  unsigned long long evals;
   int64_t wbuf[DP_NW + 1];
   double dbuf[2 * (DP_NW + 1)];
-  int64_t red_v[DP_NW];
   int32_t red_s[DP_NW];
+  unsigned phase;
   int err;
 };
 
@@ -137,10 +149,35 @@ struct LayerCtx {
   int* err;
 };
 
-__device__ __forceinline__ unsigned group_mask(int G) {
-  if (G >= 32) return FULL;
-  const unsigned base = (threadIdx.x & 31) & ~(unsigned)(G - 1);
-  return ((1u << G) - 1) << base;
+// scratch for the long-row queue of one level, carved from dynamic shared memory
+template <typename VT>
+struct Scratch {
+  int* qj;     // [QMAX] row j
+  int* qlo;    // [QMAX] bracket low end
+  int* qlen;   // [QMAX] bracket length (0 = dead entry)
+  int* qpb;    // [QMAX] first piece
+  VT* qP;      // [QMAX] P_j
+  VT* pv;      // [PMAX] piece minima
+  int* ps;     // [PMAX] piece argmins
+};
+
+template <typename VT>
+__host__ __device__ __forceinline__ size_t scratch_bytes() {
+  return align256((size_t)QMAX * (16 + sizeof(VT))) + align256((size_t)PMAX * (4 + sizeof(VT)));
+}
+
+template <typename VT>
+__device__ __forceinline__ Scratch<VT> carve(uint8_t* base) {
+  Scratch<VT> S;
+  S.qj = reinterpret_cast<int*>(base);
+  S.qlo = S.qj + QMAX;
+  S.qlen = S.qlo + QMAX;
+  S.qpb = S.qlen + QMAX;
+  S.qP = reinterpret_cast<VT*>(S.qpb + QMAX);
+  uint8_t* b2 = base + align256((size_t)QMAX * (16 + sizeof(VT)));
+  S.pv = reinterpret_cast<VT*>(b2);
+  S.ps = reinterpret_cast<int*>(S.pv + PMAX);
+  return S;
 }
 
 template <typename VT>
@@ -151,31 +188,45 @@ __device__ __forceinline__ void lex_min(VT& bv, int& bs, VT ov, int os) {
   }
 }
 
-// bracket of row j at the level with half-spacing h
-template <typename Ctx>
-__device__ __forceinline__ void row_bracket(const Ctx& c, int j, int h, int& lo, int& hi) {
-  lo = 1;
-  hi = j;
-  const int jl = j - h, jr = j + h;
-  if (jl >= 1) lo = c.sopt[jl];
-  if (jr <= c.N) hi = min((int)c.sopt[jr], j);
-  if (c.optprev) lo = max(lo, (int)c.optprev[j]);
-}
-
-// per-thread scan of candidates s = lo + t, lo + t + G, ... <= hi (s increasing: strict '<'
-// keeps the lowest index within the thread)
 template <typename VT>
-__device__ __forceinline__ void scan_candidates(const VT* __restrict__ b, VT Pj, int lo, int hi,
-                                                int t, int G, VT& bv, int& bs) {
-  int s = lo + t;
-#pragma unroll 4
-  for (; s <= hi; s += G) {
-    const VT v = cand(b[s], s, Pj);
-    if (v < bv) {
-      bv = v;
-      bs = s;
+__device__ __forceinline__ VT vmin(VT a, VT b) { return a < b ? a : b; }
+
+// Leftmost argmin of b_s - s P_j over s = s0, s0 + st, ... <= s1 (s increasing).  The main loop
+// takes groups of four: the group minimum (2 min instructions for int32: VIMNMX + VIMNMX3)
+// replaces the running minimum only when strictly smaller, so the first group holding the
+// minimum wins; its lowest candidate equal to the minimum is recovered afterwards.
+template <typename VT>
+__device__ __forceinline__ void eval_range(const VT* __restrict__ b, VT Pj, int s0, int s1,
+                                           int st, VT& bv, int& bs) {
+  VT best = Lim<VT>::inf();
+  int bg = -1;
+  int s = s0;
+  for (; s + 3 * st <= s1; s += 4 * st) {
+    const VT v0 = cand(b[s], s, Pj);
+    const VT v1 = cand(b[s + st], s + st, Pj);
+    const VT v2 = cand(b[s + 2 * st], s + 2 * st, Pj);
+    const VT v3 = cand(b[s + 3 * st], s + 3 * st, Pj);
+    const VT m = vmin(vmin(v0, v1), vmin(v2, v3));
+    if (m < best) {
+      best = m;
+      bg = s;
     }
   }
+  int arg = INT_MAX;
+  if (bg >= 0) {
+#pragma unroll
+    for (int k = 3; k >= 0; --k)
+      if (cand(b[bg + k * st], bg + k * st, Pj) == best) arg = bg + k * st;
+  }
+  for (; s <= s1; s += st) {
+    const VT v = cand(b[s], s, Pj);
+    if (v < best) {
+      best = v;
+      arg = s;
+    }
+  }
+  bv = best;
+  bs = arg;
 }
 
 template <typename VT, typename Ctx>
@@ -197,135 +248,164 @@ __device__ __forceinline__ void row_write(const Ctx& c, int j, int lo, int hi, V
 }
 
 // fp64: rounding can make neighbouring brackets cross by a hair; clamp instead of flagging
-template <typename Ctx>
-__device__ __forceinline__ void fix_bracket(const Ctx&, double*, int& lo, int hi) {
+__device__ __forceinline__ void fix_bracket(double*, int& lo, int hi) {
   if (lo > hi) lo = hi;
 }
-template <typename Ctx, typename VT>
-__device__ __forceinline__ void fix_bracket(const Ctx&, VT*, int&, int) {}
+template <typename VT>
+__device__ __forceinline__ void fix_bracket(VT*, int&, int) {}
 
-// one level, groups of G <= 32 threads per row (rows strided over groups)
-template <typename VT, int G, typename Ctx>
-__device__ void level_small(const Ctx& c, int h, int R) {
-  const int gid = threadIdx.x / G, t = threadIdx.x % G;
-  constexpr int NG = DP_NT / G;
-  const unsigned gmask = group_mask(G);
-  for (int i = gid; i < R; i += NG) {
-    const int j = h * (2 * i + 1);
-    int lo, hi;
-    row_bracket(c, j, h, lo, hi);
-    fix_bracket(c, (VT*)nullptr, lo, hi);
-    const VT Pj = (VT)c.P[j];
-    VT bv = Lim<VT>::inf();
-    int bs = INT_MAX;
-    scan_candidates(c.b, Pj, lo, hi, t, G, bv, bs);
+// One D&C level: every row j = h(2i+1) <= N, i < R.
+//  phase 1  each thread takes rows i = tid + u NT, loads their brackets and P_j in batches of
+//           RB (independent loads in flight), solves rows with <= T_INLINE candidates itself and
+//           queues the longer ones, reserving ceil(len / PS) pieces with one 64-bit atomic
+//           (queue index and piece base in one word, so queue order == piece order);
+//  phase 2  threads take pieces p = tid + k NT; piece k of a row scans s = lo + k + i np
+//           (interleaved so that neighbouring lanes read neighbouring words of b);
+//  phase 3  one warp per queued row reduces its pieces (lexicographic (value, index) min) and
+//           writes the row.
+// Returns after its last barrier; the caller adds none.
+template <typename VT, typename Ctx>
+__device__ void run_level(const Ctx& c, Shared& sh, const Scratch<VT>& S, int h, int R,
+                          int lvl, unsigned long long& nev) {
+  unsigned long long* ctr = &sh.ctr[lvl % 3];
+  if (threadIdx.x == 0) sh.ctr[(lvl + 1) % 3] = 0;   // last used two levels ago
+  const int N = c.N;
+  const bool optN = (N % (2 * h)) == 0;               // row N solved at an earlier level
+  for (int i0 = threadIdx.x; i0 < R; i0 += DP_NT * RB) {
+    int jj[RB], lo[RB], hi[RB];
+    VT Pj[RB];
 #pragma unroll
-    for (int o = G / 2; o >= 1; o >>= 1) {
-      const VT ov = __shfl_xor_sync(gmask, bv, o);
-      const int os = __shfl_xor_sync(gmask, bs, o);
-      lex_min(bv, bs, ov, os);
+    for (int u = 0; u < RB; ++u) {
+      const int i = i0 + u * DP_NT;
+      jj[u] = 0;
+      lo[u] = 1;
+      hi[u] = 0;
+      Pj[u] = 0;
+      if (i < R) {
+        const int j = h * (2 * i + 1);
+        int l = 1, r = j;
+        if (j - h >= 1) l = c.sopt[j - h];
+        if (j + h <= N) r = min((int)c.sopt[j + h], j);
+        else if (optN) r = min((int)c.sopt[N], j);
+        if (c.optprev) l = max(l, (int)c.optprev[j]);
+        jj[u] = j;
+        lo[u] = l;
+        hi[u] = r;
+        Pj[u] = (VT)c.P[j];
+      }
     }
-    if (t == 0) row_write(c, j, lo, hi, Pj, bv, bs);
+#pragma unroll
+    for (int u = 0; u < RB; ++u) {
+      if (jj[u] == 0) continue;
+      const int j = jj[u];
+      int l = lo[u];
+      const int r = hi[u];
+      fix_bracket((VT*)nullptr, l, r);
+      const int len = r - l + 1;
+      if (len > 0) nev += (unsigned)len;
+      if (len > T_INLINE) {
+        const int np = (len + PS - 1) / PS;
+        const unsigned long long old = atomicAdd(ctr, (1ull << 32) | (unsigned long long)np);
+        const int q = (int)(old >> 32), pb = (int)(old & 0xffffffffu);
+        if (q < QMAX) {
+          const bool fits = pb + np <= PMAX;
+          S.qj[q] = j;
+          S.qlo[q] = l;
+          S.qlen[q] = fits ? len : 0;   // a dead entry keeps the piece order intact
+          S.qpb[q] = pb;
+          S.qP[q] = Pj[u];
+          if (fits) continue;
+        }
+        // no room: solve it here (correct, just slower)
+      }
+      VT bv;
+      int bs;
+      eval_range(c.b, Pj[u], l, r, 1, bv, bs);
+      row_write(c, j, l, r, Pj[u], bv, bs);
+    }
   }
-}
-
-// one level, groups of G > 32 threads (several warps) per row; uniform trip count so that
-// __syncthreads can be used for the cross-warp reduction
-template <typename VT, int G, typename Ctx>
-__device__ void level_big(const Ctx& c, Shared& sh, int h, int R) {
-  const int gid = threadIdx.x / G, t = threadIdx.x % G;
-  constexpr int NG = DP_NT / G, WPG = G / 32;
-  const int iters = (R + NG - 1) / NG;
-  for (int it = 0; it < iters; ++it) {
-    const int i = it * NG + gid;
-    const bool valid = i < R;
-    int lo = 1, hi = 0, j = 1;
-    VT Pj = 0;
+  __syncthreads();   // B1: inline rows written, queue complete
+  const unsigned long long tot = *ctr;
+  const int Q = min((int)(tot >> 32), QMAX);
+  const int NP = min((int)(tot & 0xffffffffu), PMAX);
+  if (Q == 0) return;
+  for (int p = threadIdx.x; p < NP; p += DP_NT) {
+    int a = 0, z = Q - 1;   // last queue entry with qpb <= p
+    while (a < z) {
+      const int mid = (a + z + 1) >> 1;
+      if (S.qpb[mid] <= p) a = mid; else z = mid - 1;
+    }
+    const int len = S.qlen[a];
+    const int np = (len + PS - 1) / PS;
+    const int k = p - S.qpb[a];
     VT bv = Lim<VT>::inf();
     int bs = INT_MAX;
-    if (valid) {
-      j = h * (2 * i + 1);
-      row_bracket(c, j, h, lo, hi);
-      fix_bracket(c, (VT*)nullptr, lo, hi);
-      Pj = (VT)c.P[j];
-      scan_candidates(c.b, Pj, lo, hi, t, G, bv, bs);
-    }
+    if (k < np) eval_range(c.b, S.qP[a], S.qlo[a] + k, S.qlo[a] + len - 1, np, bv, bs);
+    S.pv[p] = bv;
+    S.ps[p] = bs;
+  }
+  __syncthreads();   // B2: piece minima written
+  const int lane = lane_id();
+  for (int q = warp_id(); q < Q; q += DP_NW) {
+    const int len = S.qlen[q];
+    if (len == 0) continue;
+    const int np = (len + PS - 1) / PS, pb = S.qpb[q];
+    VT bv = Lim<VT>::inf();
+    int bs = INT_MAX;
+    for (int k = lane; k < np; k += 32) lex_min(bv, bs, S.pv[pb + k], S.ps[pb + k]);
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
       const VT ov = __shfl_xor_sync(FULL, bv, o);
       const int os = __shfl_xor_sync(FULL, bs, o);
       lex_min(bv, bs, ov, os);
     }
-    if (lane_id() == 0) {
-      // stored through the int64 buffer (doubles by bit pattern)
-      if constexpr (sizeof(VT) == 8) {
-        sh.red_v[warp_id()] = *reinterpret_cast<const int64_t*>(&bv);
-      } else {
-        sh.red_v[warp_id()] = (int64_t)bv;
-      }
-      sh.red_s[warp_id()] = bs;
-    }
-    __syncthreads();
-    if (valid && t == 0) {
-      for (int q = 1; q < WPG; ++q) {
-        VT ov;
-        if constexpr (sizeof(VT) == 8) {
-          ov = *reinterpret_cast<const VT*>(&sh.red_v[warp_id() + q]);
-        } else {
-          ov = (VT)sh.red_v[warp_id() + q];
-        }
-        lex_min(bv, bs, ov, sh.red_s[warp_id() + q]);
-      }
-      row_write(c, j, lo, hi, Pj, bv, bs);
-    }
-    __syncthreads();
+    if (lane == 0) row_write(c, S.qj[q], S.qlo[q], S.qlo[q] + len - 1, S.qP[q], bv, bs);
   }
+  __syncthreads();   // B3: queued rows written
 }
 
-template <typename VT, typename Ctx>
-__device__ void run_level(const Ctx& c, Shared& sh, int h, int R) {
-  // expected bracket width ~ 2h; aim at DP_TPL evaluations per thread, but use every thread
-  int G = 1;
-  const int want = (2 * h) / DP_TPL;
-  while (G * 2 <= want && G < DP_NT) G *= 2;
-  int rp = 1;
-  while (rp < R) rp *= 2;
-  const int need = DP_NT / rp;   // 0 when R > DP_NT
-  if (G < need) G = need;
-  switch (G) {
-    case 1: level_small<VT, 1>(c, h, R); break;
-    case 2: level_small<VT, 2>(c, h, R); break;
-    case 4: level_small<VT, 4>(c, h, R); break;
-    case 8: level_small<VT, 8>(c, h, R); break;
-    case 16: level_small<VT, 16>(c, h, R); break;
-    case 32: level_small<VT, 32>(c, h, R); break;
-    case 64: level_big<VT, 64>(c, sh, h, R); break;
-    case 128: level_big<VT, 128>(c, sh, h, R); break;
-    case 256: level_big<VT, 256>(c, sh, h, R); break;
-    default: level_big<VT, 512>(c, sh, h, R); break;
+// ---- TMA bulk copy global -> shared (cp.async.bulk, completion on an mbarrier) ---------------
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, unsigned bytes,
+                                         uint64_t* mbar, unsigned& phase) {
+  const unsigned mb = (unsigned)__cvta_generic_to_shared(mbar);
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+                 : "memory");
+    const unsigned sd = (unsigned)__cvta_generic_to_shared(smem_dst);
+    for (unsigned off = 0; off < bytes; off += 32768u) {
+      const unsigned n = min(32768u, bytes - off);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+          "[%3];" ::"r"(sd + off),
+          "l"((const char*)gmem_src + off), "r"(n), "r"(mb)
+          : "memory");
+    }
   }
-}
-
-template <typename PT>
-__device__ __forceinline__ uint8_t* slot_of(const DpParams& p) {
-  return p.ws + (size_t)blockIdx.x * p.slot;
+  asm volatile(
+      "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; "
+      "@!p bra WAIT_%=; }" ::"r"(mb),
+      "r"(phase)
+      : "memory");
+  phase ^= 1u;
 }
 
 // Solve one entry with value type VT; b in shared memory (BS) or in the slot's global arrays.
 template <typename VT, bool BS, typename PT, typename CT>
-__device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t* sopt, int e,
-                            CT TN) {
+__device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t* sopt,
+                            uint8_t* scratch, int e, CT TN, const PT* P, unsigned& phase) {
   const int N = p.N, M = p.M;
-  uint8_t* slot = p.ws + (size_t)blockIdx.x * p.slot;
-  const PT* P = reinterpret_cast<const PT*>(slot);
+  uint8_t* slot = p.ws + SP_WS_STATS_BYTES + (size_t)blockIdx.x * p.slot;
   VT* bA = reinterpret_cast<VT*>(slot + align256(8 * (size_t)(N + 1)));
   VT* bB = reinterpret_cast<VT*>(slot + 2 * align256(8 * (size_t)(N + 1)));
-  uint16_t* opt = reinterpret_cast<uint16_t*>(slot + 3 * align256(8 * (size_t)(N + 1)));
+  uint16_t* opt = reinterpret_cast<uint16_t*>(slot + slot_opt_off(N));
+  const Scratch<VT> S = carve<VT>(scratch);
 
   VT* b = BS ? smem_b : bA;
   VT* bnext = bB;
   // layer 1: e_0 == 0 => b_s = s P_{s-1}
   for (int s = threadIdx.x + 1; s <= N; s += DP_NT) b[s] = icpt((VT)0, s, (VT)P[s - 1]);
+  if (threadIdx.x < 3) sh.ctr[threadIdx.x] = 0;
   __syncthreads();
 
   LayerCtx<VT, PT, CT> c;
@@ -336,6 +416,8 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
   c.cbb_e = p.cbb ? reinterpret_cast<CT*>(p.cbb) + (int64_t)e * (M + 1) : nullptr;
   c.cost_e = reinterpret_cast<CT*>(p.cost) + e;
   c.err = &sh.err;
+  unsigned long long nev = 0;
+  int lvl = 0;
   for (int m = 1; m <= M; ++m) {
     c.b = b;
     c.bnext = bnext;
@@ -343,18 +425,17 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
     c.last = (m == M);
     c.optout = opt + (size_t)(m - 1) * (N + 1);
     c.optprev = m >= 2 ? opt + (size_t)(m - 2) * (N + 1) : nullptr;
-    for (int k = 0; k < p.L; ++k) {
+    for (int k = 0; k < p.L; ++k, ++lvl) {
       const int h = 1 << (p.L - 1 - k);
       const int R = ((N / h) + 1) >> 1;
-      run_level<VT>(c, sh, h, R);
-      __syncthreads();
+      run_level<VT>(c, sh, S, h, R, lvl, nev);
     }
     if (m < M) {
-      if (BS) {
-        for (int s = threadIdx.x + 2; s <= N; s += DP_NT) b[s] = bnext[s];
-        if (threadIdx.x == 0) b[1] = 0;   // e_m(0) + 1 * P_0 = 0
+      if (threadIdx.x == 0) bnext[1] = 0;   // e_m(0) + 1 * P_0 = 0
+      if constexpr (BS) {
+        // all rows are written (last level ended on a barrier): reload b from b_next by TMA
+        bulk_g2s(b, bnext, (unsigned)((4 * (N + 1) + 15) & ~15), &sh.mbar, phase);
       } else {
-        if (threadIdx.x == 0) bnext[1] = 0;
         VT* t = b;
         b = bnext;
         bnext = t;
@@ -362,12 +443,13 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
       __syncthreads();
     }
   }
+  atomicAdd(&sh.evals, nev);
 }
 
 // ---- a3 for counts: P_j (int64) and T_N, block-wide scan over bins 1..N --------------------
 template <typename WT>
-__device__ void prefix_counts(const WT* we, int N, int64_t* P, Shared& sh, int64_t& TN,
-                              int64_t& n, int& neg) {
+__device__ void prefix_counts(const WT* we, int N, int64_t* P, int32_t* P32, Shared& sh,
+                              int64_t& TN, int64_t& n, int& neg) {
   int64_t carry = 0, tpart = 0;
   int bad = 0;
   for (int base = 0; base <= N; base += DP_NT) {
@@ -377,7 +459,10 @@ __device__ void prefix_counts(const WT* we, int N, int64_t* P, Shared& sh, int64
     bad |= cnt < 0;
     int64_t tot;
     const int64_t ex = block_exclusive_scan<DP_NT>(cnt, sh.wbuf, &tot);
-    if (t <= N) P[t] = carry + ex + cnt;
+    if (t <= N) {
+      P[t] = carry + ex + cnt;
+      P32[t] = (int32_t)(carry + ex + cnt);   // used only when the int32 path is exact
+    }
     carry += tot;
     tpart += (int64_t)t * cnt;
   }
@@ -470,6 +555,15 @@ __device__ double eval_cost_f64(const double* we, int N, const int32_t* pos, int
   return tot.hi + tot.lo;
 }
 
+// dynamic shared memory: opt_m (uint16[N+1]) | int32 b (if it fits) + int32-path scratch,
+// overlapped with the int64/fp64-path scratch (those paths keep b in global memory)
+__host__ __device__ __forceinline__ size_t dyn_smem_bytes(int N, bool smem_b) {
+  const size_t a = smem_b ? align256(4 * (size_t)(N + 1)) : 0;
+  const size_t n32 = a + scratch_bytes<int32_t>();
+  const size_t n64 = scratch_bytes<int64_t>();
+  return align256(2 * (size_t)(N + 1)) + (n32 > n64 ? n32 : n64);
+}
+
 template <typename WT>
 __global__ void __launch_bounds__(DP_NT) dp_place_kernel(DpParams p) {
   using PT = typename WTraits<WT>::PT;
@@ -479,45 +573,64 @@ __global__ void __launch_bounds__(DP_NT) dp_place_kernel(DpParams p) {
   __shared__ Shared sh;
   const int N = p.N, M = p.M;
   uint16_t* sopt = reinterpret_cast<uint16_t*>(dsm);
-  int32_t* smem_b32 = reinterpret_cast<int32_t*>(dsm + align256(2 * (size_t)(N + 1)));
+  uint8_t* after_sopt = dsm + align256(2 * (size_t)(N + 1));
+  int32_t* smem_b32 = reinterpret_cast<int32_t*>(after_sopt);
+  uint8_t* scratch32 = after_sopt + (p.smem_b ? align256(4 * (size_t)(N + 1)) : 0);
+  uint8_t* scratch64 = after_sopt;
   const WT* w = reinterpret_cast<const WT*>(p.w);
   CT* cost = reinterpret_cast<CT*>(p.cost);
   CT* cbb = reinterpret_cast<CT*>(p.cbb);
+  unsigned phase = 0;   // TMA mbarrier parity, identical in every thread
+  if (threadIdx.x == 0) {
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&sh.mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 
   for (int e = blockIdx.x; e < p.E; e += gridDim.x) {
-    uint8_t* slot = p.ws + (size_t)blockIdx.x * p.slot;
+    uint8_t* slot = p.ws + SP_WS_STATS_BYTES + (size_t)blockIdx.x * p.slot;
     PT* P = reinterpret_cast<PT*>(slot);
+    int32_t* P32 = reinterpret_cast<int32_t*>(slot + slot_p32_off(N, M));
     const WT* we = w + (int64_t)e * (N + 1);
     CT TN, n;
     int neg;
     if constexpr (F64) {
       prefix_f64(we, N, P, sh, TN, n, neg);
     } else {
-      prefix_counts<WT>(we, N, P, sh, TN, n, neg);
+      prefix_counts<WT>(we, N, P, P32, sh, TN, n, neg);
     }
     if (threadIdx.x == 0) {
       sh.err = 0;
+      sh.evals = 0;
       if (cbb) cbb[(int64_t)e * (M + 1)] = TN;   // V_0 = T_N
       cost[e] = TN;
     }
     __syncthreads();
 
     // ---- a4: the DP ----------------------------------------------------------------------
-    int status = 0;
+    int status = 0, path = -1;
     if (neg) {
       status = SP_ERR_BAD_ARGUMENT;
     } else if (M > 0) {
       if constexpr (F64) {
-        solve_entry<double, false, PT, CT>(p, sh, nullptr, sopt, e, TN);
+        solve_entry<double, false, PT, CT>(p, sh, nullptr, sopt, scratch64, e, TN, P, phase);
+        path = 2;
       } else {
         // narrow (exact int32) when 2 n N < 2^31, else int64 (exact when 2 n N < 2^62)
         const bool narrow = n < (int64_t(1) << 30) / N;
         const bool wide_ok = n < (int64_t(1) << 61) / N;
         if (narrow) {
-          if (p.smem_b) solve_entry<int32_t, true, PT, CT>(p, sh, smem_b32, sopt, e, TN);
-          else solve_entry<int32_t, false, PT, CT>(p, sh, nullptr, sopt, e, TN);
+          if (p.smem_b)
+            solve_entry<int32_t, true, int32_t, CT>(p, sh, smem_b32, sopt, scratch32, e, TN, P32,
+                                                    phase);
+          else
+            solve_entry<int32_t, false, int32_t, CT>(p, sh, nullptr, sopt, scratch32, e, TN, P32,
+                                                     phase);
+          path = 0;
         } else if (wide_ok) {
-          solve_entry<int64_t, false, PT, CT>(p, sh, nullptr, sopt, e, TN);
+          solve_entry<int64_t, false, PT, CT>(p, sh, nullptr, sopt, scratch64, e, TN, P, phase);
+          path = 1;
         } else {
           status = SP_ERR_OVERFLOW;
         }
@@ -525,14 +638,20 @@ __global__ void __launch_bounds__(DP_NT) dp_place_kernel(DpParams p) {
     }
     __syncthreads();
     if (sh.err) status = sh.err;
+    if (threadIdx.x == 0) {
+      sp_dp_stats* st = reinterpret_cast<sp_dp_stats*>(p.ws);
+      atomicAdd(&st->evaluations, sh.evals);
+      if (path == 0) atomicAdd(&st->entries_i32, 1ull);
+      if (path == 1) atomicAdd(&st->entries_i64, 1ull);
+      if (path == 2) atomicAdd(&st->entries_f64, 1ull);
+    }
 
     // ---- a5: rule-B backtrack (one thread; <= M dependent reads) ---------------------------
     int32_t* out = p.pos + (int64_t)e * M;
     if (threadIdx.x == 0) {
       int k = 0;
       if (status == 0 && M > 0) {
-        const uint16_t* opt =
-            reinterpret_cast<const uint16_t*>(slot + 3 * align256(8 * (size_t)(N + 1)));
+        const uint16_t* opt = reinterpret_cast<const uint16_t*>(slot + slot_opt_off(N));
         int j = N, m = M;
         while (m > 0 && P[j] > 0) {
           const int s = opt[(size_t)(m - 1) * (N + 1) + j];
@@ -566,15 +685,11 @@ __global__ void __launch_bounds__(DP_NT) dp_place_kernel(DpParams p) {
 
 }  // namespace sp
 
-static size_t dp_dyn_smem(int N, bool smem_b) {
-  size_t s = sp::align256(2 * (size_t)(N + 1));
-  if (smem_b) s += sp::align256(4 * (size_t)(N + 1));
-  return s;
+static bool dp_smem_b_fits(int N) {
+  return sp::dyn_smem_bytes(N, true) + sizeof(sp::Shared) + 1024 <= 227 * 1024;
 }
 
-static bool dp_smem_b_fits(int N) {
-  return dp_dyn_smem(N, true) + sizeof(sp::Shared) + 1024 <= 227 * 1024;
-}
+static size_t dp_dyn_smem(int N, bool smem_b) { return sp::dyn_smem_bytes(N, smem_b); }
 
 template <typename WT>
 static int dp_grid_t(int E, int N) {
@@ -603,7 +718,7 @@ static int dp_grid(int E, int N) {
 extern "C" size_t sp_place_checkpoints_workspace_bytes(int32_t n_entries, int32_t N, int32_t M) {
   if (N < 1 || N > SP_MAX_N || n_entries < 0 || M < 0 || M > N) return 0;
   if (n_entries == 0) return 0;
-  return (size_t)dp_grid(n_entries, N) * sp::slot_bytes(N, M);
+  return SP_WS_STATS_BYTES + (size_t)dp_grid(n_entries, N) * sp::slot_bytes(N, M);
 }
 
 extern "C" sp_status sp_place_checkpoints(const void* weights, sp_weight_type wtype,
@@ -621,7 +736,7 @@ extern "C" sp_status sp_place_checkpoints(const void* weights, sp_weight_type wt
   if (wtype == SP_W_COUNTS_I32) grid = dp_grid_t<int32_t>(n_entries, N);
   else if (wtype == SP_W_COUNTS_I64) grid = dp_grid_t<int64_t>(n_entries, N);
   else grid = dp_grid_t<double>(n_entries, N);
-  const size_t need = (size_t)grid * sp::slot_bytes(N, M);
+  const size_t need = SP_WS_STATS_BYTES + (size_t)grid * sp::slot_bytes(N, M);
   if (!workspace || workspace_bytes < need) return SP_ERR_WORKSPACE;
   sp::DpParams p;
   p.w = weights;
@@ -638,6 +753,7 @@ extern "C" sp_status sp_place_checkpoints(const void* weights, sp_weight_type wt
   p.smem_b = dp_smem_b_fits(N) ? 1 : 0;
   const size_t dyn = dp_dyn_smem(N, p.smem_b);
   cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(workspace, 0, SP_WS_STATS_BYTES, st) != cudaSuccess) SP_CHECK_LAUNCH();
   if (wtype == SP_W_COUNTS_I32) sp::dp_place_kernel<int32_t><<<grid, sp::DP_NT, dyn, st>>>(p);
   else if (wtype == SP_W_COUNTS_I64) sp::dp_place_kernel<int64_t><<<grid, sp::DP_NT, dyn, st>>>(p);
   else sp::dp_place_kernel<double><<<grid, sp::DP_NT, dyn, st>>>(p);

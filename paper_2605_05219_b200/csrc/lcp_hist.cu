@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(LCP_WARPS * 32)
     }
   }
   if (lane == 0) {
-    atomicAdd(hist + (int64_t)e * (N + 1) + t, 1);
+    if (hist) atomicAdd(hist + (int64_t)e * (N + 1) + t, 1);
     if (lcp_out) lcp_out[r] = (int32_t)t;
   }
 }
@@ -109,7 +109,7 @@ extern "C" sp_status sp_overlap_hist(const int32_t* entry_tokens, const int64_t*
                                      int32_t* lcp_out, sp_stream_t stream) {
   if (N < 1 || N > SP_MAX_N || n_entries < 0 || n_requests < 0) return SP_ERR_BAD_LENGTH;
   if (n_requests == 0) return SP_OK;
-  if (!entry_tokens || !entry_off || !req_tokens || !req_off || !req_entry || !hist)
+  if (!entry_tokens || !entry_off || !req_tokens || !req_off || !req_entry || (!hist && !lcp_out))
     return SP_ERR_BAD_ARGUMENT;
   // the 16-byte vector path needs 16-byte aligned token bases (offsets are checked per row)
   const int vec_ok = (((uintptr_t)entry_tokens | (uintptr_t)req_tokens) & 15) == 0;

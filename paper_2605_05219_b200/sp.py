@@ -102,17 +102,19 @@ def _stream(stream, device):
 
 
 def overlap_hist(entry_tokens, entry_off, req_tokens, req_off, req_entry, N, hist=None,
-                 lcp_out=None, n_entries=None, stream=None):
-    """a1 + a2.  Returns (hist [E][N+1] int32, accumulated in place; lcp_out [R] or None)."""
+                 lcp_out=None, n_entries=None, stream=None, with_hist=True):
+    """a1 + a2.  Returns (hist [E][N+1] int32, accumulated in place; lcp_out [R] or None).
+    with_hist=False computes the depths only (lcp_out required)."""
     E = entry_off.numel() - 1 if n_entries is None else n_entries
     R = req_off.numel() - 1
     dev = req_tokens.device
-    if hist is None:
+    if hist is None and with_hist:
         hist = torch.zeros(E, N + 1, dtype=torch.int32, device=dev)
     st = lib().sp_overlap_hist(
         _dev(entry_tokens, torch.int32, "entry_tokens"), _dev(entry_off, torch.int64, "entry_off"),
         E, _dev(req_tokens, torch.int32, "req_tokens"), _dev(req_off, torch.int64, "req_off"),
-        _dev(req_entry, torch.int32, "req_entry"), R, N, _dev(hist, torch.int32, "hist"),
+        _dev(req_entry, torch.int32, "req_entry"), R, N,
+        _dev(hist, torch.int32, "hist") if with_hist else None,
         None if lcp_out is None else _dev(lcp_out, torch.int32, "lcp_out"), _stream(stream, dev))
     _check(st, "sp_overlap_hist")
     return hist, lcp_out
@@ -129,6 +131,15 @@ def accumulate_depths(entry, depth, e_begin, e_end, N, hist, stream=None):
 
 def place_checkpoints_workspace_bytes(n_entries, N, M) -> int:
     return int(lib().sp_place_checkpoints_workspace_bytes(n_entries, N, M))
+
+
+SP_WS_STATS_BYTES = 256
+
+
+def dp_stats(workspace) -> dict:
+    """Launch statistics from the head of a DP workspace (sp_dp_stats; synchronises)."""
+    v = workspace[:32].view(torch.int64).cpu().tolist()
+    return {"evaluations": v[0], "entries_i32": v[1], "entries_i64": v[2], "entries_f64": v[3]}
 
 
 def place_checkpoints(weights, M, positions=None, n_positions=None, cost=None,

@@ -166,14 +166,16 @@ def _round_up(x: torch.Tensor, a: int) -> torch.Tensor:
 
 
 def make_trace(cfg: TraceConfig, seed: int = 0, device="cpu", entry_begin: int = 0,
-               n_req_entries: int = None, chunk: int = 1 << 27) -> dict:
+               n_req_entries: int = None, chunk: int = 1 << 27, world: int = 1,
+               rank: int = 0) -> dict:
     """Entry token CSR + request token CSR for cfg.
 
     Requests are generated for entries [entry_begin, entry_begin + n_req_entries) (all entries
-    by default) so that a rank can materialise only its own requests.  Returns a dict of tensors
-    on `device`: entry_tokens int32, entry_off int64 [E+1], req_tokens int32, req_off int64
-    [R+1], req_entry int32 [R], depth int32 [R] (the drawn depth = the LCP by construction, not
-    clamped to N), N (int).
+    by default); with world > 1 only the requests that "arrive" at `rank` are materialised
+    (request g arrives at rank hash(g) % world: uniformly at random).  Returns a
+    dict of tensors on `device`: entry_tokens int32, entry_off int64 [E+1], req_tokens int32,
+    req_off int64 [R+1], req_entry int32 [R], depth int32 [R] (the drawn depth = the LCP by
+    construction, not clamped to N), N (int).
     """
     dev = torch.device(device)
     E, a = cfg.n_entries, max(cfg.align, 1)
@@ -195,6 +197,9 @@ def make_trace(cfg: TraceConfig, seed: int = 0, device="cpu", entry_begin: int =
     req_entry = re.repeat_interleave(cfg.req_per_entry)
     ridx = torch.arange(cfg.req_per_entry, dtype=torch.int64, device=dev).repeat(nre)
     gid = req_entry * cfg.req_per_entry + ridx          # global request id (rank independent)
+    if world > 1:
+        mine = (stream(seed, 15, gid) % world) == rank
+        req_entry, ridx, gid = req_entry[mine], ridx[mine], gid[mine]
     Lr = L[req_entry]
     depth = draw_depths(shape_ids(cfg.shape, req_entry), Lr, seed, req_entry, ridx)
     if cfg.miss_frac > 0:

@@ -1,0 +1,42 @@
+"""Profiling driver: one warm-up + one measured sp_place_checkpoints launch on W5-shaped dense
+histograms (E entries), then the LCP kernel on a W5-shaped trace.  Used under ncu."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_2605_05219_b200 import sp
+from paper_2605_05219_b200 import workload as wl
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--entries", type=int, default=148)
+ap.add_argument("--workload", default="W5")
+ap.add_argument("--M", type=int, default=None)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--lcp", action="store_true")
+a = ap.parse_args()
+cfg = wl.scaled(wl.CONFIGS[a.workload], a.entries)
+M = a.M or cfg.M
+dev = torch.device("cuda:0")
+H = wl.make_dense_hist(cfg, seed=0, device=dev) if cfg.dense_n else wl.uniform_hist(a.entries, cfg.N, dev)
+ws = torch.empty(sp.place_checkpoints_workspace_bytes(a.entries, cfg.N, M), dtype=torch.uint8, device=dev)
+for r in range(a.reps):
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    sp.place_checkpoints(H, M, workspace=ws)
+    e.record()
+    torch.cuda.synchronize()
+    st = sp.dp_stats(ws)
+    print(f"dp rep {r}: {s.elapsed_time(e):.3f} ms  cells={a.entries*cfg.N*M:.3e} "
+          f"evals/cell={st['evaluations']/(a.entries*cfg.N*M):.2f}  "
+          f"Mcells/s={a.entries*cfg.N*M/s.elapsed_time(e)/1e3:.1f}", flush=True)
+if a.lcp:
+    tr = wl.make_trace(cfg, seed=0, device=dev)
+    lcp = torch.empty(tr["req_off"].numel() - 1, dtype=torch.int32, device=dev)
+    hist = torch.zeros(a.entries, cfg.N + 1, dtype=torch.int32, device=dev)
+    for r in range(a.reps):
+        sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], tr["req_tokens"], tr["req_off"],
+                        tr["req_entry"], cfg.N, hist=hist, lcp_out=lcp)
+    torch.cuda.synchronize()

@@ -26,13 +26,28 @@
 
 namespace sp {
 
-constexpr int DP_NT = 512;
+#ifndef SP_DP_NT
+#define SP_DP_NT 1024
+#endif
+constexpr int DP_NT = SP_DP_NT;
 constexpr int DP_NW = DP_NT / 32;
 constexpr int T_INLINE = 8;   // rows with at most this many candidates: one thread solves it
-constexpr int PS = 32;        // candidates per piece of a queued (long) row
-constexpr int QMAX = 512;     // queued rows per level
-constexpr int PMAX = 2048;    // pieces per level
-constexpr int RB = 4;         // rows per thread per batch in the bracket pass
+constexpr int PS = 64;        // candidates per piece of a queued (long) row (top levels)
+constexpr int QMAX = 128;     // queued rows per top level
+constexpr int PMAX = 1024;    // pieces per top level
+constexpr int RB = 2;         // rows per thread per batch in the bracket pass
+#ifndef SP_SEG_ROWS
+#define SP_SEG_ROWS 512
+#endif
+constexpr int SEG_ROWS = SP_SEG_ROWS; // rows per warp-owned segment (the subtree below the top levels)
+#ifndef SP_WCAP
+#define SP_WCAP 32
+#endif
+constexpr int WCAP = SP_WCAP;      // long rows a warp can defer per segment level
+#ifndef SP_TW
+#define SP_TW 8
+#endif
+constexpr int TW = SP_TW;         // rows longer than this are solved warp-cooperatively
 
 // ------------------------------------------------------------------------------------------
 // value-type traits
@@ -122,9 +137,26 @@ struct DpParams {
   int smem_b;   // 1: the int32 b array fits in shared memory next to opt_m
 };
 
+constexpr int TOPP_CAP = 160;
+#ifdef SP_TIMING
+#define SP_T0() long long _t = clock64()
+#define SP_TICK(sh, i)                                                  \
+  do {                                                                  \
+    const long long _n = clock64();                                     \
+    if (threadIdx.x == 0) (sh).tclk[i] += (unsigned long long)(_n - _t); \
+    _t = _n;                                                            \
+  } while (0)
+#else
+#define SP_T0() (void)0
+#define SP_TICK(sh, i) (void)0
+#endif
 struct Shared {
   uint64_t mbar;                  // TMA bulk-copy completion barrier
+  int64_t topP[TOPP_CAP];         // P_j of the top-level rows (j multiple of h0), as VT
+  unsigned long long tclk[10];    // SP_TIMING: per-phase cycles of this CTA
   unsigned long long ctr[3];      // per-level queue counters (triple-buffered)
+  int segctr;                     // next segment to grab
+  int nmulti[3];                  // queued rows with more than one piece
   unsigned long long evals;
   int64_t wbuf[DP_NW + 1];
   double dbuf[2 * (DP_NW + 1)];
@@ -162,8 +194,23 @@ struct Scratch {
 };
 
 template <typename VT>
+__host__ __device__ __forceinline__ size_t wlist_bytes() {
+  return (size_t)DP_NW * WCAP * (12 + sizeof(VT));
+}
+
+constexpr int TOPR = 64;   // rows a lean top level handles
+template <typename VT>
+__host__ __device__ __forceinline__ size_t top_scratch_bytes() {
+  return (size_t)TOPR * DP_NW * (sizeof(VT) + 4) + 3 * TOPR * 4;
+}
+
+template <typename VT>
 __host__ __device__ __forceinline__ size_t scratch_bytes() {
-  return align256((size_t)QMAX * (16 + sizeof(VT))) + align256((size_t)PMAX * (4 + sizeof(VT)));
+  const size_t q = align256((size_t)QMAX * (16 + sizeof(VT))) + align256((size_t)PMAX * (4 + sizeof(VT)));
+  const size_t w = align256(wlist_bytes<VT>());
+  const size_t t = align256(top_scratch_bytes<VT>());
+  const size_t m = q > w ? q : w;   // the phases never overlap: one union
+  return m > t ? m : t;
 }
 
 template <typename VT>
@@ -229,6 +276,23 @@ __device__ __forceinline__ void eval_range(const VT* __restrict__ b, VT Pj, int 
   bs = arg;
 }
 
+// plain leftmost argmin over s = s0..s1 (short rows)
+template <typename VT>
+__device__ __forceinline__ void eval_short(const VT* __restrict__ b, VT Pj, int s0, int s1,
+                                           VT& bv, int& bs) {
+  VT best = Lim<VT>::inf();
+  int arg = INT_MAX;
+  for (int s = s0; s <= s1; ++s) {
+    const VT v = cand(b[s], s, Pj);
+    if (v < best) {
+      best = v;
+      arg = s;
+    }
+  }
+  bv = best;
+  bs = arg;
+}
+
 template <typename VT, typename Ctx>
 __device__ __forceinline__ void row_write(const Ctx& c, int j, int lo, int hi, VT Pj, VT bv,
                                           int bs) {
@@ -268,9 +332,11 @@ template <typename VT, typename Ctx>
 __device__ void run_level(const Ctx& c, Shared& sh, const Scratch<VT>& S, int h, int R,
                           int lvl, unsigned long long& nev) {
   unsigned long long* ctr = &sh.ctr[lvl % 3];
-  if (threadIdx.x == 0) sh.ctr[(lvl + 1) % 3] = 0;   // last used two levels ago
+  if (threadIdx.x == 0) {   // last used two levels ago
+    sh.ctr[(lvl + 1) % 3] = 0;
+    sh.nmulti[(lvl + 1) % 3] = 0;
+  }
   const int N = c.N;
-  const bool optN = (N % (2 * h)) == 0;               // row N solved at an earlier level
   for (int i0 = threadIdx.x; i0 < R; i0 += DP_NT * RB) {
     int jj[RB], lo[RB], hi[RB];
     VT Pj[RB];
@@ -281,13 +347,10 @@ __device__ void run_level(const Ctx& c, Shared& sh, const Scratch<VT>& S, int h,
       lo[u] = 1;
       hi[u] = 0;
       Pj[u] = 0;
-      if (i < R) {
+      if (i < R && h * (2 * i + 1) < N) {   // row N is solved first
         const int j = h * (2 * i + 1);
-        int l = 1, r = j;
-        if (j - h >= 1) l = c.sopt[j - h];
-        if (j + h <= N) r = min((int)c.sopt[j + h], j);
-        else if (optN) r = min((int)c.sopt[N], j);
-        if (c.optprev) l = max(l, (int)c.optprev[j]);
+        const int l = max((int)c.sopt[j - h], (int)c.sopt[j]);   // opt_m(j-h), opt_{m-1}(j)
+        const int r = min((int)c.sopt[min(j + h, N)], j);
         jj[u] = j;
         lo[u] = l;
         hi[u] = r;
@@ -314,13 +377,17 @@ __device__ void run_level(const Ctx& c, Shared& sh, const Scratch<VT>& S, int h,
           S.qlen[q] = fits ? len : 0;   // a dead entry keeps the piece order intact
           S.qpb[q] = pb;
           S.qP[q] = Pj[u];
-          if (fits) continue;
+          if (fits) {
+            if (np > 1) atomicAdd(&sh.nmulti[lvl % 3], 1);
+            continue;
+          }
         }
         // no room: solve it here (correct, just slower)
       }
       VT bv;
       int bs;
-      eval_range(c.b, Pj[u], l, r, 1, bv, bs);
+      if (len <= T_INLINE) eval_short(c.b, Pj[u], l, r, bv, bs);
+      else eval_range(c.b, Pj[u], l, r, 1, bv, bs);
       row_write(c, j, l, r, Pj[u], bv, bs);
     }
   }
@@ -329,27 +396,55 @@ __device__ void run_level(const Ctx& c, Shared& sh, const Scratch<VT>& S, int h,
   const int Q = min((int)(tot >> 32), QMAX);
   const int NP = min((int)(tot & 0xffffffffu), PMAX);
   if (Q == 0) return;
-  for (int p = threadIdx.x; p < NP; p += DP_NT) {
-    int a = 0, z = Q - 1;   // last queue entry with qpb <= p
-    while (a < z) {
-      const int mid = (a + z + 1) >> 1;
-      if (S.qpb[mid] <= p) a = mid; else z = mid - 1;
+  const int nmulti = sh.nmulti[lvl % 3];
+  // phase 2: thread t takes the contiguous pieces [t per, (t+1) per): one binary search, then walk
+  {
+    const int per = (NP + DP_NT - 1) / DP_NT;
+    const int p0 = threadIdx.x * per, p1 = min(p0 + per, NP);
+    if (p0 < p1) {
+      int a = 0, z = Q - 1;   // last queue entry with qpb <= p0
+      while (a < z) {
+        const int mid = (a + z + 1) >> 1;
+        if (S.qpb[mid] <= p0) a = mid; else z = mid - 1;
+      }
+      for (int p = p0; p < p1; ++p) {
+        while (a + 1 < Q && S.qpb[a + 1] <= p) ++a;
+        const int len = S.qlen[a];
+        const int np = (len + PS - 1) / PS;
+        const int k = p - S.qpb[a];
+        if (k >= np) continue;
+        VT bv;
+        int bs;
+        const int lo = S.qlo[a];
+        eval_range(c.b, S.qP[a], lo + k, lo + len - 1, np, bv, bs);
+        if (np == 1) {
+          row_write(c, S.qj[a], lo, lo + len - 1, S.qP[a], bv, bs);
+        } else {
+          S.pv[p] = bv;
+          S.ps[p] = bs;
+        }
+      }
     }
-    const int len = S.qlen[a];
-    const int np = (len + PS - 1) / PS;
-    const int k = p - S.qpb[a];
-    VT bv = Lim<VT>::inf();
-    int bs = INT_MAX;
-    if (k < np) eval_range(c.b, S.qP[a], S.qlo[a] + k, S.qlo[a] + len - 1, np, bv, bs);
-    S.pv[p] = bv;
-    S.ps[p] = bs;
   }
-  __syncthreads();   // B2: piece minima written
+  __syncthreads();   // B2: single-piece rows written, piece minima of the others stored
+  if (nmulti == 0) return;
+  // phase 3: rows with several pieces; one thread per row (<= 64 pieces) or one warp
+  for (int q = threadIdx.x; q < Q; q += DP_NT) {
+    const int len = S.qlen[q];
+    const int np = (len + PS - 1) / PS;
+    if (np < 2 || np > 64) continue;
+    const int pb = S.qpb[q];
+    VT bv = S.pv[pb];
+    int bs = S.ps[pb];
+    for (int k = 1; k < np; ++k) lex_min(bv, bs, S.pv[pb + k], S.ps[pb + k]);
+    row_write(c, S.qj[q], S.qlo[q], S.qlo[q] + len - 1, S.qP[q], bv, bs);
+  }
   const int lane = lane_id();
   for (int q = warp_id(); q < Q; q += DP_NW) {
     const int len = S.qlen[q];
-    if (len == 0) continue;
-    const int np = (len + PS - 1) / PS, pb = S.qpb[q];
+    const int np = (len + PS - 1) / PS;
+    if (np <= 64) continue;
+    const int pb = S.qpb[q];
     VT bv = Lim<VT>::inf();
     int bs = INT_MAX;
     for (int k = lane; k < np; k += 32) lex_min(bv, bs, S.pv[pb + k], S.ps[pb + k]);
@@ -362,6 +457,367 @@ __device__ void run_level(const Ctx& c, Shared& sh, const Scratch<VT>& S, int h,
     if (lane == 0) row_write(c, S.qj[q], S.qlo[q], S.qlo[q] + len - 1, S.qP[q], bv, bs);
   }
   __syncthreads();   // B3: queued rows written
+}
+
+// ---- warp-cooperative leftmost argmin of b_s - s P over s in [lo, hi] ------------------------
+// Generic version: lanes stride the candidates, lexicographic (value, index) shuffle reduction.
+template <typename VT>
+__device__ __forceinline__ void warp_row_min(const VT* __restrict__ b, VT Pj, int lo, int hi,
+                                             VT& bv, int& bs) {
+  const int lane = lane_id();
+  bv = Lim<VT>::inf();
+  bs = INT_MAX;
+  for (int s = lo + lane; s <= hi; s += 32) {
+    const VT v = cand(b[s], s, Pj);
+    if (v < bv) {
+      bv = v;
+      bs = s;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const VT ov = __shfl_xor_sync(FULL, bv, o);
+    const int os = __shfl_xor_sync(FULL, bs, o);
+    lex_min(bv, bs, ov, os);
+  }
+}
+
+// Exact-int32 version: each lane scans 16-byte aligned groups of four candidates (one LDS.128,
+// a VIMNMX3-based min of four, index kept per group), the unaligned head/tail candidates go to
+// lanes 0-2, and the warp reduction is two REDUX instructions (min value, then min index among
+// the lanes holding it) -- the leftmost argmin, exactly.
+template <>
+__device__ __forceinline__ void warp_row_min<int32_t>(const int32_t* __restrict__ b, int32_t Pj,
+                                                      int lo, int hi, int32_t& bv, int& bs) {
+  const int lane = lane_id();
+  int best = INT_MAX, arg = INT_MAX;
+  const int a = min(hi + 1, (lo + 3) & ~3);        // first aligned candidate
+  const int nfull = (hi + 1 - a) >> 2;              // aligned groups of 4
+  const int t0 = a + 4 * nfull;                     // first tail candidate
+  if (lane < a - lo) {                              // head: at most 3 candidates
+    const int s = lo + lane;
+    best = b[s] - s * Pj;
+    arg = s;
+  }
+  int gb = INT_MAX, gi = -1;
+  for (int g = lane; g < nfull; g += 32) {
+    const int s = a + 4 * g;
+    const int4 q = *reinterpret_cast<const int4*>(b + s);
+    const int v0 = q.x - s * Pj, v1 = q.y - (s + 1) * Pj;
+    const int v2 = q.z - (s + 2) * Pj, v3 = q.w - (s + 3) * Pj;
+    const int m = min(min(v0, v1), min(v2, v3));
+    if (m < gb) {
+      gb = m;
+      gi = s;
+    }
+  }
+  if (gi >= 0 && gb < best) {   // head candidates (if any) have smaller indices: strict '<'
+    int k = gi + 3;
+#pragma unroll
+    for (int d = 2; d >= 0; --d)
+      if (b[gi + d] - (gi + d) * Pj == gb) k = gi + d;
+    best = gb;
+    arg = k;
+  }
+  if (lane < hi + 1 - t0) {                         // tail: at most 3 candidates
+    const int s = t0 + lane;
+    const int v = b[s] - s * Pj;
+    if (v < best) {
+      best = v;
+      arg = s;
+    }
+  }
+  const int vmin = __reduce_min_sync(FULL, best);
+  bs = __reduce_min_sync(FULL, best == vmin ? arg : INT_MAX);
+  bv = vmin;
+}
+
+// ---- warp-level argmin reduction of per-lane (value, index) pairs -----------------------------
+template <typename VT>
+__device__ __forceinline__ void warp_lexmin(VT& bv, int& bs) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const VT ov = __shfl_xor_sync(FULL, bv, o);
+    const int os = __shfl_xor_sync(FULL, bs, o);
+    lex_min(bv, bs, ov, os);
+  }
+}
+template <>
+__device__ __forceinline__ void warp_lexmin<int32_t>(int32_t& bv, int& bs) {
+  const int vmin = __reduce_min_sync(FULL, bv);
+  bs = __reduce_min_sync(FULL, bv == vmin ? bs : INT_MAX);
+  bv = vmin;
+}
+
+// Lean top level (R <= TOPR rows, all long): every warp computes the R brackets itself (two rows
+// per lane, shuffle scan of the lengths), the level's candidates are flattened over all threads
+// (warp w owns [w*32C, (w+1)*32C), lane l takes every 32nd candidate so b reads are
+// conflict-free), each warp reduces per row with warp_lexmin and stores a partial, and one
+// thread per row finalises.  Two barriers, no global loads (P of top rows cached in smem).
+template <typename VT, typename Ctx>
+__device__ void top_level(const Ctx& c, Shared& sh, uint8_t* scratch, const VT* topP, int h0,
+                          int h, int R, int lvl, unsigned long long& nev) {
+  const int N = c.N, lane = lane_id(), w = warp_id();
+  if (threadIdx.x == 0) {   // keep run_level's counter rotation valid
+    sh.ctr[(lvl + 1) % 3] = 0;
+    sh.nmulti[(lvl + 1) % 3] = 0;
+  }
+  VT* pv = reinterpret_cast<VT*>(scratch);                       // [TOPR][DP_NW]
+  int* ps = reinterpret_cast<int*>(pv + TOPR * DP_NW);           // [TOPR][DP_NW]
+  int* rlo = ps + TOPR * DP_NW;                                  // [TOPR]
+  int* rlen = rlo + TOPR;                                        // [TOPR]
+  int* rst = rlen + TOPR;                                        // [TOPR]
+  int lo[2], len[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int i = lane + 32 * u;
+    const int j = h * (2 * i + 1);
+    lo[u] = 1;
+    len[u] = 0;
+    if (i < R && j < N) {
+      const int l = max((int)c.sopt[j - h], (int)c.sopt[j]);   // opt_m(j-h), opt_{m-1}(j)
+      const int r = min((int)c.sopt[min(j + h, N)], j);
+      lo[u] = l;
+      len[u] = max(r - l + 1, 0);
+    }
+  }
+  int inc0 = len[0], inc1 = len[1];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y0 = __shfl_up_sync(FULL, inc0, o), y1 = __shfl_up_sync(FULL, inc1, o);
+    if (lane >= o) {
+      inc0 += y0;
+      inc1 += y1;
+    }
+  }
+  const int tot0 = __shfl_sync(FULL, inc0, 31);
+  const int W = tot0 + __shfl_sync(FULL, inc1, 31);
+  const int st0 = inc0 - len[0], st1 = tot0 + inc1 - len[1];
+  if (w == 0) {   // every warp computed the same; warp 0 records it for the finalisers
+    rlo[lane] = lo[0];
+    rlen[lane] = len[0];
+    rst[lane] = st0;
+    rlo[lane + 32] = lo[1];
+    rlen[lane + 32] = len[1];
+    rst[lane + 32] = st1;
+  }
+  if (threadIdx.x == 0) nev += (unsigned)W;
+  const int C = (W + DP_NT - 1) / DP_NT;   // candidates per thread
+  const int wb = w * 32 * C, we = min(wb + 32 * C, W);
+  if (wb < we) {
+    // rows are contiguous in the flattened order: the first row of this warp is the number of
+    // rows that end at or before wb
+    const int rfirst = __popc(__ballot_sync(FULL, st0 + len[0] <= wb)) +
+                       __popc(__ballot_sync(FULL, st1 + len[1] <= wb));
+    for (int r = rfirst; r < 64; ++r) {
+      const int sr = r < 32 ? __shfl_sync(FULL, st0, r & 31) : __shfl_sync(FULL, st1, r & 31);
+      if (sr >= we) break;
+      const int lr = r < 32 ? __shfl_sync(FULL, len[0], r & 31) : __shfl_sync(FULL, len[1], r & 31);
+      const int lor = r < 32 ? __shfl_sync(FULL, lo[0], r & 31) : __shfl_sync(FULL, lo[1], r & 31);
+      if (lr == 0) continue;
+      const int j = h * (2 * r + 1);
+      const VT Pj = topP[j / h0];
+      const int fa = max(sr, wb), fz = min(sr + lr, we);
+      int f = wb + lane;
+      if (f < fa) f += ((fa - f + 31) >> 5) << 5;
+      VT bv = Lim<VT>::inf();
+      int bs = INT_MAX;
+      for (; f < fz; f += 32) {
+        const int s = lor + (f - sr);
+        const VT v = cand(c.b[s], s, Pj);
+        if (v < bv) {
+          bv = v;
+          bs = s;
+        }
+      }
+      warp_lexmin(bv, bs);
+      if (lane == 0) {
+        pv[r * DP_NW + w] = bv;
+        ps[r * DP_NW + w] = bs;
+      }
+    }
+  }
+  __syncthreads();   // partials of every (row, warp) stored, row info recorded
+  // finalise: warp r reduces row r's partials (lane q holds warp q's, if warp q touched it)
+  for (int r = w; r < R; r += DP_NW) {
+    const int j = h * (2 * r + 1);
+    if (j >= N) continue;
+    const int lr = rlen[r];
+    VT bv = Lim<VT>::inf();
+    int bs = INT_MAX;
+    if (lr > 0) {
+      const int sr = rst[r];
+      const int w0 = sr / (32 * C), w1 = (sr + lr - 1) / (32 * C);
+      for (int q = w0 + lane; q <= w1; q += 32) lex_min(bv, bs, pv[r * DP_NW + q], ps[r * DP_NW + q]);
+    }
+    warp_lexmin(bv, bs);
+    if (lane == 0) {
+      if (bs == INT_MAX) {   // empty bracket: never expected (reading R6 self-check)
+        atomicExch(c.err, SP_ERR_INTERNAL);
+        bs = max(1, min(rlo[r], j));
+        bv = 0;
+      }
+      c.sopt[j] = (uint16_t)bs;
+      c.optout[j] = (uint16_t)bs;
+      c.bnext[j + 1] = icpt(bv, j + 1, topP[j / h0]);
+    }
+  }
+  __syncthreads();   // row results visible to the next level
+}
+
+// Row N first (every layer): the whole CTA splits [max(1, opt_{m-1}(N)), N] and reduces.  With
+// opt_m(N) known, every other row j has the right bound sopt[min(j + h, N)] (monotonicity), so
+// the per-row code below needs no boundary branches.
+template <typename VT, typename Ctx>
+__device__ void solve_row_N(const Ctx& c, Shared& sh, unsigned long long& nev) {
+  const int N = c.N;
+  const int lo = c.sopt[N], hi = N;   // sopt[N] = opt_{m-1}(N), or 1 before layer 1
+  const VT Pj = (VT)c.P[N];
+  VT bv = Lim<VT>::inf();
+  int bs = INT_MAX;
+  for (int s = lo + (int)threadIdx.x; s <= hi; s += DP_NT) {
+    const VT v = cand(c.b[s], s, Pj);
+    if (v < bv) {
+      bv = v;
+      bs = s;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const VT ov = __shfl_xor_sync(FULL, bv, o);
+    const int os = __shfl_xor_sync(FULL, bs, o);
+    lex_min(bv, bs, ov, os);
+  }
+  __syncthreads();   // sopt[N] read by everyone before it is rewritten
+  VT* red = reinterpret_cast<VT*>(sh.wbuf);   // DP_NW values of VT fit in wbuf
+  if (lane_id() == 0) {
+    red[warp_id()] = bv;
+    sh.red_s[warp_id()] = bs;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < DP_NW; ++w) lex_min(bv, bs, red[w], sh.red_s[w]);
+    nev += (unsigned)(hi - lo + 1);
+    row_write(c, N, lo, hi, Pj, bv, bs);
+  }
+  __syncthreads();
+}
+
+// Levels below the top ones: the rows split into segments (s h0, (s+1) h0) whose subtrees are
+// independent once the top levels are solved.  Each warp grabs whole segments (dynamic, one smem
+// counter) and solves their levels with __syncwarp only: lanes take rows; rows longer than TW are
+// deferred to a warp list and solved cooperatively (lanes stride the candidates, coalesced in b,
+// then a lexicographic shuffle min).  Warps overlap each other's L2 latencies.
+// Levels below the top ones: the rows split into segments (s h0, (s+1) h0) whose subtrees are
+// independent once the top levels are solved.  Each warp grabs whole segments (dynamic, one smem
+// counter) and solves their levels with __syncwarp only: lanes take rows; rows longer than TW are
+// deferred to a warp list and solved cooperatively (warp_row_min).  Warps overlap each other's
+// latencies.
+template <typename VT, typename Ctx>
+__device__ void run_segments(const Ctx& c, Shared& sh, uint8_t* scratch, int L, int K0,
+                             unsigned long long& nev) {
+  const int N = c.N;
+  const int h0 = 1 << (L - K0);
+  const int NS = N / h0 + 1;
+  const int lane = lane_id(), w = warp_id();
+  int* lj = reinterpret_cast<int*>(scratch) + w * 3 * WCAP;
+  int* llo = lj + WCAP;
+  int* llen = llo + WCAP;
+  VT* lP = reinterpret_cast<VT*>(reinterpret_cast<int*>(scratch) + DP_NW * 3 * WCAP) + w * WCAP;
+  const VT* __restrict__ b = c.b;
+  const uint16_t* sopt = c.sopt;
+  unsigned nv = 0;
+#ifdef SP_TIMING
+  long long t_long = 0, t_pass = 0;
+#endif
+  for (;;) {
+    int seg = 0;
+    if (lane == 0) seg = atomicAdd(&sh.segctr, 1);
+    seg = __shfl_sync(FULL, seg, 0);
+    if (seg >= NS) break;
+    const int base = seg * h0;
+    for (int k = K0; k < L; ++k) {
+      const int h = 1 << (L - 1 - k);
+      const int nr = 1 << (k - K0);
+      int cnt = 0;
+#ifdef SP_TIMING
+      long long t1 = clock64();
+#endif
+      for (int i0 = 0; i0 < nr; i0 += 32) {
+        const int i = i0 + lane;
+        const int j = base + h * (2 * i + 1);
+        const bool valid = i < nr && j < N;   // row N is solved first
+        int lo = 1, hi = 0;
+        VT Pj = 0;
+        if (valid) {
+          lo = max((int)sopt[j - h], (int)sopt[j]);   // opt_m(j-h), opt_{m-1}(j)
+          hi = min((int)sopt[min(j + h, N)], j);
+          Pj = (VT)c.P[j];
+        }
+        fix_bracket((VT*)nullptr, lo, hi);
+        const int len = hi - lo + 1;
+        nv += valid ? (unsigned)len : 0u;
+        const bool lng = valid && len > TW;
+        const unsigned bal = __ballot_sync(FULL, lng);
+        const int pos = cnt + __popc(bal & ((1u << lane) - 1));
+        cnt += __popc(bal);
+        if (lng && pos < WCAP) {
+          lj[pos] = j;
+          llo[pos] = lo;
+          llen[pos] = len;
+          lP[pos] = Pj;
+        }
+        if (valid && (!lng || pos >= WCAP)) {   // short row, or the list is full
+          VT best = Lim<VT>::inf();
+          int arg = INT_MAX;
+          for (int s = lo; s <= hi; ++s) {
+            const VT v = cand(b[s], s, Pj);
+            if (v < best) {
+              best = v;
+              arg = s;
+            }
+          }
+          if (arg == INT_MAX) {   // empty bracket: never expected (reading R6 self-check)
+            atomicExch(c.err, SP_ERR_INTERNAL);
+            arg = max(1, min(lo, j));
+            best = 0;
+          }
+          c.sopt[j] = (uint16_t)arg;
+          c.optout[j] = (uint16_t)arg;
+          c.bnext[j + 1] = icpt(best, j + 1, Pj);
+        }
+      }
+      cnt = min(cnt, WCAP);
+      __syncwarp();
+#ifdef SP_TIMING
+      long long t2 = clock64();
+      t_pass += t2 - t1;
+#endif
+      for (int q = 0; q < cnt; ++q) {
+        const int j = lj[q], lo = llo[q], len = llen[q];
+        const VT Pj = lP[q];
+        VT bv;
+        int bs;
+        warp_row_min(b, Pj, lo, lo + len - 1, bv, bs);
+        if (lane == 0) {
+          c.sopt[j] = (uint16_t)bs;
+          c.optout[j] = (uint16_t)bs;
+          c.bnext[j + 1] = icpt(bv, j + 1, Pj);
+        }
+      }
+      __syncwarp();
+#ifdef SP_TIMING
+      t_long += clock64() - t2;
+#endif
+    }
+  }
+  nev += nv;
+#ifdef SP_TIMING
+  if (lane == 0) {
+    atomicAdd(&sh.tclk[7], (unsigned long long)t_long);
+    atomicAdd(&sh.tclk[6], (unsigned long long)t_pass);   // tclk[6] is reused below as max
+  }
+#endif
 }
 
 // ---- TMA bulk copy global -> shared (cp.async.bulk, completion on an mbarrier) ---------------
@@ -405,7 +861,13 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
   VT* bnext = bB;
   // layer 1: e_0 == 0 => b_s = s P_{s-1}
   for (int s = threadIdx.x + 1; s <= N; s += DP_NT) b[s] = icpt((VT)0, s, (VT)P[s - 1]);
-  if (threadIdx.x < 3) sh.ctr[threadIdx.x] = 0;
+  if (threadIdx.x < 3) {
+    sh.ctr[threadIdx.x] = 0;
+    sh.nmulti[threadIdx.x] = 0;
+  }
+  // sopt[0] = 1 is the virtual row 0 (lower bound 1); sopt[j] = 1 makes the layer bound
+  // max(., opt_{m-1}(j)) a no-op in layer 1
+  for (int j = threadIdx.x; j <= N; j += DP_NT) sopt[j] = 1;
   __syncthreads();
 
   LayerCtx<VT, PT, CT> c;
@@ -418,6 +880,15 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
   c.err = &sh.err;
   unsigned long long nev = 0;
   int lvl = 0;
+  // top levels: every level whose rows are multiples of h0 = SEG_ROWS (or all levels if N is small)
+  int K0 = p.L;
+  if (N >= 2 * SEG_ROWS) K0 = p.L - 31 + __clz(SEG_ROWS);   // 2^(L-K0) = SEG_ROWS
+  const int h0 = 1 << (p.L - K0);
+  VT* topP = reinterpret_cast<VT*>(sh.topP);
+  const bool use_topP = K0 < p.L && N / h0 + 1 <= TOPP_CAP;
+  if (use_topP)
+    for (int k = threadIdx.x; k <= N / h0; k += DP_NT) topP[k] = (VT)P[k * h0];
+  __syncthreads();
   for (int m = 1; m <= M; ++m) {
     c.b = b;
     c.bnext = bnext;
@@ -425,11 +896,45 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
     c.last = (m == M);
     c.optout = opt + (size_t)(m - 1) * (N + 1);
     c.optprev = m >= 2 ? opt + (size_t)(m - 2) * (N + 1) : nullptr;
-    for (int k = 0; k < p.L; ++k, ++lvl) {
+    SP_T0();
+    solve_row_N<VT>(c, sh, nev);
+    SP_TICK(sh, 0);
+    // top levels: CTA-cooperative (few rows, long brackets)
+    for (int k = 0; k < K0; ++k, ++lvl) {
       const int h = 1 << (p.L - 1 - k);
       const int R = ((N / h) + 1) >> 1;
-      run_level<VT>(c, sh, S, h, R, lvl, nev);
+      if (R <= TOPR) {
+        if (use_topP) top_level<VT>(c, sh, scratch, topP, h0, h, R, lvl, nev);
+        else top_level<VT>(c, sh, scratch, P, 1, h, R, lvl, nev);   // P straight from L2
+      } else {
+        run_level<VT>(c, sh, S, h, R, lvl, nev);
+      }
     }
+    SP_TICK(sh, 1);
+    // the rest: warp-owned segments
+    if (K0 < p.L) {
+      if (threadIdx.x == 0) sh.segctr = 0;
+      __syncthreads();
+#ifdef SP_TIMING
+      const long long ts = clock64();
+#endif
+      run_segments<VT>(c, sh, scratch, p.L, K0, nev);
+#ifdef SP_TIMING
+      if (lane_id() == 0) {   // per-warp busy time in the segment phase (imbalance)
+        const unsigned long long d = (unsigned long long)(clock64() - ts);
+        atomicAdd(&sh.tclk[4], d);
+        atomicMax(&sh.tclk[8], d);
+      }
+#endif
+      __syncthreads();
+#ifdef SP_TIMING
+      if (threadIdx.x == 0) {
+        sh.tclk[5] += sh.tclk[8];
+        sh.tclk[8] = 0;
+      }
+#endif
+    }
+    SP_TICK(sh, 2);
     if (m < M) {
       if (threadIdx.x == 0) bnext[1] = 0;   // e_m(0) + 1 * P_0 = 0
       if constexpr (BS) {
@@ -442,6 +947,7 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
       }
       __syncthreads();
     }
+    SP_TICK(sh, 3);
   }
   atomicAdd(&sh.evals, nev);
 }
@@ -565,7 +1071,7 @@ __host__ __device__ __forceinline__ size_t dyn_smem_bytes(int N, bool smem_b) {
 }
 
 template <typename WT>
-__global__ void __launch_bounds__(DP_NT) dp_place_kernel(DpParams p) {
+__global__ void __launch_bounds__(DP_NT, 1) dp_place_kernel(DpParams p) {
   using PT = typename WTraits<WT>::PT;
   using CT = typename WTraits<WT>::CT;
   constexpr bool F64 = sizeof(WT) == 8 && std::is_floating_point<WT>::value;
@@ -581,6 +1087,7 @@ __global__ void __launch_bounds__(DP_NT) dp_place_kernel(DpParams p) {
   CT* cost = reinterpret_cast<CT*>(p.cost);
   CT* cbb = reinterpret_cast<CT*>(p.cbb);
   unsigned phase = 0;   // TMA mbarrier parity, identical in every thread
+  if (threadIdx.x < 10) sh.tclk[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     const unsigned mb = (unsigned)__cvta_generic_to_shared(&sh.mbar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
@@ -681,6 +1188,9 @@ __global__ void __launch_bounds__(DP_NT) dp_place_kernel(DpParams p) {
     }
     __syncthreads();
   }
+#ifdef SP_TIMING
+  if (threadIdx.x < 8) atomicAdd(reinterpret_cast<unsigned long long*>(p.ws) + 8 + threadIdx.x, sh.tclk[threadIdx.x]);
+#endif
 }
 
 }  // namespace sp

@@ -12,7 +12,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsparseprefix.so")
+LIB_PATH = os.environ.get("SP_LIB") or os.path.join(_HERE, "libsparseprefix.so")
 
 SP_OK = 0
 SP_ERR_BAD_LENGTH = 1

@@ -40,3 +40,11 @@ if a.lcp:
         sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], tr["req_tokens"], tr["req_off"],
                         tr["req_entry"], cfg.N, hist=hist, lcp_out=lcp)
     torch.cuda.synchronize()
+if os.environ.get("SP_TIMING_REPORT"):
+    v = ws[:128].view(torch.int64).cpu().tolist()
+    names = ["rowN", "top", "segments(+barrier)", "reload", "seg warp busy (sum)", "seg max-warp busy (sum)", "seg passes (warp sum)", "seg long rows (warp sum)"]
+    tot = sum(v[8:12])
+    for i, nm in enumerate(names[:8]):
+        print(f"  {nm:28s} {v[8+i]/1e6:10.2f} Mcyc  ({v[8+i]/max(tot,1)*100:5.1f}% of phase total)" if i < 4 else f"  {nm:28s} {v[8+i]/1e6:10.2f} Mcyc")
+    nw = 32
+    print(f"  segment phase: mean warp busy / max warp busy = {v[12]/nw/max(v[13],1):.2f}")

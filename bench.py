@@ -294,18 +294,10 @@ def run_ours(args):
     lcp_bytes = 4 * tokens_examined + 4 * int(ent_max.sum()) + R * (4 + 16 + 16 + 4 + 4)
 
     lcp = torch.full((max(R, 1),), -1, dtype=torch.int32, device=dev)
+    merger = None
     if world > 1:
-        Rmax_t = torch.tensor([R], device=dev)
-        dist.all_reduce(Rmax_t, op=dist.ReduceOp.MAX)
-        Rmax = int(Rmax_t)
-        ent_pad = torch.full((Rmax,), -1, dtype=torch.int32, device=dev)
-        ent_pad[:R] = tr["req_entry"]
-        lcp_pad = torch.full((Rmax,), -1, dtype=torch.int32, device=dev)
-        g_ent = torch.empty(world * Rmax, dtype=torch.int32, device=dev)
-        g_lcp = torch.empty(world * Rmax, dtype=torch.int32, device=dev)
-        dist.all_gather_into_tensor(g_ent, ent_pad)
-        if args.merge == "allreduce":
-            partial = torch.zeros(E_tot, N + 1, dtype=torch.int32, device=dev)
+        from paper_2605_05219_b200.dist import HistMerger
+        merger = HistMerger(tr["req_entry"], E_own, N, mode=args.merge)
 
     stream = torch.cuda.current_stream(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -321,21 +313,16 @@ def run_ours(args):
                             N, hist=hist, lcp_out=lcp, n_entries=E_tot, stream=stream)
         elif args.merge == "sparse":
             sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], req_tokens, req_off, req_entry,
-                            N, lcp_out=lcp_pad, n_entries=E_tot, stream=stream, with_hist=False)
+                            N, lcp_out=merger.lcp_out, n_entries=E_tot, stream=stream,
+                            with_hist=False)
         else:
-            partial.zero_()
             sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], req_tokens, req_off, req_entry,
-                            N, hist=partial, lcp_out=lcp, n_entries=E_tot, stream=stream)
+                            N, hist=merger.partial, lcp_out=lcp, n_entries=E_tot, stream=stream)
         if marks:
             marks[1].record(stream)
-        # merge (the one exchange step)
+        # merge (the one exchange step; paper_2605_05219_b200.dist)
         if world > 1:
-            if args.merge == "sparse":
-                dist.all_gather_into_tensor(g_lcp, lcp_pad)
-                sp.accumulate_depths(g_ent, g_lcp, e0, e1, N, hist, stream=stream)
-            else:
-                dist.all_reduce(partial)
-                hist.add_(partial[e0:e1])
+            merger.merge(hist, stream=stream)
         if marks:
             marks[2].record(stream)
         # a3 - a5
@@ -444,6 +431,12 @@ def run_ours(args):
     # (ISETP + 2 SEL); the ALU pipe issues 64 lanes/clk/SM (16/clk/SMSP) => peak
     # = SMs * f_max * 64 / 3 evaluations/s.
     evals_per_launch = stats["evaluations"]          # exact, from the kernel's own counter
+    traffic = {}
+    try:   # DRAM bytes per launch from the committed `ncu --set full` capture (W5 config)
+        if args.workload == "W5" and E_own == 16384:
+            traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+    except Exception:
+        traffic = {}
     dp_launch_s = dp_ms / K / 1e3
     achieved = evals_per_launch / dp_launch_s / 1e9
     peak = sms * sm_max * 1e6 * 64 / 3 / 1e9
@@ -458,7 +451,7 @@ def run_ours(args):
                               "eval": eval_ms / K},
         "roofline": {"bound": "alu", "kernel": "dp_place_kernel", "achieved": achieved,
                      "peak": peak, "unit": "Geval/s", "frac": achieved / peak,
-                     "traffic": None,
+                     "traffic": traffic.get("dp_place_kernel<int>", {}).get("traffic_bytes"),
                      "work": f"{evals_per_launch} candidate evaluations per launch "
                              f"({evals_per_launch / (E_own * N * M):.2f} per DP cell)",
                      "peak_basis": f"{sms} SMs x {sm_max:.0f} MHz x 64 ALU lanes / 3 ops"},
@@ -466,7 +459,8 @@ def run_ours(args):
                          "achieved": lcp_bytes_all * K / (lcp_ms / 1e3) / 1e9 / world,
                          "peak": hbm_peak, "unit": "GB/s",
                          "frac": lcp_bytes_all * K / (lcp_ms / 1e3) / 1e9 / world / hbm_peak,
-                         "traffic": None},
+                         "traffic": traffic.get("lcp_hist_kernel", {}).get("traffic_bytes"),
+                         "algorithmic_bytes": lcp_bytes_all / world},
         "dp_paths": {k: v for k, v in stats.items() if k != "evaluations"},
         "gpu_launches": K * (3 + (1 if world > 1 and args.merge == "sparse" else 0)),
         "clocks": clk,

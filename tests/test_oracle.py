@@ -407,3 +407,54 @@ def test_lcp_clamp_and_misses():
     hist, lcp = oracle.lcp_hist(ent, eoff, req, roff, np.zeros(3, np.int32), N=4)
     assert lcp.tolist() == [4, 0, 2]
     assert hist[0].tolist() == [1, 0, 1, 0, 1]
+
+
+# ------------------------------------------------------------------------------------------
+# structural properties the CUDA D&C relies on (readings R6 / SURVEY F2)
+# ------------------------------------------------------------------------------------------
+
+
+def _structure_cases():
+    cases = []
+    for key in range(120):
+        N = 5 + (key * 37) % 180
+        z = [0.0, 0.3, 0.7, 0.95][key % 4]
+        cases.append(wl.random_small_hist(41, N, max_count=9, zero_frac=z, key=key).numpy())
+    for N in (33, 100, 257):
+        c = np.ones(N + 1, np.int64)
+        c[0] = 0
+        cases.append(c)
+    cfg = wl.TraceConfig("s", 6, 700, 12, 1, (700, 700), (1, 1), "uniform", dense_n=(300, 2000))
+    cases += list(wl.make_dense_hist(cfg, seed=8).numpy().astype(np.int64))
+    return cases
+
+
+def test_leftmost_argmin_monotone_across_layers():
+    """opt_{m-1}(j) <= opt_m(j) for the leftmost argmins (used by the kernel as a lower bracket
+    bound; the kernel also flags any empty bracket as SP_ERR_INTERNAL)."""
+    for c in _structure_cases():
+        N = len(c) - 1
+        M = min(N, 16)
+        _, O = oracle.dp(c, M, "cht")
+        for m in range(2, M + 1):
+            assert (O[m, 1:] >= O[m - 1, 1:]).all(), (N, m)
+
+
+def test_dp_monge_in_budget_and_prefix():
+    """dp[k][a] + dp[k+1][b] <= dp[k][b] + dp[k+1][a] for a < b (the marginal value of one more
+    checkpoint grows with the prefix), the property behind the layer monotonicity above."""
+    for c in _structure_cases()[::3]:
+        N = len(c) - 1
+        M = min(N, 10)
+        D, _ = oracle.dp(c, M, "cht")
+        for k in range(0, M):
+            d = D[k] - D[k + 1]            # non-decreasing in the prefix length
+            assert (np.diff(d) >= 0).all(), (N, k)
+
+
+def test_row_argmin_monotone_in_j_sparse():
+    """SURVEY F2 on sparse/zero-heavy histograms too: opt_m(j) non-decreasing in j."""
+    for c in _structure_cases():
+        N = len(c) - 1
+        _, O = oracle.dp(c, min(N, 12), "cht")
+        assert (np.diff(O[1:, 1:], axis=1) >= 0).all()

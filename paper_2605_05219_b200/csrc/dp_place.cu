@@ -118,8 +118,10 @@ __host__ __device__ __forceinline__ size_t align256(size_t x) { return (x + 255)
 // workspace slot layout (bytes):
 //   P 8B[N+1] | bA 8B[N+1] | bB 8B[N+1] | opt uint16[M][N+1] | P32 int32[N+1]
 __host__ __device__ __forceinline__ size_t slot_opt_off(int N) { return 3 * align256(8 * (size_t)(N + 1)); }
+// argmin-table row stride: N+1 rounded up to 8 entries so every row is 16-byte aligned
+__host__ __device__ __forceinline__ int opt_ld(int N) { return (N + 1 + 7) & ~7; }
 __host__ __device__ __forceinline__ size_t slot_p32_off(int N, int M) {
-  return slot_opt_off(N) + align256(2 * (size_t)(M > 0 ? M : 1) * (N + 1));
+  return slot_opt_off(N) + align256(2 * (size_t)(M > 0 ? M : 1) * opt_ld(N));
 }
 __host__ __device__ __forceinline__ size_t slot_bytes(int N, int M) {
   return slot_p32_off(N, M) + align256(4 * (size_t)(N + 1));
@@ -138,6 +140,7 @@ struct DpParams {
 };
 
 constexpr int TOPP_CAP = 160;
+constexpr int TQCAP = 2048;   // task-pool slots
 #ifdef SP_TIMING
 #define SP_T0() long long _t = clock64()
 #define SP_TICK(sh, i)                                                  \
@@ -156,6 +159,8 @@ struct Shared {
   unsigned long long tclk[10];    // SP_TIMING: per-phase cycles of this CTA
   unsigned long long ctr[3];      // per-level queue counters (triple-buffered)
   int segctr;                     // next segment to grab
+  int tq[TQCAP];                  // task pool slots (-1 = not yet pushed)
+  int tq_head, tq_tail, tq_total;
   int nmulti[3];                  // queued rows with more than one piece
   unsigned long long evals;
   int64_t wbuf[DP_NW + 1];
@@ -293,6 +298,18 @@ __device__ __forceinline__ void eval_short(const VT* __restrict__ b, VT Pj, int 
   bs = arg;
 }
 
+// The argmin table row of a layer is copied from shared memory by one TMA bulk store at the end
+// of the layer (cp.async.bulk shared -> global), not by a scattered 2-byte store per row.
+#ifndef SP_OPT_PER_ROW
+constexpr bool kOptBulk = true;
+#else
+constexpr bool kOptBulk = false;
+#endif
+template <typename Ctx>
+__device__ __forceinline__ void put_opt(const Ctx& c, int j, int v) {
+  if constexpr (!kOptBulk) c.optout[j] = (uint16_t)v;
+}
+
 template <typename VT, typename Ctx>
 __device__ __forceinline__ void row_write(const Ctx& c, int j, int lo, int hi, VT Pj, VT bv,
                                           int bs) {
@@ -302,7 +319,7 @@ __device__ __forceinline__ void row_write(const Ctx& c, int j, int lo, int hi, V
     bv = 0;
   }
   c.sopt[j] = (uint16_t)bs;
-  c.optout[j] = (uint16_t)bs;
+  put_opt(c, j, bs);
   if (j < c.N) c.bnext[j + 1] = icpt(bv, j + 1, Pj);
   if (j == c.N) {
     const auto V = c.TN + bv;   // dp[m][N] = T_N + e_m(N)
@@ -489,6 +506,24 @@ __device__ __forceinline__ void warp_row_min(const VT* __restrict__ b, VT Pj, in
 template <>
 __device__ __forceinline__ void warp_row_min<int32_t>(const int32_t* __restrict__ b, int32_t Pj,
                                                       int lo, int hi, int32_t& bv, int& bs) {
+#ifdef SP_WRM_STRIDED
+  {   // lanes stride the candidates with a strict '<' (leftmost per lane), two REDUX
+    const int lane = lane_id();
+    int best = INT_MAX, arg = INT_MAX;
+#pragma unroll 2
+    for (int s = lo + lane; s <= hi; s += 32) {
+      const int v = b[s] - s * Pj;
+      if (v < best) {
+        best = v;
+        arg = s;
+      }
+    }
+    const int vmin = __reduce_min_sync(FULL, best);
+    bs = __reduce_min_sync(FULL, best == vmin ? arg : INT_MAX);
+    bv = vmin;
+    return;
+  }
+#endif
   const int lane = lane_id();
   int best = INT_MAX, arg = INT_MAX;
   const int a = min(hi + 1, (lo + 3) & ~3);        // first aligned candidate
@@ -658,7 +693,7 @@ __device__ void top_level(const Ctx& c, Shared& sh, uint8_t* scratch, const VT* 
         bv = 0;
       }
       c.sopt[j] = (uint16_t)bs;
-      c.optout[j] = (uint16_t)bs;
+      put_opt(c, j, bs);
       c.bnext[j + 1] = icpt(bv, j + 1, topP[j / h0]);
     }
   }
@@ -713,6 +748,103 @@ __device__ void solve_row_N(const Ctx& c, Shared& sh, unsigned long long& nev) {
 // counter) and solves their levels with __syncwarp only: lanes take rows; rows longer than TW are
 // deferred to a warp list and solved cooperatively (warp_row_min).  Warps overlap each other's
 // latencies.
+// Solve the subtree of one warp-owned segment (base, base + h0): levels K0..L-1 with
+// __syncwarp only (lanes take rows; rows longer than TW deferred to a warp list and solved
+// cooperatively with warp_row_min).
+template <typename VT, typename Ctx>
+__device__ void segment_body(const Ctx& c, uint8_t* scratch, int L, int K0, int seg,
+                             unsigned& nv
+#ifdef SP_TIMING
+                             , long long& t_pass, long long& t_long
+#endif
+                             ) {
+  const int N = c.N;
+  const int h0 = 1 << (L - K0);
+  const int lane = lane_id(), w = warp_id();
+  int* lj = reinterpret_cast<int*>(scratch) + w * 3 * WCAP;
+  int* llo = lj + WCAP;
+  int* llen = llo + WCAP;
+  VT* lP = reinterpret_cast<VT*>(reinterpret_cast<int*>(scratch) + DP_NW * 3 * WCAP) + w * WCAP;
+  const VT* __restrict__ b = c.b;
+  const uint16_t* sopt = c.sopt;
+    const int base = seg * h0;
+  for (int k = K0; k < L; ++k) {
+    const int h = 1 << (L - 1 - k);
+    const int nr = 1 << (k - K0);
+    int cnt = 0;
+#ifdef SP_TIMING
+    long long t1 = clock64();
+#endif
+    for (int i0 = 0; i0 < nr; i0 += 32) {
+      const int i = i0 + lane;
+      const int j = base + h * (2 * i + 1);
+      const bool valid = i < nr && j < N;   // row N is solved first
+      int lo = 1, hi = 0;
+      VT Pj = 0;
+      if (valid) {
+        lo = max((int)sopt[j - h], (int)sopt[j]);   // opt_m(j-h), opt_{m-1}(j)
+        hi = min((int)sopt[min(j + h, N)], j);
+        Pj = (VT)c.P[j];
+      }
+      fix_bracket((VT*)nullptr, lo, hi);
+      const int len = hi - lo + 1;
+      nv += valid ? (unsigned)len : 0u;
+      const bool lng = valid && len > TW;
+      const unsigned bal = __ballot_sync(FULL, lng);
+      const int pos = cnt + __popc(bal & ((1u << lane) - 1));
+      cnt += __popc(bal);
+      if (lng && pos < WCAP) {
+        lj[pos] = j;
+        llo[pos] = lo;
+        llen[pos] = len;
+        lP[pos] = Pj;
+      }
+      if (valid && (!lng || pos >= WCAP)) {   // short row, or the list is full
+        VT best = Lim<VT>::inf();
+        int arg = INT_MAX;
+#pragma unroll 1
+        for (int s = lo; s <= hi; ++s) {
+          const VT v = cand(b[s], s, Pj);
+          if (v < best) {
+            best = v;
+            arg = s;
+          }
+        }
+        if (arg == INT_MAX) {   // empty bracket: never expected (reading R6 self-check)
+          atomicExch(c.err, SP_ERR_INTERNAL);
+          arg = max(1, min(lo, j));
+          best = 0;
+        }
+        c.sopt[j] = (uint16_t)arg;
+        put_opt(c, j, arg);
+        c.bnext[j + 1] = icpt(best, j + 1, Pj);
+      }
+    }
+    cnt = min(cnt, WCAP);
+    __syncwarp();
+#ifdef SP_TIMING
+    long long t2 = clock64();
+    t_pass += t2 - t1;
+#endif
+    for (int q = 0; q < cnt; ++q) {
+      const int j = lj[q], lo = llo[q], len = llen[q];
+      const VT Pj = lP[q];
+      VT bv;
+      int bs;
+      warp_row_min(b, Pj, lo, lo + len - 1, bv, bs);
+      if (lane == 0) {
+        c.sopt[j] = (uint16_t)bs;
+        put_opt(c, j, bs);
+        c.bnext[j + 1] = icpt(bv, j + 1, Pj);
+      }
+    }
+    __syncwarp();
+#ifdef SP_TIMING
+    t_long += clock64() - t2;
+#endif
+  }
+  }
+
 template <typename VT, typename Ctx>
 __device__ void run_segments(const Ctx& c, Shared& sh, uint8_t* scratch, int L, int K0,
                              unsigned long long& nev) {
@@ -770,6 +902,7 @@ __device__ void run_segments(const Ctx& c, Shared& sh, uint8_t* scratch, int L, 
         if (valid && (!lng || pos >= WCAP)) {   // short row, or the list is full
           VT best = Lim<VT>::inf();
           int arg = INT_MAX;
+#pragma unroll 1
           for (int s = lo; s <= hi; ++s) {
             const VT v = cand(b[s], s, Pj);
             if (v < best) {
@@ -783,7 +916,7 @@ __device__ void run_segments(const Ctx& c, Shared& sh, uint8_t* scratch, int L, 
             best = 0;
           }
           c.sopt[j] = (uint16_t)arg;
-          c.optout[j] = (uint16_t)arg;
+          put_opt(c, j, arg);
           c.bnext[j + 1] = icpt(best, j + 1, Pj);
         }
       }
@@ -801,7 +934,7 @@ __device__ void run_segments(const Ctx& c, Shared& sh, uint8_t* scratch, int L, 
         warp_row_min(b, Pj, lo, lo + len - 1, bv, bs);
         if (lane == 0) {
           c.sopt[j] = (uint16_t)bs;
-          c.optout[j] = (uint16_t)bs;
+          put_opt(c, j, bs);
           c.bnext[j + 1] = icpt(bv, j + 1, Pj);
         }
       }
@@ -816,6 +949,90 @@ __device__ void run_segments(const Ctx& c, Shared& sh, uint8_t* scratch, int L, 
   if (lane == 0) {
     atomicAdd(&sh.tclk[7], (unsigned long long)t_long);
     atomicAdd(&sh.tclk[6], (unsigned long long)t_pass);   // tclk[6] is reused below as max
+  }
+#endif
+}
+
+// ---- the dynamic task pool (replaces barrier-synchronous top levels) -------------------------
+// A task is an interval (a, a + 2^lg) whose endpoints a and a + 2^lg (or N) are solved.  Internal
+// tasks (2^lg > h0) solve their mid row a + 2^(lg-1) with one warp (warp_row_min: REDUX argmin)
+// and push both halves; segment tasks (2^lg == h0) solve their whole subtree (segment_body).
+// Node (a, 2^lg) exists iff a + 1 < N, so the number of tasks per layer is known up front and a
+// warp pops indices until they run out, spinning (nanosleep) on slots whose parent has not
+// finished yet.  A popped task's parent is always being processed by a non-spinning warp, so the
+// pool cannot deadlock.  Release/acquire through __threadfence_block + volatile slots.
+__device__ __forceinline__ int task_count(int N, int L, int lg0) {
+  int T = 0;
+  for (int lg = lg0; lg <= L; ++lg) T += ((N - 2) >> lg) + 1;
+  return T;
+}
+
+template <typename VT, typename Ctx>
+__device__ void run_tasks(const Ctx& c, Shared& sh, uint8_t* scratch, int L, int K0,
+                          unsigned long long& nev) {
+  const int N = c.N, lane = lane_id();
+  const int lg0 = L - K0;   // segment length h0 = 2^lg0
+  volatile int* tq = sh.tq;
+  const int total = sh.tq_total;
+  unsigned nv = 0;
+#ifdef SP_TIMING
+  long long t_pass = 0, t_long = 0;
+#endif
+  for (;;) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(&sh.tq_head, 1);
+    idx = __shfl_sync(FULL, idx, 0);
+    if (idx >= total) break;
+    int code = 0;
+    if (lane == 0) {
+      while ((code = tq[idx]) < 0) __nanosleep(20);
+    }
+    code = __shfl_sync(FULL, code, 0);
+    __threadfence_block();   // acquire: the parent's rows are visible
+    const int a = code >> 5, lg = code & 31;
+    if (lg == lg0) {
+      segment_body<VT>(c, scratch, L, K0, a >> lg0, nv
+#ifdef SP_TIMING
+                       , t_pass, t_long
+#endif
+      );
+      continue;
+    }
+    const int h = 1 << (lg - 1);
+    const int mid = a + h;
+    if (mid < N) {   // (mid == N is solved first; mid > N does not exist)
+      const int lo = max((int)c.sopt[a], (int)c.sopt[mid]);   // opt_m(a), opt_{m-1}(mid)
+      const int hi = min((int)c.sopt[min(a + 2 * h, N)], mid);
+      const VT Pj = (VT)c.P[mid];
+      VT bv;
+      int bs;
+      warp_row_min(c.b, Pj, lo, hi, bv, bs);
+      if (lane == 0) {
+        nv += (unsigned)max(hi - lo + 1, 0);
+        if (bs == INT_MAX) {   // empty bracket: never expected (reading R6 self-check)
+          atomicExch(c.err, SP_ERR_INTERNAL);
+          bs = max(1, min(lo, mid));
+          bv = 0;
+        }
+        c.sopt[mid] = (uint16_t)bs;
+        put_opt(c, mid, bs);
+        c.bnext[mid + 1] = icpt(bv, mid + 1, Pj);
+      }
+    }
+    if (lane == 0) {
+      __threadfence_block();   // release: the mid row before the children become ready
+      const bool left = a + 1 < N, right = mid + 1 < N;
+      int t = atomicAdd(&sh.tq_tail, (int)left + (int)right);
+      if (left) tq[t++] = (a << 5) | (lg - 1);
+      if (right) tq[t] = (mid << 5) | (lg - 1);
+    }
+    __syncwarp();
+  }
+  nev += nv;
+#ifdef SP_TIMING
+  if (lane == 0) {
+    atomicAdd(&sh.tclk[7], (unsigned long long)t_long);
+    atomicAdd(&sh.tclk[6], (unsigned long long)t_pass);
   }
 #endif
 }
@@ -886,6 +1103,12 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
   const int h0 = 1 << (p.L - K0);
   VT* topP = reinterpret_cast<VT*>(sh.topP);
   const bool use_topP = K0 < p.L && N / h0 + 1 <= TOPP_CAP;
+  const int tq_total = K0 < p.L ? task_count(N, p.L, p.L - K0) : 0;
+#ifdef SP_NO_TASKS
+  const bool use_tasks = false;
+#else
+  const bool use_tasks = tq_total <= TQCAP;
+#endif
   if (use_topP)
     for (int k = threadIdx.x; k <= N / h0; k += DP_NT) topP[k] = (VT)P[k * h0];
   __syncthreads();
@@ -894,11 +1117,40 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
     c.bnext = bnext;
     c.m = m;
     c.last = (m == M);
-    c.optout = opt + (size_t)(m - 1) * (N + 1);
-    c.optprev = m >= 2 ? opt + (size_t)(m - 2) * (N + 1) : nullptr;
+    c.optout = opt + (size_t)(m - 1) * opt_ld(N);
+    c.optprev = m >= 2 ? opt + (size_t)(m - 2) * opt_ld(N) : nullptr;
     SP_T0();
     solve_row_N<VT>(c, sh, nev);
     SP_TICK(sh, 0);
+    if (K0 < p.L && use_tasks) {
+      // dynamic task pool: top-level rows and warp-owned segments, no barriers in between
+      for (int t = threadIdx.x; t < tq_total; t += DP_NT) sh.tq[t] = t == 0 ? (0 << 5) | p.L : -1;
+      if (threadIdx.x == 0) {
+        sh.tq_head = 0;
+        sh.tq_tail = 1;
+        sh.tq_total = tq_total;
+      }
+      __syncthreads();
+#ifdef SP_TIMING
+      const long long ts = clock64();
+#endif
+      run_tasks<VT>(c, sh, scratch, p.L, K0, nev);
+#ifdef SP_TIMING
+      if (lane_id() == 0) {
+        const unsigned long long d = (unsigned long long)(clock64() - ts);
+        atomicAdd(&sh.tclk[4], d);
+        atomicMax(&sh.tclk[8], d);
+      }
+#endif
+      __syncthreads();
+#ifdef SP_TIMING
+      if (threadIdx.x == 0) {
+        sh.tclk[5] += sh.tclk[8];
+        sh.tclk[8] = 0;
+      }
+#endif
+      SP_TICK(sh, 2);
+    } else {
     // top levels: CTA-cooperative (few rows, long brackets)
     for (int k = 0; k < K0; ++k, ++lvl) {
       const int h = 1 << (p.L - 1 - k);
@@ -935,6 +1187,18 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
 #endif
     }
     SP_TICK(sh, 2);
+    }
+    if (kOptBulk && threadIdx.x == 0) {   // every row of the layer is in sopt (barrier above)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(c.optout),
+                   "r"((unsigned)__cvta_generic_to_shared(sopt)), "r"((unsigned)(2 * opt_ld(N)))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (m == M) {   // the backtrack (thread 0) reads the table next
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+    }
     if (m < M) {
       if (threadIdx.x == 0) bnext[1] = 0;   // e_m(0) + 1 * P_0 = 0
       if constexpr (BS) {
@@ -945,6 +1209,8 @@ __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t*
         b = bnext;
         bnext = t;
       }
+      // sopt is rewritten by the next layer only after the bulk store has read it
+      if (kOptBulk && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncthreads();
     }
     SP_TICK(sh, 3);
@@ -1161,7 +1427,7 @@ __global__ void __launch_bounds__(DP_NT, 1) dp_place_kernel(DpParams p) {
         const uint16_t* opt = reinterpret_cast<const uint16_t*>(slot + slot_opt_off(N));
         int j = N, m = M;
         while (m > 0 && P[j] > 0) {
-          const int s = opt[(size_t)(m - 1) * (N + 1) + j];
+          const int s = opt[(size_t)(m - 1) * opt_ld(N) + j];
           out[k++] = s;
           j = s - 1;
           --m;

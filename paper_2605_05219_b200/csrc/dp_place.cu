@@ -328,6 +328,22 @@ __device__ __forceinline__ void row_write(const Ctx& c, int j, int lo, int hi, V
   }
 }
 
+// SP_DEBUG builds check every bracket before it is scanned (1 <= lo <= hi <= j < N, the bound
+// rows already solved) and flag the entry (n_positions = -SP_ERR_INTERNAL) instead of reading
+// out of range; compute-sanitizer is not available on this pool.
+#ifdef SP_DEBUG
+#define SP_CHECK_BRACKET(c, j, lo, hi)                                                  \
+  do {                                                                                 \
+    if (!((lo) >= 1 && (lo) <= (hi) && (hi) <= (j) && (j) <= (c).N)) {                 \
+      atomicExch((c).err, SP_ERR_INTERNAL);                                            \
+      (lo) = 1;                                                                        \
+      (hi) = 0;                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define SP_CHECK_BRACKET(c, j, lo, hi) (void)0
+#endif
+
 // fp64: rounding can make neighbouring brackets cross by a hair; clamp instead of flagging
 __device__ __forceinline__ void fix_bracket(double*, int& lo, int hi) {
   if (lo > hi) lo = hi;
@@ -787,6 +803,7 @@ __device__ void segment_body(const Ctx& c, uint8_t* scratch, int L, int K0, int 
         Pj = (VT)c.P[j];
       }
       fix_bracket((VT*)nullptr, lo, hi);
+      if (valid) SP_CHECK_BRACKET(c, j, lo, hi);
       const int len = hi - lo + 1;
       nv += valid ? (unsigned)len : 0u;
       const bool lng = valid && len > TW;
@@ -887,6 +904,7 @@ __device__ void run_segments(const Ctx& c, Shared& sh, uint8_t* scratch, int L, 
           Pj = (VT)c.P[j];
         }
         fix_bracket((VT*)nullptr, lo, hi);
+        if (valid) SP_CHECK_BRACKET(c, j, lo, hi);
         const int len = hi - lo + 1;
         nv += valid ? (unsigned)len : 0u;
         const bool lng = valid && len > TW;
@@ -1001,8 +1019,9 @@ __device__ void run_tasks(const Ctx& c, Shared& sh, uint8_t* scratch, int L, int
     const int h = 1 << (lg - 1);
     const int mid = a + h;
     if (mid < N) {   // (mid == N is solved first; mid > N does not exist)
-      const int lo = max((int)c.sopt[a], (int)c.sopt[mid]);   // opt_m(a), opt_{m-1}(mid)
-      const int hi = min((int)c.sopt[min(a + 2 * h, N)], mid);
+      int lo = max((int)c.sopt[a], (int)c.sopt[mid]);   // opt_m(a), opt_{m-1}(mid)
+      int hi = min((int)c.sopt[min(a + 2 * h, N)], mid);
+      SP_CHECK_BRACKET(c, mid, lo, hi);
       const VT Pj = (VT)c.P[mid];
       VT bv;
       int bs;

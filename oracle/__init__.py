@@ -58,6 +58,10 @@ def lib():
         L.or_dp_naive_f64.argtypes = [_f64p, _c_i32, _c_i32, _f64p, _i32p]
         L.or_expected_cost_f64.argtypes = [_f64p, _c_i32, _i32p, _c_i32]
         L.or_expected_cost_f64.restype = ctypes.c_double
+        L.or_dp_grid_naive.argtypes = [_i64p, _c_i32, _c_i32, _c_i32, _i64p, _i32p]
+        L.or_clip_to_blocks.argtypes = [_i32p, _c_i32, _c_i32, _i32p]
+        L.or_sqrt_positions.argtypes = [_c_i32, _i32p]
+        L.or_log_positions.argtypes = [_c_i32, _c_i32, _i32p]
         L.or_place_batch.argtypes = [_i32p, _c_i32, _c_i32, _c_i32, _c_int, _i32p, _i32p, _i64p,
                                      _vp, _c_int]
         L.or_eval_batch.argtypes = [_i32p, _c_i32, _c_i32, _i32p, _i32p, _c_i32, _c_i32, _c_int,
@@ -213,3 +217,43 @@ def eval_batch(hist, positions, n_positions, broadcast=True, nthreads=1):
     _check(lib().or_eval_batch(hist, E, W - 1, positions, n_positions, S, max_pos,
                                1 if broadcast else 0, cost, _ptr(worst), nthreads), "eval_batch")
     return cost, worst
+
+
+def place_grid(c, M, B):
+    """Block-restricted DP (S:206-214 candidate_grid): positions in multiples of B.  Backtrack:
+    leftmost argmin, stopping as soon as no checkpoint improves the remaining prefix
+    (dp[m][j] == dp[0][j] = T_j) -- the colex-minimal optimum; for the unrestricted DP this is
+    exactly rule B's P_j = 0 stop (reading R13)."""
+    c = _counts(c)
+    N = c.size - 1
+    D = np.zeros((M + 1) * (N + 1), np.int64)
+    O = np.zeros((M + 1) * (N + 1), np.int32)
+    _check(lib().or_dp_grid_naive(c, N, M, B, D, O), "dp_grid")
+    D, O = D.reshape(M + 1, N + 1), O.reshape(M + 1, N + 1)
+    P, _ = prefix(c)
+    pos, j, m = [], N, M
+    while m > 0 and D[m, j] < D[0, j]:
+        s = int(O[m, j])
+        pos.append(s)
+        j, m = s - 1, m - 1
+    return np.asarray(pos[::-1], np.int32), int(D[M, N]), D[:, N].copy()
+
+
+def clip_to_blocks(pos, B):
+    pos = np.ascontiguousarray(pos, dtype=np.int32)
+    out = np.zeros(max(pos.size, 1), np.int32)
+    k = lib().or_clip_to_blocks(pos if pos.size else np.zeros(1, np.int32), pos.size, B, out)
+    return out[:k].copy()
+
+
+def sqrt_positions(N):
+    out = np.zeros(N, np.int32)
+    return out[:lib().or_sqrt_positions(N, out)].copy()
+
+
+def log_positions(N, M):
+    out = np.zeros(max(M, 1), np.int32)
+    k = lib().or_log_positions(N, M, out)
+    if k < 0:
+        raise ValueError("log_positions: bad N/M")
+    return out[:k].copy()

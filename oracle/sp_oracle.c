@@ -333,6 +333,78 @@ double or_expected_cost_f64(const double* w, int32_t N, const int32_t* pos, int3
 }
 
 /* ------------------------------------------------------------------------------------------ */
+/* f1: block-aware placement.  The block-restricted DP (S:206-214 candidate_grid) is Thm 2's   */
+/* recurrence with the last checkpoint s restricted to multiples of B; with the    */
+/* at-most reading R1 dp[m][0..B-1] is the no-checkpoint cost T_j.  Leftmost argmin as before.  */
+/* ------------------------------------------------------------------------------------------ */
+int or_dp_grid_naive(const int64_t* c, int32_t N, int32_t M, int32_t B, int64_t* dp, int32_t* opt) {
+  if (N < 1 || B < 1) return -1;
+  if (M < 0 || M > N) return -2;
+  int64_t* P = (int64_t*)malloc(sizeof(int64_t) * (size_t)(N + 1));
+  int64_t* T = (int64_t*)malloc(sizeof(int64_t) * (size_t)(N + 1));
+  if (!P || !T) { free(P); free(T); return -3; }
+  or_prefix(c, N, P, T);
+  const int64_t W = (int64_t)N + 1;
+  for (int32_t j = 0; j <= N; ++j) { dp[j] = T[j]; opt[j] = 0; }
+  for (int32_t m = 1; m <= M; ++m) {
+    for (int32_t j = 0; j <= N; ++j) {
+      if (j < B) {                  /* no grid position at or below j: no checkpoint usable */
+        dp[m * W + j] = T[j];
+        opt[m * W + j] = 0;
+        continue;
+      }
+      i128 best = 0;
+      int32_t arg = 0;
+      for (int32_t s = B; s <= j; s += B) {   /* leftmost argmin over grid candidates */
+        i128 w = (i128)(T[j] - T[s - 1]) - (i128)s * (P[j] - P[s - 1]);
+        i128 v = (i128)dp[(m - 1) * W + (s - 1)] + w;
+        if (arg == 0 || v < best) { best = v; arg = s; }
+      }
+      dp[m * W + j] = (int64_t)best;
+      opt[m * W + j] = arg;
+    }
+  }
+  free(P);
+  free(T);
+  return 0;
+}
+
+int or_clip_to_blocks(const int32_t* pos, int32_t k, int32_t B, int32_t* out) {
+  if (B < 1 || k < 0) return -1;
+  int32_t n = 0;
+  for (int32_t i = 0; i < k; ++i) {
+    int32_t f = (pos[i] / B) * B;            /* clip DOWN: a state above t cannot serve t */
+    if (f <= 0) continue;                   /* zeros dropped */
+    if (n > 0 && out[n - 1] == f) continue; /* duplicates merged (input ascending) */
+    out[n++] = f;
+  }
+  return n;
+}
+
+int or_sqrt_positions(int32_t N, int32_t* out) {
+  if (N < 1) return -1;
+  int32_t q = 1;
+  while ((int64_t)(q + 1) * (q + 1) <= N) ++q;   /* floor(sqrt(N)) */
+  return or_block(N, q, out);
+}
+
+int or_log_positions(int32_t N, int32_t M, int32_t* out) {
+  if (N < 1) return -1;
+  if (M < 1 || M > N || M > 62) return -2;
+  const i128 den = ((i128)1 << M) - 1;
+  int32_t n = 0;
+  for (int32_t i = 1; i <= M; ++i) {
+    const i128 num = (i128)N * (((i128)1 << i) - 1);
+    int64_t r = (int64_t)((2 * num + den) / (2 * den));   /* round half up */
+    if (r < 1) r = 1;
+    if (r > N) r = N;
+    if (n > 0 && out[n - 1] >= r) continue;
+    out[n++] = (int32_t)r;
+  }
+  return n;
+}
+
+/* ------------------------------------------------------------------------------------------ */
 /* Batched drivers: one entry at a time per thread (entries are independent problems,          */
 /* P:189-190).                                                                                  */
 /* ------------------------------------------------------------------------------------------ */

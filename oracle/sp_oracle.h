@@ -67,6 +67,18 @@ int or_dp_naive_f64(const double* w, int32_t N, int32_t M, double* dp, int32_t* 
 /* definitional fp64 objective, accumulated in long double. */
 double or_expected_cost_f64(const double* w, int32_t N, const int32_t* pos, int32_t k);
 
+/* f1 block-aware placement.
+ * or_dp_grid_naive: the recurrence of Thm 2 with candidate positions restricted to multiples of
+ *   B (the block-restricted DP of S:208): dp[m][j] = min over s in {B, 2B, ..} with s <= j.
+ * or_clip_to_blocks: floor each position to a multiple of B, drop zeros, merge duplicates.
+ * or_sqrt_positions: multiples of floor(sqrt(N)) up to N (Table 1).
+ * or_log_positions: round(N (2^i - 1) / (2^M - 1)), i = 1..M, clamped to [1, N], deduplicated
+ *   (SPEC's reading S:198 of P:358). Return the number of positions. */
+int or_dp_grid_naive(const int64_t* c, int32_t N, int32_t M, int32_t B, int64_t* dp, int32_t* opt);
+int or_clip_to_blocks(const int32_t* pos, int32_t k, int32_t B, int32_t* out);
+int or_sqrt_positions(int32_t N, int32_t* out);
+int or_log_positions(int32_t N, int32_t M, int32_t* out);
+
 /* Batched drivers (threaded across entries, pthreads) used by tests and the CPU baseline.
  * hist: int32 [E][N+1].  algo: 0 = naive, 1 = CHT.  pos [E][M] zero-padded, npos [E],
  * cost [E] (= dp[M][N]), cost_by_budget [E][M+1] or NULL. */

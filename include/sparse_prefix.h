@@ -145,10 +145,40 @@ sp_status sp_expected_recompute(const void* weights, sp_weight_type wtype, int32
                                 int32_t n_sets, int32_t max_pos, int32_t broadcast, void* cost,
                                 int32_t* worst_case, sp_stream_t stream);
 
+/* ------------------------------------------------------------------------------------------
+ * f1 -- block-aware placement ("clip every checkpoint position to the block boundaries",
+ * B = 128; P:397 B = 64).
+ *
+ * sp_place_checkpoints_grid: the exact DP with checkpoints restricted to multiples of B
+ * (S:208 candidate_grid).  Outputs as sp_place_checkpoints (positions are multiples of B; at
+ * most min(M, floor(N/B)) of them; cost = sum_t c_t (t - l(t;C)) exactly).  Computed as the
+ * unrestricted DP on the block-aggregated histogram C_k = sum_{t in [kB,(k+1)B)} c_t plus the
+ * placement-independent constant sum_t c_t (t - B floor(t/B)).  Canonical
+ * output: the colex-minimal optimal grid set (reading R13).  Errors as sp_place_checkpoints,
+ * plus BAD_ARGUMENT for B < 1.
+ * sp_clip_to_blocks: post-hoc clipping, per entry: floor(c / B) B, zeros dropped, duplicates
+ * merged; n_positions < 0 (a per-entry status) is passed through.
+ * ---------------------------------------------------------------------------------------- */
+size_t sp_place_checkpoints_grid_workspace_bytes(int32_t n_entries, int32_t N, int32_t M,
+                                                 int32_t B);
+sp_status sp_place_checkpoints_grid(const void* weights, sp_weight_type wtype, int32_t n_entries,
+                                    int32_t N, int32_t M, int32_t B, int32_t* positions,
+                                    int32_t* n_positions, void* cost, void* cost_by_budget,
+                                    void* workspace, size_t workspace_bytes, sp_stream_t stream);
+sp_status sp_clip_to_blocks(const int32_t* positions /*[E][max_pos]*/,
+                            const int32_t* n_positions /*[E]*/, int32_t n_entries,
+                            int32_t max_pos, int32_t B, int32_t* out_positions /*[E][max_pos]*/,
+                            int32_t* out_n /*[E]*/, sp_stream_t stream);
+
 /* Host-side helpers for the Table 1 baselines.  out_host must hold M (resp.
  * floor(N/B)) ints.  Return the number of positions written, or a negative sp_status. */
 int32_t sp_balanced_positions(int32_t N, int32_t M, int32_t* out_host);
 int32_t sp_block_positions(int32_t N, int32_t B, int32_t* out_host);
+/* sqrt(L) schedule: multiples of floor(sqrt(N)).  out_host holds N ints. */
+int32_t sp_sqrt_positions(int32_t N, int32_t* out_host);
+/* logarithmic schedule (SPEC's reading S:198): round(N (2^i - 1) / (2^M - 1)), i = 1..M,
+ * clamped to [1, N], duplicates dropped; 1 <= M <= min(N, 62).  out_host holds M ints. */
+int32_t sp_log_positions(int32_t N, int32_t M, int32_t* out_host);
 
 const char* sp_status_string(sp_status status);
 /* Last CUDA error text seen by this thread (static storage, never NULL). */

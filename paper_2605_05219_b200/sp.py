@@ -44,6 +44,12 @@ SYMBOLS = {
                                             _vp, _vp, _sz, _vp]),
     "sp_expected_recompute": (ctypes.c_int, [_vp, ctypes.c_int, _i32, _i32, _vp, _vp, _i32, _i32,
                                              _i32, _vp, _vp, _vp]),
+    "sp_place_checkpoints_grid_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32]),
+    "sp_place_checkpoints_grid": (ctypes.c_int, [_vp, ctypes.c_int, _i32, _i32, _i32, _i32, _vp,
+                                                 _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sp_clip_to_blocks": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "sp_sqrt_positions": (_i32, [_i32, _vp]),
+    "sp_log_positions": (_i32, [_i32, _i32, _vp]),
     "sp_balanced_positions": (_i32, [_i32, _i32, _vp]),
     "sp_block_positions": (_i32, [_i32, _i32, _vp]),
     "sp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
@@ -218,6 +224,66 @@ def block_positions(N, B):
     k = lib().sp_block_positions(N, B, buf)
     if k < 0:
         raise SPError(-k, "sp_block_positions")
+    return list(buf[:k])
+
+
+def place_checkpoints_grid(weights, M, B, positions=None, n_positions=None, cost=None,
+                           cost_by_budget=False, workspace=None, stream=None):
+    """f1: the exact DP with checkpoints restricted to multiples of B."""
+    wtype = _WTYPE.get(weights.dtype)
+    if wtype is None or weights.dim() != 2:
+        raise TypeError("weights must be [E][N+1] int32, int64 or float64")
+    E, N = weights.shape[0], weights.shape[1] - 1
+    dev = weights.device
+    cdt = torch.float64 if wtype == SP_W_PROB_F64 else torch.int64
+    if positions is None:
+        positions = torch.empty(E, max(M, 0), dtype=torch.int32, device=dev)
+    if n_positions is None:
+        n_positions = torch.empty(E, dtype=torch.int32, device=dev)
+    if cost is None:
+        cost = torch.empty(E, dtype=cdt, device=dev)
+    cbb = torch.empty(E, M + 1, dtype=cdt, device=dev) if cost_by_budget is True else (
+        cost_by_budget if isinstance(cost_by_budget, torch.Tensor) else None)
+    need = int(lib().sp_place_checkpoints_grid_workspace_bytes(E, N, M, B))
+    if workspace is None:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    st = lib().sp_place_checkpoints_grid(
+        _dev(weights, weights.dtype, "weights"), wtype, E, N, M, B,
+        _dev(positions, torch.int32, "positions") if M > 0 else None,
+        _dev(n_positions, torch.int32, "n_positions"), _dev(cost, cdt, "cost"),
+        None if cbb is None else _dev(cbb, cdt, "cost_by_budget"),
+        _dev(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream, dev))
+    _check(st, "sp_place_checkpoints_grid")
+    return positions, n_positions, cost, cbb
+
+
+def clip_to_blocks(positions, n_positions, B, out=None, out_n=None, stream=None):
+    """f1: floor every position to a multiple of B, drop zeros, merge duplicates."""
+    E, max_pos = positions.shape
+    dev = positions.device
+    out = torch.empty_like(positions) if out is None else out
+    out_n = torch.empty_like(n_positions) if out_n is None else out_n
+    st = lib().sp_clip_to_blocks(_dev(positions, torch.int32, "positions") if max_pos else None,
+                                 _dev(n_positions, torch.int32, "n_positions"), E, max_pos, B,
+                                 _dev(out, torch.int32, "out") if max_pos else None,
+                                 _dev(out_n, torch.int32, "out_n"), _stream(stream, dev))
+    _check(st, "sp_clip_to_blocks")
+    return out, out_n
+
+
+def sqrt_positions(N):
+    buf = (ctypes.c_int32 * max(N, 1))()
+    k = lib().sp_sqrt_positions(N, buf)
+    if k < 0:
+        raise SPError(-k, "sp_sqrt_positions")
+    return list(buf[:k])
+
+
+def log_positions(N, M):
+    buf = (ctypes.c_int32 * max(M, 1))()
+    k = lib().sp_log_positions(N, M, buf)
+    if k < 0:
+        raise SPError(-k, "sp_log_positions")
     return list(buf[:k])
 
 

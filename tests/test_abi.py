@@ -110,3 +110,13 @@ def test_product_never_imports_oracle():
             src = open(f).read()
             assert "import oracle" not in src and "from oracle" not in src, f
             assert "sp_oracle" not in src and "liboracle" not in src, f
+
+
+@pytest.mark.parametrize("N", [1, 3, 10, 100, 1000, 8192, 32768])
+def test_sqrt_helper_matches_oracle(L, N):
+    assert sp.sqrt_positions(N) == oracle.sqrt_positions(N).tolist()
+
+
+@pytest.mark.parametrize("N,M", [(7, 3), (50, 1), (4, 3), (8192, 16), (32768, 62), (100, 62)])
+def test_log_helper_matches_oracle(L, N, M):
+    assert sp.log_positions(N, M) == oracle.log_positions(N, M).tolist()

@@ -140,6 +140,21 @@ sp_status sp_place_checkpoints(const void* weights, sp_weight_type wtype, int32_
  * cost = -1 (count types) / NaN (F64) and worst = -SP_ERR_BAD_POSITIONS for that set.
  * Errors (synchronous): BAD_LENGTH, BAD_ARGUMENT, CUDA.
  * ---------------------------------------------------------------------------------------- */
+/* f3 -- the all-budget frontier (the Pareto curves of Figs. 2-3):
+ * the same DP, plus the canonical placement of EVERY budget m = 1..M from its argmin table
+ * (layers 1..m of an M-layer run are an m-layer run, so row m-1 equals what
+ * sp_place_checkpoints(..., m, ...) returns).
+ *   frontier_positions int32 [E][M][M]: row m-1 = budget m's positions, ascending, 0-padded
+ *   frontier_n         int32 [E][M]: counts (or the entry's negative status)
+ *   cost_by_budget, positions, n_positions, cost: as sp_place_checkpoints (may be NULL except
+ *   n_positions and cost).  Same workspace as sp_place_checkpoints. */
+sp_status sp_place_checkpoints_frontier(const void* weights, sp_weight_type wtype,
+                                        int32_t n_entries, int32_t N, int32_t M,
+                                        int32_t* frontier_positions, int32_t* frontier_n,
+                                        void* cost_by_budget, int32_t* positions,
+                                        int32_t* n_positions, void* cost, void* workspace,
+                                        size_t workspace_bytes, sp_stream_t stream);
+
 sp_status sp_expected_recompute(const void* weights, sp_weight_type wtype, int32_t n_entries,
                                 int32_t N, const int32_t* positions, const int32_t* n_positions,
                                 int32_t n_sets, int32_t max_pos, int32_t broadcast, void* cost,

@@ -137,6 +137,8 @@ struct DpParams {
   uint8_t* ws;
   size_t slot;
   int smem_b;   // 1: the int32 b array fits in shared memory next to opt_m
+  int32_t* fpos;   // f3 frontier: [E][M][M] positions of every budget m = 1..M (row m-1), or NULL
+  int32_t* fn;     // f3 frontier: [E][M] counts (or a negative status), or NULL
 };
 
 constexpr int TOPP_CAP = 160;
@@ -1461,6 +1463,33 @@ __global__ void __launch_bounds__(DP_NT, 1) dp_place_kernel(DpParams p) {
       p.npos[e] = status ? -status : k;
       sh.red_s[0] = status ? -1 : k;
     }
+    if (p.fpos && M > 0) {
+      // f3: the canonical placement of EVERY budget m <= M from the same argmin table (layers
+      // 1..m of an M-layer run are exactly an m-layer run): thread m-1 backtracks budget m
+      __syncthreads();
+      const int st = sh.red_s[0];
+      const uint16_t* opt = reinterpret_cast<const uint16_t*>(slot + slot_opt_off(N));
+      for (int mb = threadIdx.x + 1; mb <= M; mb += DP_NT) {
+        int32_t* fo = p.fpos + ((int64_t)e * M + (mb - 1)) * M;
+        int k = 0;
+        if (st >= 0) {
+          int j = N, m = mb;
+          while (m > 0 && P[j] > 0) {
+            const int s = opt[(size_t)(m - 1) * opt_ld(N) + j];
+            fo[k++] = s;
+            j = s - 1;
+            --m;
+          }
+          for (int a = 0, z = k - 1; a < z; ++a, --z) {
+            const int tmp = fo[a];
+            fo[a] = fo[z];
+            fo[z] = tmp;
+          }
+        }
+        for (int q = k; q < M; ++q) fo[q] = 0;
+        p.fn[(int64_t)e * M + mb - 1] = st >= 0 ? k : st;
+      }
+    }
     if constexpr (F64) {
       // a7: report the definitional cost of the returned placement, compensated (the DP's own
       // V_M carries ~M N eps P_N absolute rounding)
@@ -1516,11 +1545,38 @@ extern "C" size_t sp_place_checkpoints_workspace_bytes(int32_t n_entries, int32_
   return SP_WS_STATS_BYTES + (size_t)dp_grid(n_entries, N) * sp::slot_bytes(N, M);
 }
 
+static sp_status place_impl(const void* weights, sp_weight_type wtype, int32_t n_entries,
+                            int32_t N, int32_t M, int32_t* positions, int32_t* n_positions,
+                            void* cost, void* cost_by_budget, int32_t* fpos, int32_t* fn,
+                            void* workspace, size_t workspace_bytes, sp_stream_t stream);
+
 extern "C" sp_status sp_place_checkpoints(const void* weights, sp_weight_type wtype,
                                           int32_t n_entries, int32_t N, int32_t M,
                                           int32_t* positions, int32_t* n_positions, void* cost,
                                           void* cost_by_budget, void* workspace,
                                           size_t workspace_bytes, sp_stream_t stream) {
+  return place_impl(weights, wtype, n_entries, N, M, positions, n_positions, cost,
+                    cost_by_budget, nullptr, nullptr, workspace, workspace_bytes, stream);
+}
+
+extern "C" sp_status sp_place_checkpoints_frontier(const void* weights, sp_weight_type wtype,
+                                                   int32_t n_entries, int32_t N, int32_t M,
+                                                   int32_t* frontier_positions,
+                                                   int32_t* frontier_n, void* cost_by_budget,
+                                                   int32_t* positions, int32_t* n_positions,
+                                                   void* cost, void* workspace,
+                                                   size_t workspace_bytes, sp_stream_t stream) {
+  if (M > 0 && (!frontier_positions || !frontier_n)) return SP_ERR_BAD_ARGUMENT;
+  return place_impl(weights, wtype, n_entries, N, M, positions, n_positions, cost,
+                    cost_by_budget, frontier_positions, frontier_n, workspace, workspace_bytes,
+                    stream);
+}
+
+static sp_status place_impl(const void* weights, sp_weight_type wtype,
+                            int32_t n_entries, int32_t N, int32_t M, int32_t* positions,
+                            int32_t* n_positions, void* cost, void* cost_by_budget, int32_t* fpos,
+                            int32_t* fn, void* workspace, size_t workspace_bytes,
+                            sp_stream_t stream) {
   if (N < 1 || N > SP_MAX_N || n_entries < 0) return SP_ERR_BAD_LENGTH;
   if (M < 0 || M > N) return SP_ERR_BUDGET_TOO_LARGE;
   if (wtype != SP_W_COUNTS_I32 && wtype != SP_W_COUNTS_I64 && wtype != SP_W_PROB_F64)
@@ -1546,6 +1602,8 @@ extern "C" sp_status sp_place_checkpoints(const void* weights, sp_weight_type wt
   p.ws = (uint8_t*)workspace;
   p.slot = sp::slot_bytes(N, M);
   p.smem_b = dp_smem_b_fits(N) ? 1 : 0;
+  p.fpos = fpos;
+  p.fn = fn;
   const size_t dyn = dp_dyn_smem(N, p.smem_b);
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(workspace, 0, SP_WS_STATS_BYTES, st) != cudaSuccess) SP_CHECK_LAUNCH();

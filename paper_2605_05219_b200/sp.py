@@ -44,6 +44,8 @@ SYMBOLS = {
                                             _vp, _vp, _sz, _vp]),
     "sp_expected_recompute": (ctypes.c_int, [_vp, ctypes.c_int, _i32, _i32, _vp, _vp, _i32, _i32,
                                              _i32, _vp, _vp, _vp]),
+    "sp_place_checkpoints_frontier": (ctypes.c_int, [_vp, ctypes.c_int, _i32, _i32, _i32, _vp,
+                                                     _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "sp_place_checkpoints_grid_workspace_bytes": (_sz, [_i32, _i32, _i32, _i32]),
     "sp_place_checkpoints_grid": (ctypes.c_int, [_vp, ctypes.c_int, _i32, _i32, _i32, _i32, _vp,
                                                  _vp, _vp, _vp, _vp, _sz, _vp]),
@@ -225,6 +227,35 @@ def block_positions(N, B):
     if k < 0:
         raise SPError(-k, "sp_block_positions")
     return list(buf[:k])
+
+
+def place_checkpoints_frontier(weights, M, workspace=None, stream=None):
+    """f3: positions of every budget m = 1..M from one DP.  Returns (frontier_positions
+    [E][M][M] (row m-1 = budget m), frontier_n [E][M], cost_by_budget [E][M+1])."""
+    wtype = _WTYPE.get(weights.dtype)
+    if wtype is None or weights.dim() != 2:
+        raise TypeError("weights must be [E][N+1] int32, int64 or float64")
+    E, N = weights.shape[0], weights.shape[1] - 1
+    dev = weights.device
+    cdt = torch.float64 if wtype == SP_W_PROB_F64 else torch.int64
+    fpos = torch.empty(E, M, M, dtype=torch.int32, device=dev)
+    fn = torch.empty(E, M, dtype=torch.int32, device=dev)
+    cbb = torch.empty(E, M + 1, dtype=cdt, device=dev)
+    pos = torch.empty(E, M, dtype=torch.int32, device=dev)
+    npos = torch.empty(E, dtype=torch.int32, device=dev)
+    cost = torch.empty(E, dtype=cdt, device=dev)
+    need = place_checkpoints_workspace_bytes(E, N, M)
+    if workspace is None:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    st = lib().sp_place_checkpoints_frontier(
+        _dev(weights, weights.dtype, "weights"), wtype, E, N, M,
+        _dev(fpos, torch.int32, "frontier_positions") if M > 0 else None,
+        _dev(fn, torch.int32, "frontier_n") if M > 0 else None, _dev(cbb, cdt, "cbb"),
+        _dev(pos, torch.int32, "positions") if M > 0 else None, _dev(npos, torch.int32, "npos"),
+        _dev(cost, cdt, "cost"), _dev(workspace, torch.uint8, "workspace"), workspace.numel(),
+        _stream(stream, dev))
+    _check(st, "sp_place_checkpoints_frontier")
+    return fpos, fn, cbb
 
 
 def place_checkpoints_grid(weights, M, B, positions=None, n_positions=None, cost=None,

@@ -1,0 +1,121 @@
+"""W4 budget sweep (the axes of Figs. 2-3): one frontier DP at
+M_max = 64 gives the optimal placement of every budget m <= 64 per entry; the Table 1 baselines
+(balanced, logarithmic, sqrt, block) are scored by the a6 evaluation kernel.  Writes the
+S:542-style CSV (strategy, budget, slots, expected_recompute, savings, reduction, bytes, pareto)
+with aggregates over all entries (savings normalised over overlap tokens):
+
+    savings   = 1 - sum_e E_e[r] / sum_e R_nc,e        R_nc,e = sum_t c_t t  (= V_0)
+    reduction = 1 / (1 - savings)
+    slots     = mean checkpoints stored per entry;  bytes = slots * --state-bytes
+
+Everything runs through the C ABI on the GPU; no oracle here.
+
+    python tools/budget_sweep.py --out profiles/r01_w4_sweep.csv
+"""
+import argparse
+import csv
+import json
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_05219_b200 import sp  # noqa: E402
+from paper_2605_05219_b200 import workload as wl  # noqa: E402
+
+
+def pack(sets, dev):
+    width = max([len(s) for s in sets] + [1])
+    pos = torch.zeros(len(sets), width, dtype=torch.int32)
+    for i, s in enumerate(sets):
+        if len(s):
+            pos[i, :len(s)] = torch.as_tensor(s, dtype=torch.int32)
+    return pos.to(dev), torch.tensor([len(s) for s in sets], dtype=torch.int32, device=dev)
+
+
+def pareto_flags(rows):
+    """Non-dominated in (slots down, savings up) over every row of the table."""
+    flags = []
+    for r in rows:
+        dom = any((o["slots"] <= r["slots"] and o["savings"] >= r["savings"]) and
+                  (o["slots"] < r["slots"] or o["savings"] > r["savings"]) for o in rows)
+        flags.append(0 if dom else 1)
+    return flags
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--entries", type=int, default=None, help="default: W4's E")
+    ap.add_argument("--mmax", type=int, default=64)
+    ap.add_argument("--blocks", default="16,32,64,128,256,512")
+    ap.add_argument("--state-bytes", type=int, default=1 << 20,
+                    help="bytes per stored recurrent-state checkpoint (cost model)")
+    ap.add_argument("--seed", type=int, default=4)
+    ap.add_argument("--out", default="profiles/r01_w4_sweep.csv")
+    a = ap.parse_args()
+
+    dev = torch.device("cuda:0")
+    cfg = wl.CONFIGS["W4"]
+    if a.entries:
+        cfg = wl.scaled(cfg, a.entries)
+    E, N, Mx = cfg.n_entries, cfg.N, a.mmax
+    H = wl.make_dense_hist(cfg, seed=a.seed).to(dev)
+
+    # the frontier: one DP, all budgets
+    sp.place_checkpoints_frontier(H, Mx)                     # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fpos, fn, cbb = sp.place_checkpoints_frontier(H, Mx)
+    torch.cuda.synchronize()
+    t_frontier = time.perf_counter() - t0
+    rnc = cbb[:, 0].sum().item()
+
+    # consistency: the a6 kernel re-scores every frontier row to the DP's value
+    dcost, _ = sp.expected_recompute(H, fpos, fn.clamp(min=0), broadcast=False)
+    assert torch.equal(dcost, cbb[:, 1:]), "frontier positions do not achieve the DP values"
+
+    rows = []
+
+    def add(strategy, budget, slots_total, cost_total):
+        sav = 1.0 - cost_total / rnc if rnc else 0.0
+        red = float("inf") if cost_total == 0 else rnc / cost_total
+        rows.append(dict(strategy=strategy, budget=budget, slots=slots_total / E,
+                         expected_recompute=cost_total / max(1, int(H[:, 1:].sum().item())),
+                         savings=sav, reduction=red, bytes=slots_total / E * a.state_bytes))
+
+    add("none", 0, 0, rnc)
+    ms = list(range(1, Mx + 1))
+    for m in ms:
+        add("dp", m, fn[:, m - 1].sum().item(), cbb[:, m].sum().item())
+    base = [("balanced", m, sp.balanced_positions(N, m)) for m in ms]
+    base += [("logarithmic", m, sp.log_positions(N, m)) for m in ms]
+    base += [("sqrt", len(sp.sqrt_positions(N)), sp.sqrt_positions(N))]
+    base += [("block", B, sp.block_positions(N, B)) for B in map(int, a.blocks.split(","))]
+    pos, npos = pack([s for _, _, s in base], dev)
+    bc, _ = sp.expected_recompute(H, pos, npos, broadcast=True)
+    bc = bc.sum(0).tolist()
+    for (name, m, s), c in zip(base, bc):
+        add(name, m, len(s) * E, c)
+
+    for r, f in zip(rows, pareto_flags(rows)):
+        r["pareto"] = f
+    os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
+    with open(a.out, "w", newline="") as fh:
+        w = csv.DictWriter(fh, fieldnames=["strategy", "budget", "slots", "expected_recompute",
+                                           "savings", "reduction", "bytes", "pareto"])
+        w.writeheader()
+        for r in rows:
+            w.writerow({k: (f"{v:.6g}" if isinstance(v, float) else v) for k, v in r.items()})
+    # dominance summary (S:565's qualitative claim, at this workload)
+    dp = {r["budget"]: r["savings"] for r in rows if r["strategy"] == "dp"}
+    worse = [(r["strategy"], r["budget"]) for r in rows
+             if r["strategy"] in ("balanced", "logarithmic") and r["savings"] > dp[r["budget"]] + 1e-12]
+    print(json.dumps({"workload": f"W4 E={E} N={N}", "frontier_ms": round(t_frontier * 1e3, 3),
+                      "budgets": Mx, "rows": len(rows), "dp_dominated_at": worse,
+                      "dp_savings_m1": dp[1], "dp_savings_m64": dp[Mx], "out": a.out}))
+
+
+if __name__ == "__main__":
+    main()

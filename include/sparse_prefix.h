@@ -92,7 +92,10 @@ sp_status sp_accumulate_depths(const int32_t* entry, const int32_t* depth, int64
  *   P_j = sum_{t<=j} c_t,  T_j = sum_{t<=j} t c_t
  *   dp[0][j] = T_j,  dp[m][0] = 0 (at-most-m reading R1),
  *   dp[m][j] = min_{1<=s<=j} dp[m-1][s-1] + (T_j - T_{s-1}) - s (P_j - P_{s-1})
- * computed on the GPU as a divide-and-conquer monotone argmin per layer, exactly.
+ * computed on the GPU exactly: count weights on the exact-int32 path by the paper's monotone
+ * convex-hull trick with all layers advancing in lockstep, one warp per entry
+ * (dp_hull.cu); the other entries (int64 range, ring overflow) and fp64 weights by a
+ * divide-and-conquer monotone argmin per layer (dp_place.cu).  DESIGN.md section 7.
  *
  *   weights        [E][N+1] of type wtype (bin 0 ignored; not normalised)
  *   positions      int32 [E][M]: the rule-B placement, ascending, unused slots 0
@@ -113,12 +116,15 @@ size_t sp_place_checkpoints_workspace_bytes(int32_t n_entries, int32_t N, int32_
 
 /* Launch statistics written (stream-ordered) at the start of the workspace by every
  * sp_place_checkpoints call: the exact number of candidate evaluations b_s - s P_j the
- * divide-and-conquer performed (the DP's executed work; cells = E N M), and the entries solved
- * on the exact-int32 / int64 / fp64 paths. */
+ * divide-and-conquer performed, the line tests of the hull kernel (the DP's executed work;
+ * cells = E N M), and the entries solved on the exact-int32 / int64 / fp64 paths and by the
+ * hull kernel. */
 #define SP_WS_STATS_BYTES 256
 typedef struct {
-  unsigned long long evaluations;
-  unsigned long long entries_i32, entries_i64, entries_f64;
+  unsigned long long evaluations;      /* D&C candidate evaluations b_s - s P_j               */
+  unsigned long long entries_i32, entries_i64, entries_f64;   /* entries per arithmetic path */
+  unsigned long long hull_tests;       /* hull kernel: back-pop + front-pop line tests        */
+  unsigned long long entries_hull;     /* entries solved by the hull kernel (rest: D&C)       */
 } sp_dp_stats;
 
 sp_status sp_place_checkpoints(const void* weights, sp_weight_type wtype, int32_t n_entries,

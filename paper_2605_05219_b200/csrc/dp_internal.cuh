@@ -1,0 +1,19 @@
+// dp_internal.cuh -- internal plumbing between the two DP kernels (dp_hull.cu, dp_place.cu):
+// workspace layout and the hull-kernel launch helpers.  Product path only.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+// Workspace head (SP_WS_STATS_BYTES): sp_dp_stats at 0, SP_TIMING counters at 64..127, and two
+// internal counters, zeroed by the launch's header memset:
+#define SP_WS_FB_COUNT_OFF 192    // unsigned: entries handed from the hull kernel to the D&C
+#define SP_WS_ENTRY_CTR_OFF 200   // unsigned: next entry for the hull kernel's warps
+
+// Workspace after the head:  fallback list int32[E] | hull slots | D&C slots  (256-B aligned)
+int sp_hull_grid(int E, int N, int M, int wtype);
+size_t sp_hull_slot_bytes(int N, int M);
+cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
+                           int32_t* npos, int64_t* cost, int64_t* cbb, int32_t* fpos,
+                           int32_t* fn, uint8_t* ws, int32_t* fb, uint8_t* slots, int grid,
+                           cudaStream_t st);

@@ -20,9 +20,12 @@
 // current layer lives in shared memory (uint16); P_j, b_next and the full argmin table
 // opt[M][N+1] (uint16) live in the CTA's workspace slot.
 #include <climits>
+#include <cstdlib>
+#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
+#include "dp_internal.cuh"
 
 namespace sp {
 
@@ -139,6 +142,9 @@ struct DpParams {
   int smem_b;   // 1: the int32 b array fits in shared memory next to opt_m
   int32_t* fpos;   // f3 frontier: [E][M][M] positions of every budget m = 1..M (row m-1), or NULL
   int32_t* fn;     // f3 frontier: [E][M] counts (or a negative status), or NULL
+  uint8_t* slots;  // this kernel's per-CTA slots
+  const int32_t* list;     // entries to solve (the hull kernel's fallbacks), or NULL = all E
+  const unsigned* list_n;  // device count of `list`
 };
 
 constexpr int TOPP_CAP = 160;
@@ -1089,7 +1095,7 @@ template <typename VT, bool BS, typename PT, typename CT>
 __device__ void solve_entry(const DpParams& p, Shared& sh, VT* smem_b, uint16_t* sopt,
                             uint8_t* scratch, int e, CT TN, const PT* P, unsigned& phase) {
   const int N = p.N, M = p.M;
-  uint8_t* slot = p.ws + SP_WS_STATS_BYTES + (size_t)blockIdx.x * p.slot;
+  uint8_t* slot = p.slots + (size_t)blockIdx.x * p.slot;
   VT* bA = reinterpret_cast<VT*>(slot + align256(8 * (size_t)(N + 1)));
   VT* bB = reinterpret_cast<VT*>(slot + 2 * align256(8 * (size_t)(N + 1)));
   uint16_t* opt = reinterpret_cast<uint16_t*>(slot + slot_opt_off(N));
@@ -1382,8 +1388,10 @@ __global__ void __launch_bounds__(DP_NT, 1) dp_place_kernel(DpParams p) {
   }
   __syncthreads();
 
-  for (int e = blockIdx.x; e < p.E; e += gridDim.x) {
-    uint8_t* slot = p.ws + SP_WS_STATS_BYTES + (size_t)blockIdx.x * p.slot;
+  const int n_items = p.list ? (int)*p.list_n : p.E;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int e = p.list ? p.list[it] : it;
+    uint8_t* slot = p.slots + (size_t)blockIdx.x * p.slot;
     PT* P = reinterpret_cast<PT*>(slot);
     int32_t* P32 = reinterpret_cast<int32_t*>(slot + slot_p32_off(N, M));
     const WT* we = w + (int64_t)e * (N + 1);
@@ -1542,7 +1550,13 @@ static int dp_grid(int E, int N) {
 extern "C" size_t sp_place_checkpoints_workspace_bytes(int32_t n_entries, int32_t N, int32_t M) {
   if (N < 1 || N > SP_MAX_N || n_entries < 0 || M < 0 || M > N) return 0;
   if (n_entries == 0) return 0;
-  return SP_WS_STATS_BYTES + (size_t)dp_grid(n_entries, N) * sp::slot_bytes(N, M);
+  size_t hull = 0;
+  if (M > 0) {
+    const int gh = std::max(sp_hull_grid(n_entries, N, M, SP_W_COUNTS_I32),
+                            sp_hull_grid(n_entries, N, M, SP_W_COUNTS_I64));
+    hull = sp::align256(4 * (size_t)n_entries) + (size_t)gh * sp_hull_slot_bytes(N, M);
+  }
+  return SP_WS_STATS_BYTES + hull + (size_t)dp_grid(n_entries, N) * sp::slot_bytes(N, M);
 }
 
 static sp_status place_impl(const void* weights, sp_weight_type wtype, int32_t n_entries,
@@ -1587,7 +1601,14 @@ static sp_status place_impl(const void* weights, sp_weight_type wtype,
   if (wtype == SP_W_COUNTS_I32) grid = dp_grid_t<int32_t>(n_entries, N);
   else if (wtype == SP_W_COUNTS_I64) grid = dp_grid_t<int64_t>(n_entries, N);
   else grid = dp_grid_t<double>(n_entries, N);
-  const size_t need = SP_WS_STATS_BYTES + (size_t)grid * sp::slot_bytes(N, M);
+  // count weights: the hull kernel (dp_hull.cu) solves every entry it can on the exact-int32
+  // path and lists the rest (int64 range, negative counts, ring overflow) for the D&C kernel
+  const bool use_hull = wtype != SP_W_PROB_F64 && M > 0 && !getenv("SP_NO_HULL");
+  const int hgrid = use_hull ? sp_hull_grid(n_entries, N, M, wtype) : 0;
+  const size_t fb_off = SP_WS_STATS_BYTES;
+  const size_t hull_off = fb_off + (use_hull ? sp::align256(4 * (size_t)n_entries) : 0);
+  const size_t dc_off = hull_off + (size_t)hgrid * (use_hull ? sp_hull_slot_bytes(N, M) : 0);
+  const size_t need = dc_off + (size_t)grid * sp::slot_bytes(N, M);
   if (!workspace || workspace_bytes < need) return SP_ERR_WORKSPACE;
   sp::DpParams p;
   p.w = weights;
@@ -1604,9 +1625,23 @@ static sp_status place_impl(const void* weights, sp_weight_type wtype,
   p.smem_b = dp_smem_b_fits(N) ? 1 : 0;
   p.fpos = fpos;
   p.fn = fn;
+  p.slots = (uint8_t*)workspace + dc_off;
+  p.list = use_hull ? reinterpret_cast<const int32_t*>((uint8_t*)workspace + fb_off) : nullptr;
+  p.list_n = reinterpret_cast<const unsigned*>((uint8_t*)workspace + SP_WS_FB_COUNT_OFF);
   const size_t dyn = dp_dyn_smem(N, p.smem_b);
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(workspace, 0, SP_WS_STATS_BYTES, st) != cudaSuccess) SP_CHECK_LAUNCH();
+  if (use_hull) {
+    const cudaError_t he = sp_hull_launch(
+        weights, wtype, n_entries, N, M, positions, n_positions, (int64_t*)cost,
+        (int64_t*)cost_by_budget, fpos, fn, (uint8_t*)workspace,
+        reinterpret_cast<int32_t*>((uint8_t*)workspace + fb_off), (uint8_t*)workspace + hull_off,
+        hgrid, st);
+    if (he != cudaSuccess) {
+      sp_set_cuda_error(he);
+      return SP_ERR_CUDA;
+    }
+  }
   if (wtype == SP_W_COUNTS_I32) sp::dp_place_kernel<int32_t><<<grid, sp::DP_NT, dyn, st>>>(p);
   else if (wtype == SP_W_COUNTS_I64) sp::dp_place_kernel<int64_t><<<grid, sp::DP_NT, dyn, st>>>(p);
   else sp::dp_place_kernel<double><<<grid, sp::DP_NT, dyn, st>>>(p);

@@ -1,0 +1,147 @@
+"""GPU parity of the hull kernel (dp_hull.cu: the paper's monotone convex-hull trick, P:764-773,
+with all layers in lockstep, one warp per entry) and of its hand-off to the divide-and-conquer
+kernel (ring overflow, int64 range, bad counts) -- against the CPU oracle's naive DP (the
+definition, Thm 2) or its CHT, bit-exact in every integer output."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2605_05219_b200 import sp
+from paper_2605_05219_b200 import workload as wl
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_2605_05219_b200 import build
+    build.build()
+    sp.lib()
+    return torch.device("cuda:0")
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def place(H, M, dev, dtype=torch.int32, frontier=False):
+    w = torch.as_tensor(H).to(dtype).to(dev).contiguous()
+    E, N = w.shape[0], w.shape[1] - 1
+    ws = torch.empty(sp.place_checkpoints_workspace_bytes(E, N, M), dtype=torch.uint8, device=dev)
+    if frontier:
+        fp, fn, cbb = sp.place_checkpoints_frontier(w, M, workspace=ws)
+        torch.cuda.synchronize()
+        return dict(fpos=np_(fp), fn=np_(fn), cbb=np_(cbb), stats=sp.dp_stats(ws))
+    pos, npos, cost, cbb = sp.place_checkpoints(w, M, cost_by_budget=True, workspace=ws)
+    torch.cuda.synchronize()
+    return dict(pos=np_(pos), npos=np_(npos), cost=np_(cost), cbb=np_(cbb), stats=sp.dp_stats(ws))
+
+
+def check(H, M, r, algo="cht", rows=None):
+    rows = range(H.shape[0]) if rows is None else rows
+    for e in rows:
+        rp, rc, rcbb = oracle.place(H[e].astype(np.int64), M, algo)
+        k = len(rp)
+        assert r["npos"][e] == k, (e, r["npos"][e], k)
+        assert r["pos"][e, :k].tolist() == rp.tolist(), (e, r["pos"][e, :k], rp)
+        assert (r["pos"][e, k:] == 0).all()
+        assert r["cost"][e] == rc, (e, r["cost"][e], rc)
+        assert (r["cbb"][e] == rcbb).all(), e
+
+
+def dense(E, N, seed, law="mix", lo=None, hi=None):
+    cfg = wl.TraceConfig("t", E, N, 8, 1, (N, N), (1, 1), law,
+                         dense_n=(lo or N // 3, hi or N // 2))
+    return wl.make_dense_hist(cfg, seed=seed).numpy()
+
+
+@pytest.mark.parametrize("M", [1, 2, 31, 32, 33, 47, 63, 64])
+def test_hull_layer_slots(dev, M):
+    """K = 1 (M <= 32) and K = 2 (M > 32, partially filled second slot) against the naive DP."""
+    H = dense(12, 600, seed=M)
+    r = place(H, M, dev)
+    assert r["stats"]["entries_hull"] == 12
+    check(H, M, r, algo="naive")
+
+
+@pytest.mark.parametrize("N,M", [(700, 65), (700, 100), (500, 129), (400, 200), (300, 300)])
+def test_hull_multi_pass(dev, N, M):
+    """M > 64: passes of 64 layers chained through the e-row buffer."""
+    H = dense(6, N, seed=N + M, lo=N // 2, hi=N)
+    r = place(H, M, dev)
+    assert r["stats"]["entries_hull"] + r["stats"]["entries_i64"] >= 1
+    check(H, M, r, algo="cht")
+
+
+def test_hull_sparse_ties_and_plateaus(dev):
+    """Many zero bins (long P_j plateaus: ties between lines), tiny counts, all equal counts."""
+    rng = np.random.default_rng(3)
+    N, E = 777, 24
+    H = np.zeros((E, N + 1), np.int64)
+    for e in range(E):
+        k = rng.integers(1, 60)
+        H[e, rng.integers(1, N + 1, k)] = rng.integers(1, 3, k)
+    H[0, :] = 0
+    H[1, 1:] = 0
+    H[1, N] = 4
+    r = place(H, 16, dev)
+    check(H, 16, r, algo="naive")
+    r = place(H, 64, dev)
+    check(H, 64, r, algo="naive")
+
+
+def test_hull_overflow_falls_back_exactly(dev):
+    """Uniform mass: layer-1 hull ~N/2 lines overflows the ring -> the D&C kernel solves the
+    entry; mixed in one batch with dense entries, an int64-range entry and a bad entry."""
+    N, M = 3000, 40
+    H = dense(8, N, seed=1).astype(np.int64)
+    H[2, 1:] = 1                              # ring overflow
+    H[5, 1:] = 3                              # ring overflow
+    H[6] *= 400000 // max(1, H[6].sum())       # 2 n N >= 2^31: int64 path
+    assert H[6].sum() * N * 2 >= 2 ** 31
+    r = place(H, M, dev, dtype=torch.int64)
+    assert r["stats"]["entries_hull"] == 5
+    check(H, M, r)
+    Hb = H.copy()
+    Hb[3, 9] = -1
+    r = place(Hb, M, dev, dtype=torch.int64)
+    assert r["npos"][3] == -sp.SP_ERR_BAD_ARGUMENT
+    check(Hb, M, r, rows=[0, 1, 2, 4, 5, 6, 7])
+
+
+def test_hull_matches_dc_kernel_w5_rows(dev):
+    """Hull kernel vs the D&C kernel (SP_NO_HULL) on W5-shaped rows at full N=32768, M=64:
+    identical positions, counts and every V_m."""
+    cfg = wl.scaled(wl.CONFIGS["W5"], 40)
+    H = wl.make_dense_hist(cfg, seed=4).numpy()
+    a = place(H, 64, dev)
+    assert a["stats"]["entries_hull"] == 40
+    os.environ["SP_NO_HULL"] = "1"
+    try:
+        b = place(H, 64, dev)
+    finally:
+        del os.environ["SP_NO_HULL"]
+    assert b["stats"]["entries_hull"] == 0
+    for k in ("pos", "npos", "cost", "cbb"):
+        assert (a[k] == b[k]).all(), k
+    check(H, 64, a, rows=[0, 13, 39])
+
+
+def test_hull_frontier(dev):
+    """f3 frontier positions from the hull kernel's argmin table == single-budget oracle runs."""
+    H = dense(5, 900, seed=8)
+    M = 40
+    r = place(H, M, dev, frontier=True)
+    assert r["stats"]["entries_hull"] == 5
+    for e in range(5):
+        for m in (1, 7, 32, 33, 40):
+            rp, rc, _ = oracle.place(H[e].astype(np.int64), m, "cht")
+            k = len(rp)
+            assert r["fn"][e, m - 1] == k
+            assert r["fpos"][e, m - 1, :k].tolist() == rp.tolist()
+            assert (r["fpos"][e, m - 1, k:] == 0).all()

@@ -123,8 +123,9 @@ size_t sp_place_checkpoints_workspace_bytes(int32_t n_entries, int32_t N, int32_
 typedef struct {
   unsigned long long evaluations;      /* D&C candidate evaluations b_s - s P_j               */
   unsigned long long entries_i32, entries_i64, entries_f64;   /* entries per arithmetic path */
-  unsigned long long hull_tests;       /* hull kernel: back-pop + front-pop line tests        */
+  unsigned long long hull_pops;        /* hull kernel: lines popped (back + front)            */
   unsigned long long entries_hull;     /* entries solved by the hull kernel (rest: D&C)       */
+  unsigned long long hull_event_rows;  /* hull kernel: rows with c_j > 0 (line push + query)  */
 } sp_dp_stats;
 
 sp_status sp_place_checkpoints(const void* weights, sp_weight_type wtype, int32_t n_entries,

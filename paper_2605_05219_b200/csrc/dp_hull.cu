@@ -10,23 +10,33 @@
 // second-to-last line to the new one), then pop the front while the next line is STRICTLY
 // better at P_j (ties keep the lower index: the leftmost argmin, reading R3).
 //
-// The only dependency between layers is e_{m-1}(j-1) -> b_j of layer m.  So every layer can
-// advance one row per step in lockstep: lane l of the warp owns layers l+1 and l+33 (K = 2
-// slots; K = 1 when M <= 32), and at step j it receives e_{m-1}(j-1) -- produced by the lane
-// below at step j-1 -- with one shuffle.  One warp solves one entry; a step costs O(1)
-// amortised per layer (the paper's bound), with no barriers, no brackets and no D&C levels.
-// M > 64 runs in passes of 64 layers chained through a global e-row buffer.
+// Lockstep layers.  The only dependency between layers is e_{m-1}(j-1) -> b_j of layer m, so
+// every layer advances one row per step: lane l of the warp owns layers l+1 and l+33 (K = 2
+// slots; K = 1 when M <= 32) and receives e_{m-1}(j-1) -- produced by the lane below at step
+// j-1 -- with one shuffle.  One warp solves one entry; M > 64 runs in passes of 64 layers
+// chained through a global e-row buffer.
+//
+// Zero-count rows ("plateau rule").  If c_j = 0 then P_j = P_{j-1}, and
+//   (i)  the candidate of the new line at the query point is b_j - j P_j = e_{m-1}(j-1), so
+//        e_m(j) = min(e_m(j-1), e_{m-1}(j-1)) and opt_m(j) = j iff that is strictly smaller;
+//   (ii) at every later query x = P_{j'} > P_j, line j is strictly worse than line j+1 (their
+//        difference is e_{m-1}(j) - e_{m-1}(j-1) + P_j - x < 0, e non-increasing), and
+//        queries with x = P_j are rows of the same zero run, exact by (i).
+// So only rows with c_j > 0 push a line and query the hull; a zero row is one compare per
+// layer.  The row type is the same for all lanes (one entry per warp): the branch is uniform.
 //
 // Each layer's deque lives in shared memory as a ring of HC lines, interleaved across lanes
-// ([pos][slot][lane]) so that every lane hits its own bank whatever its deque position.  The
-// rings hold the live hull, which is small for histogram-shaped inputs (tools/hull_stats:
-// <= 51 lines on W5); an entry whose hull outgrows a ring (e.g. the all-ones histogram, whose
-// layer-1 hull holds ~N/2 lines) is handed to the divide-and-conquer kernel (dp_place.cu) in
-// the same launch sequence, as are entries needing int64 / fp64 arithmetic.
+// ([pos][slot][lane]) so that every lane hits its own bank whatever its deque position; its two
+// ends are cached in registers (back, back-1 and two prefetched lines below; front and front+1),
+// so a step with at most three back pops and no front pop issues no dependent shared load.
+// Rings hold the live hull, which is small for histogram-shaped inputs (<= 51 lines on W5); an
+// entry whose hull outgrows a ring (e.g. the all-ones histogram: layer-1 hull ~N/2 lines) is
+// handed to the divide-and-conquer kernel (dp_place.cu), as are entries needing int64 range.
 //
-// Outputs per entry: the argmin table (uint16, [pass][j][lane][slot], 2 B per cell) in the
-// warp's workspace slot; V_m = T_N + e_m(N) for every m (cost_by_budget); the rule-B backtrack
-// (positions, count) by lane 0; the f3 frontier by all lanes.
+// Argmin storage: opt_m(j) changes rarely along j, so each layer appends (j, opt_m(j)) to its
+// own log only when it changes (uint32: j << 16 | opt); the backtrack finds the last entry with
+// row <= j by a warp-cooperative 32-way search.  Outputs per entry: V_m = T_N + e_m(N) for every
+// m (cost_by_budget), the rule-B backtrack (positions, count), the f3 frontier.
 #include <climits>
 
 #include "common.cuh"
@@ -46,12 +56,18 @@ __host__ __device__ __forceinline__ int hull_passes(int M) {
   const int L = 32 * hull_K(M);
   return (M + L - 1) / L;
 }
-// slot: opt table [passes][N+1][32K] uint16 | e-row buffers 2 x int32[N+1]
-__host__ __device__ __forceinline__ size_t hull_opt_bytes(int N, int M) {
-  return hull_align((size_t)hull_passes(M) * (N + 1) * 32 * hull_K(M) * 2);
+__host__ __device__ __forceinline__ int hull_layers_padded(int M) {
+  return hull_passes(M) * 32 * hull_K(M);
+}
+// slot: argmin logs uint32 [layer][N+1] | log counts int32 [layer] | e-row buffers 2 x int32[N+1]
+__host__ __device__ __forceinline__ size_t hull_log_bytes(int N, int M) {
+  return hull_align((size_t)hull_layers_padded(M) * (N + 1) * 4);
+}
+__host__ __device__ __forceinline__ size_t hull_cnt_bytes(int M) {
+  return hull_align((size_t)hull_layers_padded(M) * 4);
 }
 __host__ __device__ __forceinline__ size_t hull_slot_bytes(int N, int M) {
-  return hull_opt_bytes(N, M) + 2 * hull_align(4 * (size_t)(N + 1));
+  return hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(4 * (size_t)(N + 1));
 }
 __host__ __device__ __forceinline__ size_t hull_smem_bytes(int M) {
   return (size_t)HC * 32 * hull_K(M) * 8;   // int2 (b, s) per line
@@ -72,18 +88,63 @@ struct HullParams {
   size_t slot;
 };
 
-// back-pop test, all int32 inputs exact (|b| <= nN < 2^30, so differences fit int32):
-// the back line (s2, b2) goes if it is not strictly below the segment (s1, b1) -> (j, bj),
-// i.e. (bj - b1)(s2 - s1) <= (b2 - b1)(j - s1).  Products < 2^46 in int64.
+// back-pop test, int32 inputs exact (0 <= b <= nN < 2^30, so differences fit int32): the back
+// line (s2, b2) goes if it is not strictly below the segment (s1, b1) -> (j, bj), i.e.
+// (bj - b1)(s2 - s1) <= (b2 - b1)(j - s1).  Products < 2^46 in int64.
 __device__ __forceinline__ bool back_dominated(int db_new, int ds_old, int db_old, int ds_new) {
   return (long long)db_new * ds_old <= (long long)db_old * ds_new;
 }
+__device__ __forceinline__ bool dom3(int2 a, int2 bk, int bj, int j) {   // (a, bk, new)
+  return back_dominated(bj - a.x, bk.y - a.y, bk.x - a.x, j - a.y);
+}
 
-// opt table element of layer q (0-based within its pass) at row j
-__device__ __forceinline__ int hull_opt_at(const uint16_t* T, int N, int K, int m, int j) {
+// shared-memory ring access by explicit shared addresses (no generic-address conversion)
+__device__ __forceinline__ int2 lds2(uint32_t a) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts2(uint32_t a, int2 v) {
+  asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
+}
+
+// log slot of layer m (1-based), lane-major within a pass: [pass][slot k][lane]
+__device__ __forceinline__ int hull_layer_slot(int K, int m) {
   const int L = 32 * K;
   const int p = (m - 1) / L, q = (m - 1) % L;
-  return T[((size_t)p * (N + 1) + j) * L + (q & 31) * K + (q >> 5)];
+  return p * L + (q >> 5) * 32 + (q & 31);
+}
+
+// opt_m(j) from layer m's change log: the last entry with row <= j (entry 0 has row 1 <= j).
+// Warp-cooperative: each round the 32 lanes probe 32 evenly spaced entries.
+__device__ __forceinline__ int log_lookup_warp(const uint32_t* lg, int cnt, int j) {
+  const int lane = lane_id();
+  int lo = 0, hi = cnt - 1;
+  while (hi > lo) {
+    const int span = hi - lo;
+    const int pr = lo + (int)(((long long)span * (lane + 1) + 31) >> 5);
+    const bool ok = (int)(__ldcg(lg + pr) >> 16) <= j;
+    const unsigned bal = __ballot_sync(FULL, ok);
+    if (bal == 0) {
+      hi = __shfl_sync(FULL, pr, 0) - 1;
+    } else {
+      const int i = 31 - __clz(bal);
+      const int plo = __shfl_sync(FULL, pr, i);
+      const int pnx = __shfl_sync(FULL, pr, (i + 1) & 31);
+      lo = plo;
+      if (i < 31) hi = pnx - 1;
+    }
+  }
+  return (int)(__ldcg(lg + lo) & 0xffffu);
+}
+// single-thread version (one lane per budget in the frontier backtrack)
+__device__ __forceinline__ int log_lookup_lane(const uint32_t* lg, int cnt, int j) {
+  int lo = 0, hi = cnt - 1;   // last index with row <= j
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((int)(__ldcg(lg + mid) >> 16) <= j) lo = mid; else hi = mid - 1;
+  }
+  return (int)(__ldcg(lg + lo) & 0xffffu);
 }
 
 template <typename WT, int K>
@@ -92,15 +153,18 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   const int lane = threadIdx.x;
   const int N = p.N, M = p.M;
   constexpr int L = 32 * K;
+  constexpr uint32_t RSTRIDE = 8u * L;   // bytes between consecutive ring positions
   const int passes = (M + L - 1) / L;
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
   unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
   unsigned* ectr = reinterpret_cast<unsigned*>(p.ws + SP_WS_ENTRY_CTR_OFF);
   uint8_t* slot = p.slots + (size_t)blockIdx.x * p.slot;
-  uint16_t* optT = reinterpret_cast<uint16_t*>(slot);
-  int32_t* ebuf0 = reinterpret_cast<int32_t*>(slot + hull_opt_bytes(N, M));
-  int32_t* ebuf1 = reinterpret_cast<int32_t*>(slot + hull_opt_bytes(N, M) + hull_align(4 * (size_t)(N + 1)));
-  unsigned long long tests = 0;
+  uint32_t* logs = reinterpret_cast<uint32_t*>(slot);
+  int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
+  int32_t* ebuf0 = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M) + hull_cnt_bytes(M));
+  int32_t* ebuf1 = ebuf0 + hull_align(4 * (size_t)(N + 1)) / 4;
+  const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(ring) + 8u * lane;
+  unsigned long long pops = 0, events = 0;
   int done_entries = 0;
 
   for (;;) {
@@ -138,7 +202,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
 
     // ---- a4: all layers in lockstep, one row per step ---------------------------------------
     bool ovf = false;
-    unsigned tests_e = 0;
+    unsigned pops_e = 0, ev_e = 0;
     for (int ps = 0; ps < passes && !ovf; ++ps) {
       const int32_t* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
       int32_t* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
@@ -146,37 +210,43 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
       // Per slot: deque [f, b] (monotone counters; ring index & (HC-1)).  Cached in registers:
       // B0 = line b (back), B1 = line b-1, X1 = line b-2, X2 = line b-3 (prefetched after the
       // push), F0 = line f (front), F1 = line f+1.  A line is int2 (x = intercept b_s, y = s).
-      int f[K], b[K], eo[K], mlay[K];
+      // eo = e_m(j) (the running row minimum), op = opt_m(j).
+      int f[K], b[K], eo[K], op[K], cnt[K];
       int2 B0[K], B1[K], X1[K], X2[K], F0[K], F1[K];
       bool act[K];
+      uint32_t* lg[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        mlay[k] = ps * L + 32 * k + lane + 1;
-        act[k] = mlay[k] <= M;
+        const int mk = ps * L + 32 * k + lane + 1;
+        act[k] = mk <= M;
         f[k] = 0;
         b[k] = -1;
         eo[k] = 0;   // e_m(0) = 0 (reading R1)
+        op[k] = 1;   // opt_m(1) = 1 whatever the row type: logged up front
+        cnt[k] = 1;
+        lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * (N + 1);
+        if (act[k]) lg[k][0] = (1u << 16) | 1u;
         B0[k] = B1[k] = X1[k] = X2[k] = F0[k] = F1[k] = make_int2(0, 1);
       }
       if (chain_out && lane == 0) eout_buf[0] = 0;
       int32_t carry = 0, Pm1 = 0;
-      uint16_t* optP = optT + (size_t)ps * (N + 1) * L;
       for (int jb = 0; jb < N; jb += 32) {
         const int jr = jb + 1 + lane;
-        int32_t cnt = jr <= N ? (int32_t)we[jr] : 0;
+        const int32_t craw = jr <= N ? (int32_t)we[jr] : 0;
+        const unsigned evmask = __ballot_sync(FULL, craw > 0);   // rows with c_j > 0
+        int32_t cnt32 = craw;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const int32_t y = __shfl_up_sync(FULL, cnt, o);
-          if (lane >= o) cnt += y;
+          const int32_t y = __shfl_up_sync(FULL, cnt32, o);
+          if (lane >= o) cnt32 += y;
         }
-        const int32_t Pc = carry + cnt;
+        const int32_t Pc = carry + cnt32;
         carry = __shfl_sync(FULL, Pc, 31);
         int32_t Ec = 0;
         if (chain_in && jr <= N) Ec = ein[jr - 1];
         const int nstep = min(32, N - jb);
         for (int i = 0; i < nstep; ++i) {
           const int j = jb + 1 + i;
-          const int32_t Pj = __shfl_sync(FULL, Pc, i);
           // e_{m-1}(j-1): from the lane below (previous step); lane 0 slot 0 from outside
           int32_t in[K];
           const int32_t t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
@@ -186,133 +256,178 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
             const int32_t t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
             in[1] = lane ? t1 : t0;
           }
-          // (1) back tests for both slots, branch-free: up to three pops from registers
-          int bj[K], npop[K];
-          bool more[K];
+          int nop[K];
+          if ((evmask >> i) & 1u) {
+            // ---- c_j > 0: push line j, query the hull at x = P_j -------------------------
+            const int32_t Pj = __shfl_sync(FULL, Pc, i);
+            ++ev_e;
+            int bj[K], npop[K];
+            bool more[K];
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            bj[k] = in[k] + j * Pm1;
-            const int sz = b[k] - f[k] + 1;   // deque size before the push
-            const bool t1 = sz >= 2 && back_dominated(bj[k] - B1[k].x, B0[k].y - B1[k].y,
-                                                      B0[k].x - B1[k].x, j - B1[k].y);
-            const bool t2 = sz >= 3 && back_dominated(bj[k] - X1[k].x, B1[k].y - X1[k].y,
-                                                      B1[k].x - X1[k].x, j - X1[k].y);
-            const bool t3 = sz >= 4 && back_dominated(bj[k] - X2[k].x, X1[k].y - X2[k].y,
-                                                      X1[k].x - X2[k].x, j - X2[k].y);
-            npop[k] = t1 ? (t2 ? (t3 ? 3 : 2) : 1) : 0;
-            more[k] = act[k] && t1 && t2 && t3;
-          }
-          // (2) push line j (rare: more than three pops -> keep popping from the ring)
+            for (int k = 0; k < K; ++k) {
+              bj[k] = in[k] + j * Pm1;
+              const int sz = b[k] - f[k];   // deque size - 1, before the push
+              const bool t1 = dom3(B1[k], B0[k], bj[k], j);
+              const bool t2 = dom3(X1[k], B1[k], bj[k], j);
+              const bool t3 = dom3(X2[k], X1[k], bj[k], j);
+              const int p1 = (sz >= 1) & t1;
+              const int p2 = p1 & (sz >= 2) & t2;
+              const int p3 = p2 & (sz >= 3) & t3;
+              npop[k] = p1 + p2 + p3;
+              more[k] = act[k] & (p3 != 0);
+            }
+            int2 nb1[K];
+            int top[K];
 #pragma unroll
-          for (int k = 0; k < K; ++k) {
-            if (!act[k]) continue;
-            int2 nb1 = npop[k] == 0 ? B0[k] : npop[k] == 1 ? B1[k] : npop[k] == 2 ? X1[k] : X2[k];
-            int top = b[k] - npop[k];   // index of the new second-to-back line
-            if (more[k]) {
-              int2* rk = ring + k * 32 + lane;
-              while (top - f[k] >= 1) {
-                const int2 l1 = rk[((top - 1) & (HC - 1)) * L];
-                if (back_dominated(bj[k] - l1.x, nb1.y - l1.y, nb1.x - l1.x, j - l1.y)) {
-                  --top;
-                  nb1 = l1;
-                  ++npop[k];
-                } else {
-                  break;
+            for (int k = 0; k < K; ++k) {
+              nb1[k] = npop[k] == 0 ? B0[k] : npop[k] == 1 ? B1[k] : npop[k] == 2 ? X1[k] : X2[k];
+              top[k] = b[k] - npop[k];   // index of the new second-to-back line
+            }
+            bool anymore = more[0];
+            if constexpr (K == 2) anymore |= more[1];
+            if (__any_sync(FULL, anymore)) {   // rare: more than three pops
+#pragma unroll
+              for (int k = 0; k < K; ++k) {
+                if (!more[k]) continue;
+                const uint32_t rk = rbase + 256u * k;
+                while (top[k] - f[k] >= 1) {
+                  const int2 l1 = lds2(rk + ((top[k] - 1) & (HC - 1)) * RSTRIDE);
+                  if (dom3(l1, nb1[k], bj[k], j)) {
+                    --top[k];
+                    nb1[k] = l1;
+                    ++npop[k];
+                  } else {
+                    break;
+                  }
                 }
               }
             }
-            tests_e += (unsigned)npop[k];
-            const int nb = top + 1;
-            const int2 nl = make_int2(bj[k], j);
-            int2* rk = ring + k * 32 + lane;
-            rk[(nb & (HC - 1)) * L] = nl;
-            if (nb == f[k]) F0[k] = nl;                // the deque was empty (first row)
-            if (nb == f[k] + 1) F1[k] = nl;            // line f+1 was popped or is new
-            B1[k] = nb1;
-            B0[k] = nl;
-            b[k] = nb;
-            ovf |= (nb - f[k]) >= HC;
-            X1[k] = rk[((nb - 2) & (HC - 1)) * L];     // prefetch for the next step's tests
-            X2[k] = rk[((nb - 3) & (HC - 1)) * L];
+            int v0[K], v1[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              pops_e += (unsigned)npop[k];
+              const int nb = top[k] + 1;
+              const int2 nl = make_int2(bj[k], j);
+              const uint32_t rk = rbase + 256u * k;
+              sts2(rk + (nb & (HC - 1)) * RSTRIDE, nl);
+              if (nb == f[k]) F0[k] = nl;                // the deque was empty
+              if (nb == f[k] + 1) F1[k] = nl;            // line f+1 was popped or is new
+              B1[k] = nb1[k];
+              B0[k] = nl;
+              b[k] = nb;
+              ovf |= act[k] & ((nb - f[k]) >= HC);
+              X1[k] = lds2(rk + ((nb - 2) & (HC - 1)) * RSTRIDE);   // next step's tests
+              X2[k] = lds2(rk + ((nb - 3) & (HC - 1)) * RSTRIDE);
+              v0[k] = F0[k].x - F0[k].y * Pj;
+              v1[k] = F1[k].x - F1[k].y * Pj;
+            }
+            bool fpop[K];
+            bool anyf = false;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              fpop[k] = act[k] & (f[k] < b[k]) & (v1[k] < v0[k]);
+              anyf |= fpop[k];
+            }
+            if (__any_sync(FULL, anyf)) {   // rare: the front moves
+#pragma unroll
+              for (int k = 0; k < K; ++k) {
+                if (!fpop[k]) continue;
+                const uint32_t rk = rbase + 256u * k;
+                do {
+                  ++f[k];
+                  ++pops_e;
+                  F0[k] = F1[k];
+                  v0[k] = v1[k];
+                  if (f[k] < b[k]) {
+                    F1[k] = lds2(rk + ((f[k] + 1) & (HC - 1)) * RSTRIDE);
+                    v1[k] = F1[k].x - F1[k].y * Pj;
+                  }
+                } while (f[k] < b[k] && v1[k] < v0[k]);
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              eo[k] = v0[k];
+              nop[k] = F0[k].y;
+            }
+            Pm1 = Pj;
+          } else {
+            // ---- c_j = 0: line j enters only through the row minimum (plateau rule) -------
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const bool win = in[k] < eo[k];
+              eo[k] = win ? in[k] : eo[k];
+              nop[k] = win ? j : op[k];
+            }
           }
-          // (3) query x = P_j: pop the front while the next line is strictly better
+          // argmin change log
 #pragma unroll
           for (int k = 0; k < K; ++k) {
-            if (!act[k]) continue;
-            int v0 = F0[k].x - F0[k].y * Pj;
-            int v1 = F1[k].x - F1[k].y * Pj;
-            if (f[k] < b[k] && v1 < v0) {   // rare
-              int2* rk = ring + k * 32 + lane;
-              do {
-                ++f[k];
-                ++tests_e;
-                F0[k] = F1[k];
-                v0 = v1;
-                if (f[k] < b[k]) {
-                  F1[k] = rk[((f[k] + 1) & (HC - 1)) * L];
-                  v1 = F1[k].x - F1[k].y * Pj;
-                }
-              } while (f[k] < b[k] && v1 < v0);
+            if (act[k] & (nop[k] != op[k])) {
+              lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop[k];
+              ++cnt[k];
             }
-            eo[k] = v0;
-          }
-          // argmin row j of this pass: [j][lane][slot]
-          if constexpr (K == 2) {
-            reinterpret_cast<uint32_t*>(optP + (size_t)j * L)[lane] =
-                (uint32_t)F0[0].y | ((uint32_t)F0[1].y << 16);
-          } else {
-            optP[(size_t)j * L + lane] = (uint16_t)F0[0].y;
+            op[k] = nop[k];
           }
           if (chain_out && lane == 31) eout_buf[j] = eo[K - 1];
-          Pm1 = Pj;
         }
         if (__any_sync(FULL, ovf)) {
           ovf = true;
           break;
         }
       }
-      if (!ovf) {   // V_m = T_N + e_m(N)
+      if (!ovf) {
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           if (!act[k]) continue;
-          const long long V = TN + (long long)eo[k];
-          if (p.cbb) p.cbb[(int64_t)e * (M + 1) + mlay[k]] = V;
-          if (mlay[k] == M) p.cost[e] = V;
+          const int mk = ps * L + 32 * k + lane + 1;
+          logn[ps * L + 32 * k + lane] = cnt[k];
+          const long long V = TN + (long long)eo[k];   // V_m = T_N + e_m(N)
+          if (p.cbb) p.cbb[(int64_t)e * (M + 1) + mk] = V;
+          if (mk == M) p.cost[e] = V;
         }
       }
-      __syncwarp();   // chained e-row visible to the next pass
+      __syncwarp();   // chained e-row and logs visible to the whole warp
     }
-    tests += tests_e;
+    pops += pops_e;
+    events += ev_e;
     if (ovf) {
       if (lane == 0) p.fb[atomicAdd(fb_n, 1u)] = e;
       continue;
     }
-    __syncwarp();   // the argmin table is complete and visible to every lane
+    __threadfence_block();
+    __syncwarp();
 
-    // ---- a5: rule-B backtrack (reading R3): lane 0 for budget M, all lanes for the frontier
-    if (lane == 0) {
+    // ---- a5: rule-B backtrack (reading R3): the warp for budget M, lanes for the frontier --
+    {
       int32_t* out = p.pos + (int64_t)e * M;
       int k = 0, j = N, m = M;
       while (m > 0 && j >= tfirst) {   // P_j > 0  <=>  j >= first non-zero bin
-        const int s = hull_opt_at(optT, N, K, m, j);
-        out[k++] = s;
+        const int ls = hull_layer_slot(K, m);
+        const int s = log_lookup_warp(logs + (size_t)ls * (N + 1), logn[ls], j);
+        if (lane == 0) out[k] = s;
+        ++k;
         j = s - 1;
         --m;
       }
-      for (int a = 0, z = k - 1; a < z; ++a, --z) {
-        const int t = out[a];
-        out[a] = out[z];
-        out[z] = t;
+      __syncwarp();
+      if (lane == 0) {
+        for (int a = 0, z = k - 1; a < z; ++a, --z) {
+          const int t = out[a];
+          out[a] = out[z];
+          out[z] = t;
+        }
+        p.npos[e] = k;
       }
-      for (int q = k; q < M; ++q) out[q] = 0;
-      p.npos[e] = k;
+      for (int q = k + lane; q < M; q += 32) out[q] = 0;
     }
     if (p.fpos) {
       for (int mb = lane + 1; mb <= M; mb += 32) {
         int32_t* fo = p.fpos + ((int64_t)e * M + (mb - 1)) * M;
         int k = 0, j = N, m = mb;
         while (m > 0 && j >= tfirst) {
-          const int s = hull_opt_at(optT, N, K, m, j);
+          const int ls = hull_layer_slot(K, m);
+          const int s = log_lookup_lane(logs + (size_t)ls * (N + 1), logn[ls], j);
           fo[k++] = s;
           j = s - 1;
           --m;
@@ -329,11 +444,12 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
     ++done_entries;
     __syncwarp();   // the slot is rewritten by the next entry
   }
-  tests = warp_sum(tests);
+  pops = warp_sum(pops);
   if (lane == 0) {
-    atomicAdd(&stats->hull_tests, tests);
+    atomicAdd(&stats->hull_pops, pops);
     atomicAdd(&stats->entries_hull, (unsigned long long)done_entries);
     atomicAdd(&stats->entries_i32, (unsigned long long)done_entries);
+    atomicAdd(&stats->hull_event_rows, events);
   }
 }
 

@@ -16,14 +16,14 @@
 // j-1 -- with one shuffle.  One warp solves one entry; M > 64 runs in passes of 64 layers
 // chained through a global e-row buffer.
 //
-// Zero-count rows ("plateau rule").  If c_j = 0 then P_j = P_{j-1}, and
-//   (i)  the candidate of the new line at the query point is b_j - j P_j = e_{m-1}(j-1), so
-//        e_m(j) = min(e_m(j-1), e_{m-1}(j-1)) and opt_m(j) = j iff that is strictly smaller;
-//   (ii) at every later query x = P_{j'} > P_j, line j is strictly worse than line j+1 (their
-//        difference is e_{m-1}(j) - e_{m-1}(j-1) + P_j - x < 0, e non-increasing), and
-//        queries with x = P_j are rows of the same zero run, exact by (i).
-// So only rows with c_j > 0 push a line and query the hull; a zero row is one compare per
-// layer.  The row type is the same for all lanes (one entry per warp): the branch is uniform.
+// Zero-count rows are no-ops ("support rows").  If c_j = 0 then P_j = P_{j-1},
+// so the new line's candidate at the query point is b_j - j P_j = e_{m-1}(j-1) >= e_m(j-1)
+// (V is non-increasing in the budget at every row: "at most m", reading R1), hence
+// e_m(j) = e_m(j-1) and opt_m(j) = opt_m(j-1) exactly; and line j is strictly worse than line
+// j+1 at every later query x > P_j (their difference is e_{m-1}(j) - e_{m-1}(j-1) + P_j - x < 0),
+// so it never needs to enter the hull.  The warp therefore steps only through the support rows
+// (c_j > 0, found 32 at a time with a ballot), and every e_m / opt_m of a zero row is the value
+// at the support row before it.  The row type is the same for all lanes (one entry per warp).
 //
 // Each layer's deque lives in shared memory as a ring of HC lines, interleaved across lanes
 // ([pos][slot][lane]) so that every lane hits its own bank whatever its deque position; its two
@@ -228,12 +228,13 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
         if (act[k]) lg[k][0] = (1u << 16) | 1u;
         B0[k] = B1[k] = X1[k] = X2[k] = F0[k] = F1[k] = make_int2(0, 1);
       }
-      if (chain_out && lane == 0) eout_buf[0] = 0;
       int32_t carry = 0, Pm1 = 0;
+      int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
       for (int jb = 0; jb < N; jb += 32) {
         const int jr = jb + 1 + lane;
         const int32_t craw = jr <= N ? (int32_t)we[jr] : 0;
-        const unsigned evmask = __ballot_sync(FULL, craw > 0);   // rows with c_j > 0
+        unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
+        if (evmask == 0) continue;                          // 32 zero rows: nothing changes
         int32_t cnt32 = craw;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -242,22 +243,28 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
         }
         const int32_t Pc = carry + cnt32;
         carry = __shfl_sync(FULL, Pc, 31);
+        // previous pass's top layer at the support rows: e(j-1) of support row number t is its
+        // value at support row t-1 (constant over zero rows), 0 before the first
         int32_t Ec = 0;
-        if (chain_in && jr <= N) Ec = ein[jr - 1];
-        const int nstep = min(32, N - jb);
-        for (int i = 0; i < nstep; ++i) {
+        const int nev = __popc(evmask);
+        if (chain_in && lane < nev) Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
+        for (int q = 0; evmask; ++q) {
+          const int i = __ffs(evmask) - 1;
+          evmask &= evmask - 1;
           const int j = jb + 1 + i;
-          // e_{m-1}(j-1): from the lane below (previous step); lane 0 slot 0 from outside
+          // e_{m-1}(j-1): from the lane below (its value at the previous support row);
+          // lane 0 slot 0 from the previous pass (or e_0 = 0)
           int32_t in[K];
           const int32_t t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
-          const int32_t ext = chain_in ? __shfl_sync(FULL, Ec, i) : 0;
+          int32_t ext = 0;
+          if (chain_in) ext = __shfl_sync(FULL, Ec, q);
           in[0] = lane ? t0 : ext;
           if constexpr (K == 2) {
             const int32_t t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
             in[1] = lane ? t1 : t0;
           }
           int nop[K];
-          if ((evmask >> i) & 1u) {
+          {
             // ---- c_j > 0: push line j, query the hull at x = P_j -------------------------
             const int32_t Pj = __shfl_sync(FULL, Pc, i);
             ++ev_e;
@@ -351,14 +358,6 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
               nop[k] = F0[k].y;
             }
             Pm1 = Pj;
-          } else {
-            // ---- c_j = 0: line j enters only through the row minimum (plateau rule) -------
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              const bool win = in[k] < eo[k];
-              eo[k] = win ? in[k] : eo[k];
-              nop[k] = win ? j : op[k];
-            }
           }
           // argmin change log
 #pragma unroll
@@ -369,8 +368,9 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
             }
             op[k] = nop[k];
           }
-          if (chain_out && lane == 31) eout_buf[j] = eo[K - 1];
+          if (chain_out && lane == 31) eout_buf[evbase + q] = eo[K - 1];
         }
+        evbase += nev;
         if (__any_sync(FULL, ovf)) {
           ovf = true;
           break;

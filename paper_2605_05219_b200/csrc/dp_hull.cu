@@ -25,10 +25,11 @@
 // (c_j > 0, found 32 at a time with a ballot), and every e_m / opt_m of a zero row is the value
 // at the support row before it.  The row type is the same for all lanes (one entry per warp).
 //
-// Each layer's deque lives in shared memory as a ring of HC lines, interleaved across lanes
-// ([pos][slot][lane]) so that every lane hits its own bank whatever its deque position; its two
-// ends are cached in registers (back, back-1 and two prefetched lines below; front and front+1),
-// so a step with at most three back pops and no front pop issues no dependent shared load.
+// Each layer's deque lives in shared memory as a ring (HC0 / HC1 lines for slot 0 / 1),
+// interleaved across lanes ([slot][pos][lane]) so that every lane hits its own bank whatever its
+// deque position; its ends are cached in registers (back, back-1 and three prefetched lines below;
+// front, front+1, front+2), so a row with at most four back pops and one front pop per layer
+// issues no dependent shared load.
 // Rings hold the live hull, which is small for histogram-shaped inputs (<= 51 lines on W5); an
 // entry whose hull outgrows a ring (e.g. the all-ones histogram: layer-1 hull ~N/2 lines) is
 // handed to the divide-and-conquer kernel (dp_place.cu), as are entries needing int64 range.
@@ -44,11 +45,16 @@
 
 namespace sp {
 
-#ifndef SP_HULL_CAP
-#define SP_HULL_CAP 64
+// Ring capacity per layer (power of two): layers 1-32 (slot 0) hold the longest hulls (W5: up to
+// ~51 support lines), layers 33-64 (slot 1) at most ~32 (tools/hull_stats.c).
+#ifndef SP_HULL_CAP0
+#define SP_HULL_CAP0 64
 #endif
-constexpr int HC = SP_HULL_CAP;   // ring capacity per layer (power of two)
-static_assert((HC & (HC - 1)) == 0, "ring capacity must be a power of two");
+#ifndef SP_HULL_CAP1
+#define SP_HULL_CAP1 32
+#endif
+constexpr int HC0 = SP_HULL_CAP0, HC1 = SP_HULL_CAP1;
+static_assert((HC0 & (HC0 - 1)) == 0 && (HC1 & (HC1 - 1)) == 0, "ring capacities: powers of two");
 
 __host__ __device__ __forceinline__ size_t hull_align(size_t x) { return (x + 255) & ~(size_t)255; }
 __host__ __device__ __forceinline__ int hull_K(int M) { return M > 32 ? 2 : 1; }
@@ -70,7 +76,7 @@ __host__ __device__ __forceinline__ size_t hull_slot_bytes(int N, int M) {
   return hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(4 * (size_t)(N + 1));
 }
 __host__ __device__ __forceinline__ size_t hull_smem_bytes(int M) {
-  return (size_t)HC * 32 * hull_K(M) * 8;   // int2 (b, s) per line
+  return (size_t)(hull_K(M) == 2 ? HC0 + HC1 : HC0) * 32 * 8;   // int2 (b, s) per line
 }
 
 struct HullParams {
@@ -149,11 +155,10 @@ __device__ __forceinline__ int log_lookup_lane(const uint32_t* lg, int cnt, int 
 
 template <typename WT, int K>
 __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
-  extern __shared__ __align__(16) int2 ring[];   // [HC][K][32] lines (b, s)
+  extern __shared__ __align__(16) int2 ring[];   // slot rings [HC0][32] | [HC1][32] lines (b, s)
   const int lane = threadIdx.x;
   const int N = p.N, M = p.M;
   constexpr int L = 32 * K;
-  constexpr uint32_t RSTRIDE = 8u * L;   // bytes between consecutive ring positions
   const int passes = (M + L - 1) / L;
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
   unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
@@ -163,7 +168,15 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
   int32_t* ebuf0 = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M) + hull_cnt_bytes(M));
   int32_t* ebuf1 = ebuf0 + hull_align(4 * (size_t)(N + 1)) / 4;
-  const uint32_t rbase = (uint32_t)__cvta_generic_to_shared(ring) + 8u * lane;
+  // ring of slot 0: [HC0][32] lines, then slot 1: [HC1][32] lines; 256 B per position
+  uint32_t rb[K];
+  int hm[K];
+  rb[0] = (uint32_t)__cvta_generic_to_shared(ring) + 8u * lane;
+  hm[0] = HC0 - 1;
+  if constexpr (K == 2) {
+    rb[1] = rb[0] + 256u * HC0;
+    hm[1] = HC1 - 1;
+  }
   unsigned long long pops = 0, events = 0;
   int done_entries = 0;
 
@@ -207,12 +220,12 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
       const int32_t* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
       int32_t* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
       const bool chain_in = ps > 0, chain_out = ps + 1 < passes;
-      // Per slot: deque [f, b] (monotone counters; ring index & (HC-1)).  Cached in registers:
-      // B0 = line b (back), B1 = line b-1, X1 = line b-2, X2 = line b-3 (prefetched after the
-      // push), F0 = line f (front), F1 = line f+1.  A line is int2 (x = intercept b_s, y = s).
+      // Per slot: deque [f, b] (monotone counters; ring index & hm).  Cached in registers:
+      // B0 = line b (back), B1 = line b-1, X1..X3 = lines b-2..b-4 (prefetched after the
+      // push), F0 = line f (front), F1 = line f+1, F2 = line f+2.  A line is int2 (x = intercept b_s, y = s).
       // eo = e_m(j) (the running row minimum), op = opt_m(j).
       int f[K], b[K], eo[K], op[K], cnt[K];
-      int2 B0[K], B1[K], X1[K], X2[K], F0[K], F1[K];
+      int2 B0[K], B1[K], X1[K], X2[K], X3[K], F0[K], F1[K], F2[K];
       bool act[K];
       uint32_t* lg[K];
 #pragma unroll
@@ -226,7 +239,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
         cnt[k] = 1;
         lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * (N + 1);
         if (act[k]) lg[k][0] = (1u << 16) | 1u;
-        B0[k] = B1[k] = X1[k] = X2[k] = F0[k] = F1[k] = make_int2(0, 1);
+        B0[k] = B1[k] = X1[k] = X2[k] = X3[k] = F0[k] = F1[k] = F2[k] = make_int2(0, 1);
       }
       int32_t carry = 0, Pm1 = 0;
       int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
@@ -265,40 +278,43 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
           }
           int nop[K];
           {
-            // ---- c_j > 0: push line j, query the hull at x = P_j -------------------------
+            // ---- support row: push line j, query the hull at x = P_j -----------------------
             const int32_t Pj = __shfl_sync(FULL, Pc, i);
             ++ev_e;
             int bj[K], npop[K];
             bool more[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
+            for (int k = 0; k < K; ++k) {   // back tests from registers: up to four pops
               bj[k] = in[k] + j * Pm1;
               const int sz = b[k] - f[k];   // deque size - 1, before the push
               const bool t1 = dom3(B1[k], B0[k], bj[k], j);
               const bool t2 = dom3(X1[k], B1[k], bj[k], j);
               const bool t3 = dom3(X2[k], X1[k], bj[k], j);
+              const bool t4 = dom3(X3[k], X2[k], bj[k], j);
               const int p1 = (sz >= 1) & t1;
               const int p2 = p1 & (sz >= 2) & t2;
               const int p3 = p2 & (sz >= 3) & t3;
-              npop[k] = p1 + p2 + p3;
-              more[k] = act[k] & (p3 != 0);
+              const int p4 = p3 & (sz >= 4) & t4;
+              npop[k] = p1 + p2 + p3 + p4;
+              more[k] = act[k] & (p4 != 0);
             }
             int2 nb1[K];
             int top[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-              nb1[k] = npop[k] == 0 ? B0[k] : npop[k] == 1 ? B1[k] : npop[k] == 2 ? X1[k] : X2[k];
-              top[k] = b[k] - npop[k];   // index of the new second-to-back line
+              const int q = npop[k];
+              nb1[k] = q == 0 ? B0[k] : q == 1 ? B1[k] : q == 2 ? X1[k] : q == 3 ? X2[k] : X3[k];
+              top[k] = b[k] - q;   // index of the new second-to-back line
             }
             bool anymore = more[0];
             if constexpr (K == 2) anymore |= more[1];
-            if (__any_sync(FULL, anymore)) {   // rare: more than three pops
+            if (__any_sync(FULL, anymore)) {   // rare: more than four pops
 #pragma unroll
               for (int k = 0; k < K; ++k) {
                 if (!more[k]) continue;
-                const uint32_t rk = rbase + 256u * k;
+                const uint32_t rk = rb[k];
                 while (top[k] - f[k] >= 1) {
-                  const int2 l1 = lds2(rk + ((top[k] - 1) & (HC - 1)) * RSTRIDE);
+                  const int2 l1 = lds2(rk + ((top[k] - 1) & hm[k]) * 256u);
                   if (dom3(l1, nb1[k], bj[k], j)) {
                     --top[k];
                     nb1[k] = l1;
@@ -309,47 +325,68 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
                 }
               }
             }
-            int v0[K], v1[K];
+            int v0[K], v1[K], v2[K];
+            bool q1[K], q2[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
               pops_e += (unsigned)npop[k];
               const int nb = top[k] + 1;
               const int2 nl = make_int2(bj[k], j);
-              const uint32_t rk = rbase + 256u * k;
-              sts2(rk + (nb & (HC - 1)) * RSTRIDE, nl);
-              if (nb == f[k]) F0[k] = nl;                // the deque was empty
-              if (nb == f[k] + 1) F1[k] = nl;            // line f+1 was popped or is new
+              const uint32_t rk = rb[k];
+              sts2(rk + (nb & hm[k]) * 256u, nl);
+              const int d = nb - f[k];
+              if (d == 0) F0[k] = nl;   // the deque was empty
+              if (d == 1) F1[k] = nl;   // lines f+1 / f+2 popped or new
+              if (d == 2) F2[k] = nl;
               B1[k] = nb1[k];
               B0[k] = nl;
               b[k] = nb;
-              ovf |= act[k] & ((nb - f[k]) >= HC);
-              X1[k] = lds2(rk + ((nb - 2) & (HC - 1)) * RSTRIDE);   // next step's tests
-              X2[k] = lds2(rk + ((nb - 3) & (HC - 1)) * RSTRIDE);
+              ovf |= act[k] & (d > hm[k]);
+              X1[k] = lds2(rk + ((nb - 2) & hm[k]) * 256u);   // next row's back tests
+              X2[k] = lds2(rk + ((nb - 3) & hm[k]) * 256u);
+              X3[k] = lds2(rk + ((nb - 4) & hm[k]) * 256u);
               v0[k] = F0[k].x - F0[k].y * Pj;
               v1[k] = F1[k].x - F1[k].y * Pj;
+              v2[k] = F2[k].x - F2[k].y * Pj;
+              q1[k] = act[k] & (f[k] < b[k]) & (v1[k] < v0[k]);
+              q2[k] = q1[k] & (f[k] + 1 < b[k]) & (v2[k] < v1[k]);
             }
-            bool fpop[K];
-            bool anyf = false;
+            bool anyq2 = q2[0];
+            if constexpr (K == 2) anyq2 |= q2[1];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-              fpop[k] = act[k] & (f[k] < b[k]) & (v1[k] < v0[k]);
-              anyf |= fpop[k];
+            for (int k = 0; k < K; ++k) {   // one front pop from registers (common)
+              if (q1[k] & !q2[k]) {
+                ++f[k];
+                ++pops_e;
+                F0[k] = F1[k];
+                v0[k] = v1[k];
+                F1[k] = F2[k];
+                F2[k] = lds2(rb[k] + ((f[k] + 2) & hm[k]) * 256u);
+              }
             }
-            if (__any_sync(FULL, anyf)) {   // rare: the front moves
+            if (__any_sync(FULL, anyq2)) {   // rare: the front moves by two or more
 #pragma unroll
               for (int k = 0; k < K; ++k) {
-                if (!fpop[k]) continue;
-                const uint32_t rk = rbase + 256u * k;
-                do {
-                  ++f[k];
-                  ++pops_e;
-                  F0[k] = F1[k];
-                  v0[k] = v1[k];
-                  if (f[k] < b[k]) {
-                    F1[k] = lds2(rk + ((f[k] + 1) & (HC - 1)) * RSTRIDE);
-                    v1[k] = F1[k].x - F1[k].y * Pj;
+                if (!q2[k]) continue;
+                const uint32_t rk = rb[k];
+                f[k] += 2;
+                pops_e += 2;
+                F0[k] = F2[k];
+                v0[k] = v2[k];
+                while (f[k] < b[k]) {
+                  const int2 l1 = lds2(rk + ((f[k] + 1) & hm[k]) * 256u);
+                  const int vl = l1.x - l1.y * Pj;
+                  if (vl < v0[k]) {
+                    ++f[k];
+                    ++pops_e;
+                    F0[k] = l1;
+                    v0[k] = vl;
+                  } else {
+                    break;
                   }
-                } while (f[k] < b[k] && v1[k] < v0[k]);
+                }
+                F1[k] = lds2(rk + ((f[k] + 1) & hm[k]) * 256u);
+                F2[k] = lds2(rk + ((f[k] + 2) & hm[k]) * 256u);
               }
             }
 #pragma unroll

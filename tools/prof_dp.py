@@ -31,7 +31,9 @@ for r in range(a.reps):
     st = sp.dp_stats(ws)
     print(f"dp rep {r}: {s.elapsed_time(e):.3f} ms  cells={a.entries*cfg.N*M:.3e} "
           f"evals/cell={st['evaluations']/(a.entries*cfg.N*M):.2f}  "
-          f"Mcells/s={a.entries*cfg.N*M/s.elapsed_time(e)/1e3:.1f}", flush=True)
+          f"Mcells/s={a.entries*cfg.N*M/s.elapsed_time(e)/1e3:.1f}  "
+          f"hull={st['entries_hull']} support_rows/entry={st['hull_event_rows']/max(1,st['entries_hull']):.0f} "
+          f"pops/support-cell={st['hull_pops']/max(1,st['hull_event_rows']*M):.3f}", flush=True)
 if a.lcp:
     tr = wl.make_trace(cfg, seed=0, device=dev)
     lcp = torch.empty(tr["req_off"].numel() - 1, dtype=torch.int32, device=dev)

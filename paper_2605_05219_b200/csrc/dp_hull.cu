@@ -168,15 +168,10 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
   int32_t* ebuf0 = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M) + hull_cnt_bytes(M));
   int32_t* ebuf1 = ebuf0 + hull_align(4 * (size_t)(N + 1)) / 4;
-  // ring of slot 0: [HC0][32] lines, then slot 1: [HC1][32] lines; 256 B per position
-  uint32_t rb[K];
+  // ring of slot 0: [HC0][32] lines, then slot 1: [HC1][32] lines (256 B per position)
   int hm[K];
-  rb[0] = (uint32_t)__cvta_generic_to_shared(ring) + 8u * lane;
   hm[0] = HC0 - 1;
-  if constexpr (K == 2) {
-    rb[1] = rb[0] + 256u * HC0;
-    hm[1] = HC1 - 1;
-  }
+  if constexpr (K == 2) hm[1] = HC1 - 1;
   unsigned long long pops = 0, events = 0;
   int done_entries = 0;
 
@@ -220,14 +215,15 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
       const int32_t* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
       int32_t* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
       const bool chain_in = ps > 0, chain_out = ps + 1 < passes;
-      // Per slot: deque [f, b] (monotone counters; ring index & hm).  Cached in registers:
-      // B0 = line b (back), B1 = line b-1, X1..X3 = lines b-2..b-4 (prefetched after the
-      // push), F0 = line f (front), F1 = line f+1, F2 = line f+2.  A line is int2 (x = intercept b_s, y = s).
-      // eo = e_m(j) (the running row minimum), op = opt_m(j).
-      int f[K], b[K], eo[K], op[K], cnt[K];
-      int2 B0[K], B1[K], X1[K], X2[K], X3[K], F0[K], F1[K], F2[K];
+      // Per slot: deque [f, b] (monotone counters; ring position & hm).  In registers: the back
+      // line B0 (the last one pushed) and the front line F0; the four lines below the back and
+      // the two above the front are loaded from the ring at the top of every support row (their
+      // positions are known a row ahead, so the loads overlap the shuffle).  A line is int2
+      // (x = intercept b_s, y = s).  eo = e_m(j) (the running row value), op = opt_m(j).
+      int f[K], b[K], eo[K], op[K];
+      int2 B0[K], F0[K];
       bool act[K];
-      uint32_t* lg[K];
+      uint32_t* lgp[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int mk = ps * L + 32 * k + lane + 1;
@@ -236,10 +232,9 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
         b[k] = -1;
         eo[k] = 0;   // e_m(0) = 0 (reading R1)
         op[k] = 1;   // opt_m(1) = 1 whatever the row type: logged up front
-        cnt[k] = 1;
-        lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * (N + 1);
-        if (act[k]) lg[k][0] = (1u << 16) | 1u;
-        B0[k] = B1[k] = X1[k] = X2[k] = X3[k] = F0[k] = F1[k] = F2[k] = make_int2(0, 1);
+        lgp[k] = logs + (size_t)(ps * L + 32 * k + lane) * (N + 1);
+        if (act[k]) *lgp[k]++ = (1u << 16) | 1u;
+        B0[k] = F0[k] = make_int2(0, 1);
       }
       int32_t carry = 0, Pm1 = 0;
       int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
@@ -265,6 +260,18 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
           const int i = __ffs(evmask) - 1;
           evmask &= evmask - 1;
           const int j = jb + 1 + i;
+          // ring lines around both ends (positions fixed by the previous row)
+          int2 L1[K], L2[K], L3[K], L4[K], G1[K], G2[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int so = k ? HC0 * 32 : 0;
+            L1[k] = ring[so + (((b[k] - 1) & hm[k]) << 5) + lane];
+            L2[k] = ring[so + (((b[k] - 2) & hm[k]) << 5) + lane];
+            L3[k] = ring[so + (((b[k] - 3) & hm[k]) << 5) + lane];
+            L4[k] = ring[so + (((b[k] - 4) & hm[k]) << 5) + lane];
+            G1[k] = ring[so + (((f[k] + 1) & hm[k]) << 5) + lane];
+            G2[k] = ring[so + (((f[k] + 2) & hm[k]) << 5) + lane];
+          }
           // e_{m-1}(j-1): from the lane below (its value at the previous support row);
           // lane 0 slot 0 from the previous pass (or e_0 = 0)
           int32_t in[K];
@@ -276,134 +283,100 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
             const int32_t t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
             in[1] = lane ? t1 : t0;
           }
-          int nop[K];
-          {
-            // ---- support row: push line j, query the hull at x = P_j -----------------------
-            const int32_t Pj = __shfl_sync(FULL, Pc, i);
-            ++ev_e;
-            int bj[K], npop[K];
-            bool more[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {   // back tests from registers: up to four pops
-              bj[k] = in[k] + j * Pm1;
-              const int sz = b[k] - f[k];   // deque size - 1, before the push
-              const bool t1 = dom3(B1[k], B0[k], bj[k], j);
-              const bool t2 = dom3(X1[k], B1[k], bj[k], j);
-              const bool t3 = dom3(X2[k], X1[k], bj[k], j);
-              const bool t4 = dom3(X3[k], X2[k], bj[k], j);
-              const int p1 = (sz >= 1) & t1;
-              const int p2 = p1 & (sz >= 2) & t2;
-              const int p3 = p2 & (sz >= 3) & t3;
-              const int p4 = p3 & (sz >= 4) & t4;
-              npop[k] = p1 + p2 + p3 + p4;
-              more[k] = act[k] & (p4 != 0);
-            }
-            int2 nb1[K];
-            int top[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              const int q = npop[k];
-              nb1[k] = q == 0 ? B0[k] : q == 1 ? B1[k] : q == 2 ? X1[k] : q == 3 ? X2[k] : X3[k];
-              top[k] = b[k] - q;   // index of the new second-to-back line
-            }
-            bool anymore = more[0];
-            if constexpr (K == 2) anymore |= more[1];
-            if (__any_sync(FULL, anymore)) {   // rare: more than four pops
-#pragma unroll
-              for (int k = 0; k < K; ++k) {
-                if (!more[k]) continue;
-                const uint32_t rk = rb[k];
-                while (top[k] - f[k] >= 1) {
-                  const int2 l1 = lds2(rk + ((top[k] - 1) & hm[k]) * 256u);
-                  if (dom3(l1, nb1[k], bj[k], j)) {
-                    --top[k];
-                    nb1[k] = l1;
-                    ++npop[k];
-                  } else {
-                    break;
-                  }
-                }
-              }
-            }
-            int v0[K], v1[K], v2[K];
-            bool q1[K], q2[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              pops_e += (unsigned)npop[k];
-              const int nb = top[k] + 1;
-              const int2 nl = make_int2(bj[k], j);
-              const uint32_t rk = rb[k];
-              sts2(rk + (nb & hm[k]) * 256u, nl);
-              const int d = nb - f[k];
-              if (d == 0) F0[k] = nl;   // the deque was empty
-              if (d == 1) F1[k] = nl;   // lines f+1 / f+2 popped or new
-              if (d == 2) F2[k] = nl;
-              B1[k] = nb1[k];
-              B0[k] = nl;
-              b[k] = nb;
-              ovf |= act[k] & (d > hm[k]);
-              X1[k] = lds2(rk + ((nb - 2) & hm[k]) * 256u);   // next row's back tests
-              X2[k] = lds2(rk + ((nb - 3) & hm[k]) * 256u);
-              X3[k] = lds2(rk + ((nb - 4) & hm[k]) * 256u);
-              v0[k] = F0[k].x - F0[k].y * Pj;
-              v1[k] = F1[k].x - F1[k].y * Pj;
-              v2[k] = F2[k].x - F2[k].y * Pj;
-              q1[k] = act[k] & (f[k] < b[k]) & (v1[k] < v0[k]);
-              q2[k] = q1[k] & (f[k] + 1 < b[k]) & (v2[k] < v1[k]);
-            }
-            bool anyq2 = q2[0];
-            if constexpr (K == 2) anyq2 |= q2[1];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {   // one front pop from registers (common)
-              if (q1[k] & !q2[k]) {
-                ++f[k];
-                ++pops_e;
-                F0[k] = F1[k];
-                v0[k] = v1[k];
-                F1[k] = F2[k];
-                F2[k] = lds2(rb[k] + ((f[k] + 2) & hm[k]) * 256u);
-              }
-            }
-            if (__any_sync(FULL, anyq2)) {   // rare: the front moves by two or more
-#pragma unroll
-              for (int k = 0; k < K; ++k) {
-                if (!q2[k]) continue;
-                const uint32_t rk = rb[k];
-                f[k] += 2;
-                pops_e += 2;
-                F0[k] = F2[k];
-                v0[k] = v2[k];
-                while (f[k] < b[k]) {
-                  const int2 l1 = lds2(rk + ((f[k] + 1) & hm[k]) * 256u);
-                  const int vl = l1.x - l1.y * Pj;
-                  if (vl < v0[k]) {
-                    ++f[k];
-                    ++pops_e;
-                    F0[k] = l1;
-                    v0[k] = vl;
-                  } else {
-                    break;
-                  }
-                }
-                F1[k] = lds2(rk + ((f[k] + 1) & hm[k]) * 256u);
-                F2[k] = lds2(rk + ((f[k] + 2) & hm[k]) * 256u);
-              }
-            }
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              eo[k] = v0[k];
-              nop[k] = F0[k].y;
-            }
-            Pm1 = Pj;
-          }
-          // argmin change log
+          const int32_t Pj = __shfl_sync(FULL, Pc, i);
+          ++ev_e;
+          // ---- push line j: up to four back pops decided from the loaded lines -------------
+          int bj[K], top[K];
+          bool more[K];
 #pragma unroll
           for (int k = 0; k < K; ++k) {
-            if (act[k] & (nop[k] != op[k])) {
-              lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop[k];
-              ++cnt[k];
+            bj[k] = in[k] + j * Pm1;
+            const int sz = b[k] - f[k];   // deque size - 1, before the push
+            const int p1 = (sz >= 1) & dom3(L1[k], B0[k], bj[k], j);
+            const int p2 = p1 & (sz >= 2) & dom3(L2[k], L1[k], bj[k], j);
+            const int p3 = p2 & (sz >= 3) & dom3(L3[k], L2[k], bj[k], j);
+            const int p4 = p3 & (sz >= 4) & dom3(L4[k], L3[k], bj[k], j);
+            top[k] = b[k] - (p1 + p2 + p3 + p4);   // position of the new second-to-back line
+            more[k] = act[k] & (p4 != 0);
+          }
+          bool anymore = more[0];
+          if constexpr (K == 2) anymore |= more[1];
+          if (__any_sync(FULL, anymore)) {   // rare: more than four pops
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              if (!more[k]) continue;
+              const int so = k ? HC0 * 32 : 0;
+              int2 cur = L4[k];
+              while (top[k] - f[k] >= 1) {
+                const int2 l1 = ring[so + (((top[k] - 1) & hm[k]) << 5) + lane];
+                if (dom3(l1, cur, bj[k], j)) {
+                  --top[k];
+                  cur = l1;
+                } else {
+                  break;
+                }
+              }
             }
-            op[k] = nop[k];
+          }
+          int2 F1[K], F2[K];
+          int v0[K], v1[K], v2[K];
+          bool q1[K], q2[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int so = k ? HC0 * 32 : 0;
+            const int nb = top[k] + 1;
+            pops_e += (unsigned)(b[k] + 1 - nb);
+            const int2 nl = make_int2(bj[k], j);
+            ring[so + ((nb & hm[k]) << 5) + lane] = nl;
+            const int d = nb - f[k];
+            F0[k] = d == 0 ? nl : F0[k];   // the deque was empty
+            F1[k] = d == 1 ? nl : G1[k];   // lines f+1 / f+2 popped or new
+            F2[k] = d == 2 ? nl : G2[k];
+            B0[k] = nl;
+            b[k] = nb;
+            ovf |= act[k] & (d > hm[k]);
+            // ---- query x = P_j: up to one front pop decided from the loaded lines -----------
+            v0[k] = F0[k].x - F0[k].y * Pj;
+            v1[k] = F1[k].x - F1[k].y * Pj;
+            v2[k] = F2[k].x - F2[k].y * Pj;
+            q1[k] = act[k] & (d >= 1) & (v1[k] < v0[k]);
+            q2[k] = q1[k] & (d >= 2) & (v2[k] < v1[k]);
+            const bool one = q1[k] & !q2[k];
+            f[k] += one;
+            F0[k] = one ? F1[k] : F0[k];
+            v0[k] = one ? v1[k] : v0[k];
+          }
+          bool anyq2 = q2[0];
+          if constexpr (K == 2) anyq2 |= q2[1];
+          if (__any_sync(FULL, anyq2)) {   // rare: the front moves by two or more
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              if (!q2[k]) continue;
+              const int so = k ? HC0 * 32 : 0;
+              f[k] += 2;
+              F0[k] = F2[k];
+              v0[k] = v2[k];
+              while (f[k] < b[k]) {
+                const int2 l1 = ring[so + (((f[k] + 1) & hm[k]) << 5) + lane];
+                const int vl = l1.x - l1.y * Pj;
+                if (vl < v0[k]) {
+                  ++f[k];
+                  F0[k] = l1;
+                  v0[k] = vl;
+                } else {
+                  break;
+                }
+              }
+            }
+          }
+          Pm1 = Pj;
+          // ---- row value, argmin change log -------------------------------------------------
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            eo[k] = v0[k];
+            const int nop = F0[k].y;
+            if (act[k] & (nop != op[k])) *lgp[k]++ = ((uint32_t)j << 16) | (uint32_t)nop;
+            op[k] = nop;
           }
           if (chain_out && lane == 31) eout_buf[evbase + q] = eo[K - 1];
         }
@@ -418,7 +391,8 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
         for (int k = 0; k < K; ++k) {
           if (!act[k]) continue;
           const int mk = ps * L + 32 * k + lane + 1;
-          logn[ps * L + 32 * k + lane] = cnt[k];
+          logn[ps * L + 32 * k + lane] =
+              (int)(lgp[k] - (logs + (size_t)(ps * L + 32 * k + lane) * (N + 1)));
           const long long V = TN + (long long)eo[k];   // V_m = T_N + e_m(N)
           if (p.cbb) p.cbb[(int64_t)e * (M + 1) + mk] = V;
           if (mk == M) p.cost[e] = V;

@@ -26,6 +26,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DP cells/s (entries*N*M)"
+TRAFFIC_JSON = "r01b_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
 UNIT = "cells/s"
 
 
@@ -426,20 +427,23 @@ def run_ours(args):
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
-    # DP roofline: INT-ALU pipe bound (min-plus, no tensor cores).  One candidate evaluation
-    # v = b_s - s P_j with a leftmost-argmin update is 1 IMAD (FMA pipe) + 3 ALU-pipe ops
-    # (ISETP + 2 SEL); the ALU pipe issues 64 lanes/clk/SM (16/clk/SMSP) => peak
-    # = SMs * f_max * 64 / 3 evaluations/s.
-    evals_per_launch = stats["evaluations"]          # exact, from the kernel's own counter
+    # DP roofline: INT-ALU bound, no tensor cores (min-plus).  The algorithmic
+    # unit is one hull update -- one (layer, support row) step of the paper's monotone CHT
+    # (P:764-773): intercept, amortised back-pop tests, push, front test, query -- counted
+    # exactly by the kernel (support rows x M).  Its minimal INT-pipe cost is UPD_OPS thread
+    # instructions (DESIGN.md derivation); the INT pipes (ALU + FMA, 64 lanes/clk/SM each)
+    # retire 128 thread-ops/clk/SM, so peak = SMs * f_max * 128 / UPD_OPS updates/s.
+    UPD_OPS = 24
+    updates = stats["hull_event_rows"] * M
     traffic = {}
     try:   # DRAM bytes per launch from the committed `ncu --set full` capture (W5 config)
         if args.workload == "W5" and E_own == 16384:
-            traffic = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+            traffic = json.load(open(os.path.join(ROOT, "profiles", TRAFFIC_JSON)))
     except Exception:
         traffic = {}
     dp_launch_s = dp_ms / K / 1e3
-    achieved = evals_per_launch / dp_launch_s / 1e9
-    peak = sms * sm_max * 1e6 * 64 / 3 / 1e9
+    achieved = updates / dp_launch_s / 1e9
+    peak = sms * sm_max * 1e6 * 128 / UPD_OPS / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True,
@@ -449,20 +453,27 @@ def run_ours(args):
         "lcp_tokens_per_s": tokens_all * K / (lcp_ms / 1e3),
         "stage_ms_per_step": {"lcp_hist": lcp_ms / K, "merge": merge_ms / K, "dp": dp_ms / K,
                               "eval": eval_ms / K},
-        "roofline": {"bound": "alu", "kernel": "dp_place_kernel", "achieved": achieved,
-                     "peak": peak, "unit": "Geval/s", "frac": achieved / peak,
-                     "traffic": traffic.get("dp_place_kernel<int>", {}).get("traffic_bytes"),
-                     "work": f"{evals_per_launch} candidate evaluations per launch "
-                             f"({evals_per_launch / (E_own * N * M):.2f} per DP cell)",
-                     "peak_basis": f"{sms} SMs x {sm_max:.0f} MHz x 64 ALU lanes / 3 ops"},
+        "roofline": {"bound": "alu", "kernel": "dp_hull_kernel", "achieved": achieved,
+                     "peak": peak, "unit": "Gupd/s", "frac": achieved / peak,
+                     "traffic": traffic.get("dp_hull_kernel<int, 2>", {}).get("traffic_bytes"),
+                     "work": f"{updates} hull updates per launch = {stats['hull_event_rows']} "
+                             f"support rows x M (support rows = {stats['hull_event_rows'] / max(1, stats['entries_hull']) / N:.3f} "
+                             f"of N per entry; zero-count rows are exact no-ops); "
+                             f"{stats['entries_hull']} entries on the hull kernel, "
+                             f"{E_own - stats['entries_hull']} on the D&C fallback "
+                             f"({stats['evaluations']} candidate evaluations)",
+                     "peak_basis": f"{sms} SMs x {sm_max:.0f} MHz x 128 INT lanes / "
+                                   f"{UPD_OPS} INT ops per hull update"},
         "roofline_lcp": {"bound": "hbm", "kernel": "lcp_hist_kernel",
                          "achieved": lcp_bytes_all * K / (lcp_ms / 1e3) / 1e9 / world,
                          "peak": hbm_peak, "unit": "GB/s",
                          "frac": lcp_bytes_all * K / (lcp_ms / 1e3) / 1e9 / world / hbm_peak,
                          "traffic": traffic.get("lcp_hist_kernel", {}).get("traffic_bytes"),
                          "algorithmic_bytes": lcp_bytes_all / world},
-        "dp_paths": {k: v for k, v in stats.items() if k != "evaluations"},
-        "gpu_launches": K * (3 + (1 if world > 1 and args.merge == "sparse" else 0)),
+        "dp_paths": {k: v for k, v in stats.items()},
+        # per step: lcp_hist, dp_hull, dp_place (D&C fallback list; exits at once when empty),
+        # eval (+ accumulate_depths for the sparse merge)
+        "gpu_launches": K * (4 + (1 if world > 1 and args.merge == "sparse" else 0)),
         "clocks": clk,
         "e2e": e2e,
     }

@@ -54,6 +54,12 @@ namespace sp {
 #define SP_HULL_CAP1 32
 #endif
 constexpr int HC0 = SP_HULL_CAP0, HC1 = SP_HULL_CAP1;
+// An entry whose hull outgrows a shared ring is re-run at once by the same warp on a global
+// overflow ring of HCG lines per layer, taken from a pool of HPOOL rings (a 64-bit occupancy mask
+// in the workspace head); only if that overflows too (or the pool is busy) does it go to the
+// divide-and-conquer kernel.
+constexpr int HCG = 2048;
+constexpr int HPOOL = 32;
 static_assert((HC0 & (HC0 - 1)) == 0 && (HC1 & (HC1 - 1)) == 0, "ring capacities: powers of two");
 
 __host__ __device__ __forceinline__ size_t hull_align(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -92,7 +98,31 @@ struct HullParams {
   int32_t* fb;      // fallback entry list
   uint8_t* slots;   // per-warp slots
   size_t slot;
+  int2* gring;      // HPOOL global overflow rings, [ring][slot][HCG][32] lines
 };
+
+__host__ __device__ __forceinline__ size_t hull_pool_bytes(int M) {
+  return (size_t)HPOOL * hull_K(M) * HCG * 32 * sizeof(int2);
+}
+
+// claim / return a global overflow ring (lane 0 only)
+__device__ __forceinline__ int pool_acquire(const HullParams& p) {
+  unsigned long long* mask = reinterpret_cast<unsigned long long*>(p.ws + SP_WS_POOL_OFF);
+  unsigned long long m = *reinterpret_cast<volatile unsigned long long*>(mask);
+  for (int tries = 0; tries < 64; ++tries) {
+    const unsigned long long fr = ~m & ((HPOOL == 64) ? ~0ull : ((1ull << HPOOL) - 1));
+    if (!fr) return -1;
+    const int g = __ffsll((long long)fr) - 1;
+    const unsigned long long old = atomicOr(mask, 1ull << g);
+    if (!(old & (1ull << g))) return g;
+    m = old | (1ull << g);
+  }
+  return -1;
+}
+__device__ __forceinline__ void pool_release(const HullParams& p, int g) {
+  __threadfence();
+  atomicAnd(reinterpret_cast<unsigned long long*>(p.ws + SP_WS_POOL_OFF), ~(1ull << g));
+}
 
 // back-pop test, int32 inputs exact (0 <= b <= nN < 2^30, so differences fit int32): the back
 // line (s2, b2) goes if it is not strictly below the segment (s1, b1) -> (j, bj), i.e.
@@ -153,6 +183,216 @@ __device__ __forceinline__ int log_lookup_lane(const uint32_t* lg, int cnt, int 
   return (int)(__ldcg(lg + lo) & 0xffffu);
 }
 
+// a4 for one entry: all layers in lockstep, one support row per step.  The rings live at rg
+// (shared memory, or a global overflow ring when GR) with slot-1 offset so1 and position masks hm.
+// Returns true when a ring overflowed (the entry's results are then invalid).
+template <typename WT, int K, bool GR>
+__device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
+                                        long long TN, int n32, int2* __restrict__ rg, int so1,
+                                        const int (&hm)[K], uint32_t* logs, int32_t* logn,
+                                        int32_t* ebuf0, int32_t* ebuf1, unsigned& pops_e,
+                                        unsigned& ev_e) {
+  const int lane = lane_id();
+  const int N = p.N, M = p.M;
+  constexpr int L = 32 * K;
+  const int passes = (M + L - 1) / L;
+    // ---- a4: all layers in lockstep, one row per step ---------------------------------------
+    bool ovf = false;
+    for (int ps = 0; ps < passes && !ovf; ++ps) {
+      const int32_t* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
+      int32_t* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
+      const bool chain_in = ps > 0, chain_out = ps + 1 < passes;
+      // Per slot: deque [f, b] (monotone counters; ring position & hm).  In registers: the back
+      // line B0 (the last one pushed) and the front line F0; the four lines below the back and
+      // the two above the front are loaded from the ring at the top of every support row (their
+      // positions are known a row ahead, so the loads overlap the shuffle).  A line is int2
+      // (x = intercept b_s, y = s).  eo = e_m(j) (the running row value), op = opt_m(j).
+      int f[K], b[K], eo[K], op[K];
+      int2 B0[K], F0[K];
+      bool act[K];
+      uint32_t* lgp[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int mk = ps * L + 32 * k + lane + 1;
+        act[k] = mk <= M;
+        f[k] = 0;
+        b[k] = -1;
+        eo[k] = 0;   // e_m(0) = 0 (reading R1)
+        op[k] = 1;   // opt_m(1) = 1 whatever the row type: logged up front
+        lgp[k] = logs + (size_t)(ps * L + 32 * k + lane) * (N + 1);
+        if (act[k]) *lgp[k]++ = (1u << 16) | 1u;
+        B0[k] = F0[k] = make_int2(0, 1);
+      }
+      int32_t carry = 0, Pm1 = 0;
+      int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
+      for (int jb = 0; jb < N; jb += 32) {
+        const int jr = jb + 1 + lane;
+        const int32_t craw = jr <= N ? (int32_t)we[jr] : 0;
+        unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
+        if (evmask == 0) continue;                          // 32 zero rows: nothing changes
+        int32_t cnt32 = craw;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(FULL, cnt32, o);
+          if (lane >= o) cnt32 += y;
+        }
+        const int32_t Pc = carry + cnt32;
+        carry = __shfl_sync(FULL, Pc, 31);
+        // previous pass's top layer at the support rows: e(j-1) of support row number t is its
+        // value at support row t-1 (constant over zero rows), 0 before the first
+        int32_t Ec = 0;
+        const int nev = __popc(evmask);
+        if (chain_in && lane < nev) Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
+        for (int q = 0; evmask; ++q) {
+          const int i = __ffs(evmask) - 1;
+          evmask &= evmask - 1;
+          const int j = jb + 1 + i;
+          // ring lines around both ends (positions fixed by the previous row)
+          int2 L1[K], L2[K], L3[K], L4[K], G1[K], G2[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int so = k ? so1 : 0;
+            L1[k] = rg[so + (((b[k] - 1) & hm[k]) << 5) + lane];
+            L2[k] = rg[so + (((b[k] - 2) & hm[k]) << 5) + lane];
+            L3[k] = rg[so + (((b[k] - 3) & hm[k]) << 5) + lane];
+            L4[k] = rg[so + (((b[k] - 4) & hm[k]) << 5) + lane];
+            G1[k] = rg[so + (((f[k] + 1) & hm[k]) << 5) + lane];
+            G2[k] = rg[so + (((f[k] + 2) & hm[k]) << 5) + lane];
+          }
+          // e_{m-1}(j-1): from the lane below (its value at the previous support row);
+          // lane 0 slot 0 from the previous pass (or e_0 = 0)
+          int32_t in[K];
+          const int32_t t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
+          int32_t ext = 0;
+          if (chain_in) ext = __shfl_sync(FULL, Ec, q);
+          in[0] = lane ? t0 : ext;
+          if constexpr (K == 2) {
+            const int32_t t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
+            in[1] = lane ? t1 : t0;
+          }
+          const int32_t Pj = __shfl_sync(FULL, Pc, i);
+          ++ev_e;
+          // ---- push line j: up to four back pops decided from the loaded lines -------------
+          int bj[K], top[K];
+          bool more[K], skip[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            bj[k] = in[k] + j * Pm1;
+            // a line that overtakes the back line only beyond x = P_N = n is never optimal at
+            // any query (x <= n): it is neither pushed nor allowed to pop
+            skip[k] = (b[k] >= f[k]) & (bj[k] - B0[k].x > n32 * (j - B0[k].y));
+            const int sz = skip[k] ? 0 : b[k] - f[k];   // deque size - 1, before the push
+            const int p1 = (sz >= 1) & dom3(L1[k], B0[k], bj[k], j);
+            const int p2 = p1 & (sz >= 2) & dom3(L2[k], L1[k], bj[k], j);
+            const int p3 = p2 & (sz >= 3) & dom3(L3[k], L2[k], bj[k], j);
+            const int p4 = p3 & (sz >= 4) & dom3(L4[k], L3[k], bj[k], j);
+            top[k] = b[k] - (p1 + p2 + p3 + p4);   // position of the new second-to-back line
+            more[k] = act[k] & (p4 != 0);
+          }
+          bool anymore = more[0];
+          if constexpr (K == 2) anymore |= more[1];
+          if (__any_sync(FULL, anymore)) {   // rare: more than four pops
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              if (!more[k]) continue;
+              const int so = k ? so1 : 0;
+              int2 cur = L4[k];
+              while (top[k] - f[k] >= 1) {
+                const int2 l1 = rg[so + (((top[k] - 1) & hm[k]) << 5) + lane];
+                if (dom3(l1, cur, bj[k], j)) {
+                  --top[k];
+                  cur = l1;
+                } else {
+                  break;
+                }
+              }
+            }
+          }
+          int2 F1[K], F2[K];
+          int v0[K], v1[K], v2[K];
+          bool q1[K], q2[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int so = k ? so1 : 0;
+            const int nb = skip[k] ? b[k] : top[k] + 1;
+            pops_e += (unsigned)(b[k] - top[k]);
+            const int2 nl = skip[k] ? B0[k] : make_int2(bj[k], j);
+            if (!skip[k]) rg[so + ((nb & hm[k]) << 5) + lane] = nl;
+            const int d = nb - f[k];
+            F0[k] = (!skip[k] & (d == 0)) ? nl : F0[k];   // the deque was empty
+            F1[k] = (!skip[k] & (d == 1)) ? nl : G1[k];   // lines f+1 / f+2 popped or new
+            F2[k] = (!skip[k] & (d == 2)) ? nl : G2[k];
+            B0[k] = nl;
+            b[k] = nb;
+            ovf |= act[k] & (d > hm[k]);
+            // ---- query x = P_j: up to one front pop decided from the loaded lines -----------
+            v0[k] = F0[k].x - F0[k].y * Pj;
+            v1[k] = F1[k].x - F1[k].y * Pj;
+            v2[k] = F2[k].x - F2[k].y * Pj;
+            q1[k] = act[k] & (d >= 1) & (v1[k] < v0[k]);
+            q2[k] = q1[k] & (d >= 2) & (v2[k] < v1[k]);
+            const bool one = q1[k] & !q2[k];
+            f[k] += one;
+            F0[k] = one ? F1[k] : F0[k];
+            v0[k] = one ? v1[k] : v0[k];
+          }
+          bool anyq2 = q2[0];
+          if constexpr (K == 2) anyq2 |= q2[1];
+          if (__any_sync(FULL, anyq2)) {   // rare: the front moves by two or more
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              if (!q2[k]) continue;
+              const int so = k ? so1 : 0;
+              f[k] += 2;
+              F0[k] = F2[k];
+              v0[k] = v2[k];
+              while (f[k] < b[k]) {
+                const int2 l1 = rg[so + (((f[k] + 1) & hm[k]) << 5) + lane];
+                const int vl = l1.x - l1.y * Pj;
+                if (vl < v0[k]) {
+                  ++f[k];
+                  F0[k] = l1;
+                  v0[k] = vl;
+                } else {
+                  break;
+                }
+              }
+            }
+          }
+          Pm1 = Pj;
+          // ---- row value, argmin change log -------------------------------------------------
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            eo[k] = v0[k];
+            const int nop = F0[k].y;
+            if (act[k] & (nop != op[k])) *lgp[k]++ = ((uint32_t)j << 16) | (uint32_t)nop;
+            op[k] = nop;
+          }
+          if (chain_out && lane == 31) eout_buf[evbase + q] = eo[K - 1];
+        }
+        evbase += nev;
+        if (__any_sync(FULL, ovf)) {
+          ovf = true;
+          break;
+        }
+      }
+      if (!ovf) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (!act[k]) continue;
+          const int mk = ps * L + 32 * k + lane + 1;
+          logn[ps * L + 32 * k + lane] =
+              (int)(lgp[k] - (logs + (size_t)(ps * L + 32 * k + lane) * (N + 1)));
+          const long long V = TN + (long long)eo[k];   // V_m = T_N + e_m(N)
+          if (p.cbb) p.cbb[(int64_t)e * (M + 1) + mk] = V;
+          if (mk == M) p.cost[e] = V;
+        }
+      }
+      __syncwarp();   // chained e-row and logs visible to the whole warp
+    }
+  return ovf;
+}
+
 template <typename WT, int K>
 __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   extern __shared__ __align__(16) int2 ring[];   // slot rings [HC0][32] | [HC1][32] lines (b, s)
@@ -207,198 +447,30 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
     if (lane == 0) {
       if (p.cbb) p.cbb[(int64_t)e * (M + 1)] = TN;   // V_0 = T_N
     }
+    const int n32 = (int)n;   // P_N; n N < 2^30, so n (j - s) fits int32
 
-    // ---- a4: all layers in lockstep, one row per step ---------------------------------------
-    bool ovf = false;
+    // ---- a4: all layers in lockstep, one support row per step --------------------------------
     unsigned pops_e = 0, ev_e = 0;
-    for (int ps = 0; ps < passes && !ovf; ++ps) {
-      const int32_t* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
-      int32_t* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
-      const bool chain_in = ps > 0, chain_out = ps + 1 < passes;
-      // Per slot: deque [f, b] (monotone counters; ring position & hm).  In registers: the back
-      // line B0 (the last one pushed) and the front line F0; the four lines below the back and
-      // the two above the front are loaded from the ring at the top of every support row (their
-      // positions are known a row ahead, so the loads overlap the shuffle).  A line is int2
-      // (x = intercept b_s, y = s).  eo = e_m(j) (the running row value), op = opt_m(j).
-      int f[K], b[K], eo[K], op[K];
-      int2 B0[K], F0[K];
-      bool act[K];
-      uint32_t* lgp[K];
+#ifdef SP_HULL_FORCE_GLOBAL   // experiment: every entry on a global ring
+    bool ovf = true;
+#else
+    bool ovf = hull_dp<WT, K, false>(p, we, e, TN, n32, ring, HC0 * 32, hm, logs, logn, ebuf0,
+                                     ebuf1, pops_e, ev_e);
+#endif
+    if (ovf) {   // retry with a global overflow ring from the pool (rare)
+      int g = -1;
+      if (lane == 0) g = pool_acquire(p);
+      g = __shfl_sync(FULL, g, 0);
+      if (g >= 0) {
+        int hg[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int mk = ps * L + 32 * k + lane + 1;
-        act[k] = mk <= M;
-        f[k] = 0;
-        b[k] = -1;
-        eo[k] = 0;   // e_m(0) = 0 (reading R1)
-        op[k] = 1;   // opt_m(1) = 1 whatever the row type: logged up front
-        lgp[k] = logs + (size_t)(ps * L + 32 * k + lane) * (N + 1);
-        if (act[k]) *lgp[k]++ = (1u << 16) | 1u;
-        B0[k] = F0[k] = make_int2(0, 1);
+        for (int k = 0; k < K; ++k) hg[k] = HCG - 1;
+        pops_e = ev_e = 0;
+        ovf = hull_dp<WT, K, true>(p, we, e, TN, n32, p.gring + (size_t)g * K * HCG * 32,
+                                   HCG * 32, hg, logs, logn, ebuf0, ebuf1, pops_e, ev_e);
+        __syncwarp();
+        if (lane == 0) pool_release(p, g);
       }
-      int32_t carry = 0, Pm1 = 0;
-      int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
-      for (int jb = 0; jb < N; jb += 32) {
-        const int jr = jb + 1 + lane;
-        const int32_t craw = jr <= N ? (int32_t)we[jr] : 0;
-        unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
-        if (evmask == 0) continue;                          // 32 zero rows: nothing changes
-        int32_t cnt32 = craw;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int32_t y = __shfl_up_sync(FULL, cnt32, o);
-          if (lane >= o) cnt32 += y;
-        }
-        const int32_t Pc = carry + cnt32;
-        carry = __shfl_sync(FULL, Pc, 31);
-        // previous pass's top layer at the support rows: e(j-1) of support row number t is its
-        // value at support row t-1 (constant over zero rows), 0 before the first
-        int32_t Ec = 0;
-        const int nev = __popc(evmask);
-        if (chain_in && lane < nev) Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
-        for (int q = 0; evmask; ++q) {
-          const int i = __ffs(evmask) - 1;
-          evmask &= evmask - 1;
-          const int j = jb + 1 + i;
-          // ring lines around both ends (positions fixed by the previous row)
-          int2 L1[K], L2[K], L3[K], L4[K], G1[K], G2[K];
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const int so = k ? HC0 * 32 : 0;
-            L1[k] = ring[so + (((b[k] - 1) & hm[k]) << 5) + lane];
-            L2[k] = ring[so + (((b[k] - 2) & hm[k]) << 5) + lane];
-            L3[k] = ring[so + (((b[k] - 3) & hm[k]) << 5) + lane];
-            L4[k] = ring[so + (((b[k] - 4) & hm[k]) << 5) + lane];
-            G1[k] = ring[so + (((f[k] + 1) & hm[k]) << 5) + lane];
-            G2[k] = ring[so + (((f[k] + 2) & hm[k]) << 5) + lane];
-          }
-          // e_{m-1}(j-1): from the lane below (its value at the previous support row);
-          // lane 0 slot 0 from the previous pass (or e_0 = 0)
-          int32_t in[K];
-          const int32_t t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
-          int32_t ext = 0;
-          if (chain_in) ext = __shfl_sync(FULL, Ec, q);
-          in[0] = lane ? t0 : ext;
-          if constexpr (K == 2) {
-            const int32_t t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
-            in[1] = lane ? t1 : t0;
-          }
-          const int32_t Pj = __shfl_sync(FULL, Pc, i);
-          ++ev_e;
-          // ---- push line j: up to four back pops decided from the loaded lines -------------
-          int bj[K], top[K];
-          bool more[K];
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            bj[k] = in[k] + j * Pm1;
-            const int sz = b[k] - f[k];   // deque size - 1, before the push
-            const int p1 = (sz >= 1) & dom3(L1[k], B0[k], bj[k], j);
-            const int p2 = p1 & (sz >= 2) & dom3(L2[k], L1[k], bj[k], j);
-            const int p3 = p2 & (sz >= 3) & dom3(L3[k], L2[k], bj[k], j);
-            const int p4 = p3 & (sz >= 4) & dom3(L4[k], L3[k], bj[k], j);
-            top[k] = b[k] - (p1 + p2 + p3 + p4);   // position of the new second-to-back line
-            more[k] = act[k] & (p4 != 0);
-          }
-          bool anymore = more[0];
-          if constexpr (K == 2) anymore |= more[1];
-          if (__any_sync(FULL, anymore)) {   // rare: more than four pops
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              if (!more[k]) continue;
-              const int so = k ? HC0 * 32 : 0;
-              int2 cur = L4[k];
-              while (top[k] - f[k] >= 1) {
-                const int2 l1 = ring[so + (((top[k] - 1) & hm[k]) << 5) + lane];
-                if (dom3(l1, cur, bj[k], j)) {
-                  --top[k];
-                  cur = l1;
-                } else {
-                  break;
-                }
-              }
-            }
-          }
-          int2 F1[K], F2[K];
-          int v0[K], v1[K], v2[K];
-          bool q1[K], q2[K];
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const int so = k ? HC0 * 32 : 0;
-            const int nb = top[k] + 1;
-            pops_e += (unsigned)(b[k] + 1 - nb);
-            const int2 nl = make_int2(bj[k], j);
-            ring[so + ((nb & hm[k]) << 5) + lane] = nl;
-            const int d = nb - f[k];
-            F0[k] = d == 0 ? nl : F0[k];   // the deque was empty
-            F1[k] = d == 1 ? nl : G1[k];   // lines f+1 / f+2 popped or new
-            F2[k] = d == 2 ? nl : G2[k];
-            B0[k] = nl;
-            b[k] = nb;
-            ovf |= act[k] & (d > hm[k]);
-            // ---- query x = P_j: up to one front pop decided from the loaded lines -----------
-            v0[k] = F0[k].x - F0[k].y * Pj;
-            v1[k] = F1[k].x - F1[k].y * Pj;
-            v2[k] = F2[k].x - F2[k].y * Pj;
-            q1[k] = act[k] & (d >= 1) & (v1[k] < v0[k]);
-            q2[k] = q1[k] & (d >= 2) & (v2[k] < v1[k]);
-            const bool one = q1[k] & !q2[k];
-            f[k] += one;
-            F0[k] = one ? F1[k] : F0[k];
-            v0[k] = one ? v1[k] : v0[k];
-          }
-          bool anyq2 = q2[0];
-          if constexpr (K == 2) anyq2 |= q2[1];
-          if (__any_sync(FULL, anyq2)) {   // rare: the front moves by two or more
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              if (!q2[k]) continue;
-              const int so = k ? HC0 * 32 : 0;
-              f[k] += 2;
-              F0[k] = F2[k];
-              v0[k] = v2[k];
-              while (f[k] < b[k]) {
-                const int2 l1 = ring[so + (((f[k] + 1) & hm[k]) << 5) + lane];
-                const int vl = l1.x - l1.y * Pj;
-                if (vl < v0[k]) {
-                  ++f[k];
-                  F0[k] = l1;
-                  v0[k] = vl;
-                } else {
-                  break;
-                }
-              }
-            }
-          }
-          Pm1 = Pj;
-          // ---- row value, argmin change log -------------------------------------------------
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            eo[k] = v0[k];
-            const int nop = F0[k].y;
-            if (act[k] & (nop != op[k])) *lgp[k]++ = ((uint32_t)j << 16) | (uint32_t)nop;
-            op[k] = nop;
-          }
-          if (chain_out && lane == 31) eout_buf[evbase + q] = eo[K - 1];
-        }
-        evbase += nev;
-        if (__any_sync(FULL, ovf)) {
-          ovf = true;
-          break;
-        }
-      }
-      if (!ovf) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          if (!act[k]) continue;
-          const int mk = ps * L + 32 * k + lane + 1;
-          logn[ps * L + 32 * k + lane] =
-              (int)(lgp[k] - (logs + (size_t)(ps * L + 32 * k + lane) * (N + 1)));
-          const long long V = TN + (long long)eo[k];   // V_m = T_N + e_m(N)
-          if (p.cbb) p.cbb[(int64_t)e * (M + 1) + mk] = V;
-          if (mk == M) p.cost[e] = V;
-        }
-      }
-      __syncwarp();   // chained e-row and logs visible to the whole warp
     }
     pops += pops_e;
     events += ev_e;
@@ -489,12 +561,14 @@ int sp_hull_grid(int E, int N, int M, int wtype) {
 }
 
 size_t sp_hull_slot_bytes(int N, int M) { return sp::hull_slot_bytes(N, M); }
+size_t sp_hull_pool_bytes(int M) { return sp::hull_pool_bytes(M); }
 
 cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
                            int32_t* npos, int64_t* cost, int64_t* cbb, int32_t* fpos,
-                           int32_t* fn, uint8_t* ws, int32_t* fb, uint8_t* slots, int grid,
-                           cudaStream_t st) {
+                           int32_t* fn, uint8_t* ws, int32_t* fb, uint8_t* pool,
+                           uint8_t* slots, int grid, cudaStream_t st) {
   sp::HullParams p;
+  p.gring = reinterpret_cast<int2*>(pool);
   p.w = weights;
   p.E = E;
   p.N = N;

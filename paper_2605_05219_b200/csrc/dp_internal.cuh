@@ -9,11 +9,14 @@
 // internal counters, zeroed by the launch's header memset:
 #define SP_WS_FB_COUNT_OFF 192    // unsigned: entries handed from the hull kernel to the D&C
 #define SP_WS_ENTRY_CTR_OFF 200   // unsigned: next entry for the hull kernel's warps
+#define SP_WS_POOL_OFF 208        // uint64: occupancy mask of the hull kernel's overflow rings
 
-// Workspace after the head:  fallback list int32[E] | hull slots | D&C slots  (256-B aligned)
+// Workspace after the head:  fallback list int32[E] | overflow-ring pool | hull slots | D&C slots
+// (each 256-B aligned)
 int sp_hull_grid(int E, int N, int M, int wtype);
 size_t sp_hull_slot_bytes(int N, int M);
+size_t sp_hull_pool_bytes(int M);
 cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
                            int32_t* npos, int64_t* cost, int64_t* cbb, int32_t* fpos,
-                           int32_t* fn, uint8_t* ws, int32_t* fb, uint8_t* slots, int grid,
-                           cudaStream_t st);
+                           int32_t* fn, uint8_t* ws, int32_t* fb, uint8_t* pool,
+                           uint8_t* slots, int grid, cudaStream_t st);

@@ -96,22 +96,30 @@ def test_hull_sparse_ties_and_plateaus(dev):
 
 
 def test_hull_overflow_falls_back_exactly(dev):
-    """Uniform mass: layer-1 hull ~N/2 lines overflows the ring -> the D&C kernel solves the
-    entry; mixed in one batch with dense entries, an int64-range entry and a bad entry."""
+    """Uniform mass: the layer-1 hull holds ~N/2 lines.  At N = 3000 it outgrows the shared ring
+    but fits a global overflow ring (solved by the hull kernel on its retry); at N = 6000 it
+    outgrows that too and the D&C kernel solves the entry.  Mixed in one batch with dense
+    entries, an int64-range entry and a bad entry."""
     N, M = 3000, 40
     H = dense(8, N, seed=1).astype(np.int64)
-    H[2, 1:] = 1                              # ring overflow
-    H[5, 1:] = 3                              # ring overflow
-    H[6] *= 400000 // max(1, H[6].sum())       # 2 n N >= 2^31: int64 path
+    H[2, 1:] = 1                              # shared-ring overflow -> global ring
+    H[5, 1:] = 3                              # shared-ring overflow -> global ring
+    H[6] *= 400000 // max(1, H[6].sum())       # 2 n N >= 2^31: int64 path (D&C)
     assert H[6].sum() * N * 2 >= 2 ** 31
     r = place(H, M, dev, dtype=torch.int64)
-    assert r["stats"]["entries_hull"] == 5
+    assert r["stats"]["entries_hull"] == 7
     check(H, M, r)
     Hb = H.copy()
     Hb[3, 9] = -1
     r = place(Hb, M, dev, dtype=torch.int64)
     assert r["npos"][3] == -sp.SP_ERR_BAD_ARGUMENT
     check(Hb, M, r, rows=[0, 1, 2, 4, 5, 6, 7])
+    N = 20000
+    H = dense(3, N, seed=2)
+    H[1, 1:] = 1                              # may outgrow the global ring too -> D&C
+    r = place(H, 8, dev)
+    assert r["stats"]["entries_hull"] >= 2
+    check(H, 8, r)
 
 
 def test_hull_matches_dc_kernel_w5_rows(dev):

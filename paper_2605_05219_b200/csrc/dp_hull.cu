@@ -81,9 +81,7 @@ __host__ __device__ __forceinline__ size_t hull_cnt_bytes(int M) {
 __host__ __device__ __forceinline__ size_t hull_slot_bytes(int N, int M) {
   return hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(4 * (size_t)(N + 1));
 }
-__host__ __device__ __forceinline__ size_t hull_smem_bytes(int M) {
-  return (size_t)(hull_K(M) == 2 ? HC0 + HC1 : HC0) * 32 * 8;   // int2 (b, s) per line
-}
+__host__ __device__ __forceinline__ size_t hull_smem_bytes(int) { return 0; }   // static rings
 
 struct HullParams {
   const void* w;
@@ -122,26 +120,6 @@ __device__ __forceinline__ int pool_acquire(const HullParams& p) {
 __device__ __forceinline__ void pool_release(const HullParams& p, int g) {
   __threadfence();
   atomicAnd(reinterpret_cast<unsigned long long*>(p.ws + SP_WS_POOL_OFF), ~(1ull << g));
-}
-
-// back-pop test, int32 inputs exact (0 <= b <= nN < 2^30, so differences fit int32): the back
-// line (s2, b2) goes if it is not strictly below the segment (s1, b1) -> (j, bj), i.e.
-// (bj - b1)(s2 - s1) <= (b2 - b1)(j - s1).  Products < 2^46 in int64.
-__device__ __forceinline__ bool back_dominated(int db_new, int ds_old, int db_old, int ds_new) {
-  return (long long)db_new * ds_old <= (long long)db_old * ds_new;
-}
-__device__ __forceinline__ bool dom3(int2 a, int2 bk, int bj, int j) {   // (a, bk, new)
-  return back_dominated(bj - a.x, bk.y - a.y, bk.x - a.x, j - a.y);
-}
-
-// shared-memory ring access by explicit shared addresses (no generic-address conversion)
-__device__ __forceinline__ int2 lds2(uint32_t a) {
-  int2 v;
-  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
-  return v;
-}
-__device__ __forceinline__ void sts2(uint32_t a, int2 v) {
-  asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
 }
 
 // log slot of layer m (1-based), lane-major within a pass: [pass][slot k][lane]
@@ -183,219 +161,253 @@ __device__ __forceinline__ int log_lookup_lane(const uint32_t* lg, int cnt, int 
   return (int)(__ldcg(lg + lo) & 0xffffu);
 }
 
-// a4 for one entry: all layers in lockstep, one support row per step.  The rings live at rg
-// (shared memory, or a global overflow ring when GR) with slot-1 offset so1 and position masks hm.
-// Returns true when a ring overflowed (the entry's results are then invalid).
-template <typename WT, int K, bool GR>
+// Ring storage policies: slot k's ring has C_k positions of 32 lines (256 B), [slot][pos][lane].
+// SRing addresses a shared array (LDS/STS with compile-time masks); GRing a global overflow ring.
+template <int C0, int C1>
+struct SRing {
+  int2* base;   // the kernel's __shared__ ring array
+  __device__ __forceinline__ int idx(int k, int pos) const {
+    return (k ? C0 * 32 : 0) + ((pos & ((k ? C1 : C0) - 1)) << 5) + lane_id();
+  }
+  __device__ __forceinline__ int2 ld(int k, int pos) const { return base[idx(k, pos)]; }
+  __device__ __forceinline__ void st(int k, int pos, int2 v) const { base[idx(k, pos)] = v; }
+  static constexpr int cap(int k) { return k ? C1 : C0; }
+};
+template <int C>
+struct GRing {
+  int2* base;   // one ring of the global pool
+  __device__ __forceinline__ int idx(int k, int pos) const {
+    return k * C * 32 + ((pos & (C - 1)) << 5) + lane_id();
+  }
+  __device__ __forceinline__ int2 ld(int k, int pos) const { return base[idx(k, pos)]; }
+  __device__ __forceinline__ void st(int k, int pos, int2 v) const { base[idx(k, pos)] = v; }
+  static constexpr int cap(int) { return C; }
+};
+
+// back-pop test with the new point (j, bj) as origin: for the pair (A, Bk) of consecutive hull
+// lines (A below Bk), with A' = A - new and Bk' = Bk - new in (s, b) coordinates, Bk goes iff it is
+// not strictly below the segment A -> new, i.e. cross(A', Bk') = A'.s Bk'.b - A'.b Bk'.s <= 0.
+// |b'| < 2^30, |s'| < 2^16: products < 2^46 in int64, exact.
+__device__ __forceinline__ bool pop_test(int as, int ab, int ks, int kb) {
+  return (long long)as * kb <= (long long)ab * ks;
+}
+
+// a4 for one entry: all layers in lockstep, one support row per step.  Returns true when a ring
+// overflowed (the entry's results are then invalid).
+template <typename WT, int K, class RING>
 __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
-                                        long long TN, int n32, int2* __restrict__ rg, int so1,
-                                        const int (&hm)[K], uint32_t* logs, int32_t* logn,
-                                        int32_t* ebuf0, int32_t* ebuf1, unsigned& pops_e,
-                                        unsigned& ev_e) {
+                                        long long TN, int n32, const RING rg, uint32_t* logs,
+                                        int32_t* logn, int32_t* ebuf0, int32_t* ebuf1,
+                                        unsigned& pops_e, unsigned& ev_e) {
   const int lane = lane_id();
   const int N = p.N, M = p.M;
   constexpr int L = 32 * K;
   const int passes = (M + L - 1) / L;
-    // ---- a4: all layers in lockstep, one row per step ---------------------------------------
-    bool ovf = false;
-    for (int ps = 0; ps < passes && !ovf; ++ps) {
-      const int32_t* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
-      int32_t* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
-      const bool chain_in = ps > 0, chain_out = ps + 1 < passes;
-      // Per slot: deque [f, b] (monotone counters; ring position & hm).  In registers: the back
-      // line B0 (the last one pushed) and the front line F0; the four lines below the back and
-      // the two above the front are loaded from the ring at the top of every support row (their
-      // positions are known a row ahead, so the loads overlap the shuffle).  A line is int2
-      // (x = intercept b_s, y = s).  eo = e_m(j) (the running row value), op = opt_m(j).
-      int f[K], b[K], eo[K], op[K];
-      int2 B0[K], F0[K];
-      bool act[K];
-      uint32_t* lgp[K];
+  bool ovf = false;
+  for (int ps = 0; ps < passes && !ovf; ++ps) {
+    const int32_t* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
+    int32_t* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
+    const bool chain_in = ps > 0, chain_out = ps + 1 < passes;
+    // Per slot: deque [f, b] (monotone counters; ring position = counter mod capacity).  In
+    // registers: the back line B0 (the last one pushed) and the front line F0; the four lines
+    // below the back and the two above the front are loaded from the ring at the top of every
+    // support row (positions known a row ahead, so the loads overlap the shuffle).  A line is
+    // int2 (x = intercept b_s, y = s).  eo = e_m(j) (the running row value), op = opt_m(j).
+    int f[K], b[K], eo[K], op[K], cnt[K];
+    int2 B0[K], F0[K];
+    bool act[K];
+    uint32_t* lg[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int mk = ps * L + 32 * k + lane + 1;
-        act[k] = mk <= M;
-        f[k] = 0;
-        b[k] = -1;
-        eo[k] = 0;   // e_m(0) = 0 (reading R1)
-        op[k] = 1;   // opt_m(1) = 1 whatever the row type: logged up front
-        lgp[k] = logs + (size_t)(ps * L + 32 * k + lane) * (N + 1);
-        if (act[k]) *lgp[k]++ = (1u << 16) | 1u;
-        B0[k] = F0[k] = make_int2(0, 1);
+    for (int k = 0; k < K; ++k) {
+      const int mk = ps * L + 32 * k + lane + 1;
+      act[k] = mk <= M;
+      f[k] = 0;
+      b[k] = -1;
+      eo[k] = 0;   // e_m(0) = 0 (reading R1)
+      op[k] = 1;   // opt_m(1) = 1 whatever the row type: logged up front
+      cnt[k] = 1;
+      lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * (N + 1);
+      if (act[k]) lg[k][0] = (1u << 16) | 1u;
+      B0[k] = F0[k] = make_int2(0, 1);
+    }
+    int32_t carry = 0, Pm1 = 0;
+    int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
+    for (int jb = 0; jb < N; jb += 32) {
+      const int jr = jb + 1 + lane;
+      const int32_t craw = jr <= N ? (int32_t)we[jr] : 0;
+      unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
+      if (evmask == 0) continue;                          // 32 zero rows: nothing changes
+      int32_t cnt32 = craw;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(FULL, cnt32, o);
+        if (lane >= o) cnt32 += y;
       }
-      int32_t carry = 0, Pm1 = 0;
-      int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
-      for (int jb = 0; jb < N; jb += 32) {
-        const int jr = jb + 1 + lane;
-        const int32_t craw = jr <= N ? (int32_t)we[jr] : 0;
-        unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
-        if (evmask == 0) continue;                          // 32 zero rows: nothing changes
-        int32_t cnt32 = craw;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int32_t y = __shfl_up_sync(FULL, cnt32, o);
-          if (lane >= o) cnt32 += y;
-        }
-        const int32_t Pc = carry + cnt32;
-        carry = __shfl_sync(FULL, Pc, 31);
-        // previous pass's top layer at the support rows: e(j-1) of support row number t is its
-        // value at support row t-1 (constant over zero rows), 0 before the first
-        int32_t Ec = 0;
-        const int nev = __popc(evmask);
-        if (chain_in && lane < nev) Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
-        for (int q = 0; evmask; ++q) {
-          const int i = __ffs(evmask) - 1;
-          evmask &= evmask - 1;
-          const int j = jb + 1 + i;
-          // ring lines around both ends (positions fixed by the previous row)
-          int2 L1[K], L2[K], L3[K], L4[K], G1[K], G2[K];
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const int so = k ? so1 : 0;
-            L1[k] = rg[so + (((b[k] - 1) & hm[k]) << 5) + lane];
-            L2[k] = rg[so + (((b[k] - 2) & hm[k]) << 5) + lane];
-            L3[k] = rg[so + (((b[k] - 3) & hm[k]) << 5) + lane];
-            L4[k] = rg[so + (((b[k] - 4) & hm[k]) << 5) + lane];
-            G1[k] = rg[so + (((f[k] + 1) & hm[k]) << 5) + lane];
-            G2[k] = rg[so + (((f[k] + 2) & hm[k]) << 5) + lane];
-          }
-          // e_{m-1}(j-1): from the lane below (its value at the previous support row);
-          // lane 0 slot 0 from the previous pass (or e_0 = 0)
-          int32_t in[K];
-          const int32_t t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
-          int32_t ext = 0;
-          if (chain_in) ext = __shfl_sync(FULL, Ec, q);
-          in[0] = lane ? t0 : ext;
-          if constexpr (K == 2) {
-            const int32_t t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
-            in[1] = lane ? t1 : t0;
-          }
-          const int32_t Pj = __shfl_sync(FULL, Pc, i);
-          ++ev_e;
-          // ---- push line j: up to four back pops decided from the loaded lines -------------
-          int bj[K], top[K];
-          bool more[K], skip[K];
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            bj[k] = in[k] + j * Pm1;
-            // a line that overtakes the back line only beyond x = P_N = n is never optimal at
-            // any query (x <= n): it is neither pushed nor allowed to pop
-            skip[k] = (b[k] >= f[k]) & (bj[k] - B0[k].x > n32 * (j - B0[k].y));
-            const int sz = skip[k] ? 0 : b[k] - f[k];   // deque size - 1, before the push
-            const int p1 = (sz >= 1) & dom3(L1[k], B0[k], bj[k], j);
-            const int p2 = p1 & (sz >= 2) & dom3(L2[k], L1[k], bj[k], j);
-            const int p3 = p2 & (sz >= 3) & dom3(L3[k], L2[k], bj[k], j);
-            const int p4 = p3 & (sz >= 4) & dom3(L4[k], L3[k], bj[k], j);
-            top[k] = b[k] - (p1 + p2 + p3 + p4);   // position of the new second-to-back line
-            more[k] = act[k] & (p4 != 0);
-          }
-          bool anymore = more[0];
-          if constexpr (K == 2) anymore |= more[1];
-          if (__any_sync(FULL, anymore)) {   // rare: more than four pops
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              if (!more[k]) continue;
-              const int so = k ? so1 : 0;
-              int2 cur = L4[k];
-              while (top[k] - f[k] >= 1) {
-                const int2 l1 = rg[so + (((top[k] - 1) & hm[k]) << 5) + lane];
-                if (dom3(l1, cur, bj[k], j)) {
-                  --top[k];
-                  cur = l1;
-                } else {
-                  break;
-                }
-              }
-            }
-          }
-          int2 F1[K], F2[K];
-          int v0[K], v1[K], v2[K];
-          bool q1[K], q2[K];
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            const int so = k ? so1 : 0;
-            const int nb = skip[k] ? b[k] : top[k] + 1;
-            pops_e += (unsigned)(b[k] - top[k]);
-            const int2 nl = skip[k] ? B0[k] : make_int2(bj[k], j);
-            if (!skip[k]) rg[so + ((nb & hm[k]) << 5) + lane] = nl;
-            const int d = nb - f[k];
-            F0[k] = (!skip[k] & (d == 0)) ? nl : F0[k];   // the deque was empty
-            F1[k] = (!skip[k] & (d == 1)) ? nl : G1[k];   // lines f+1 / f+2 popped or new
-            F2[k] = (!skip[k] & (d == 2)) ? nl : G2[k];
-            B0[k] = nl;
-            b[k] = nb;
-            ovf |= act[k] & (d > hm[k]);
-            // ---- query x = P_j: up to one front pop decided from the loaded lines -----------
-            v0[k] = F0[k].x - F0[k].y * Pj;
-            v1[k] = F1[k].x - F1[k].y * Pj;
-            v2[k] = F2[k].x - F2[k].y * Pj;
-            q1[k] = act[k] & (d >= 1) & (v1[k] < v0[k]);
-            q2[k] = q1[k] & (d >= 2) & (v2[k] < v1[k]);
-            const bool one = q1[k] & !q2[k];
-            f[k] += one;
-            F0[k] = one ? F1[k] : F0[k];
-            v0[k] = one ? v1[k] : v0[k];
-          }
-          bool anyq2 = q2[0];
-          if constexpr (K == 2) anyq2 |= q2[1];
-          if (__any_sync(FULL, anyq2)) {   // rare: the front moves by two or more
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-              if (!q2[k]) continue;
-              const int so = k ? so1 : 0;
-              f[k] += 2;
-              F0[k] = F2[k];
-              v0[k] = v2[k];
-              while (f[k] < b[k]) {
-                const int2 l1 = rg[so + (((f[k] + 1) & hm[k]) << 5) + lane];
-                const int vl = l1.x - l1.y * Pj;
-                if (vl < v0[k]) {
-                  ++f[k];
-                  F0[k] = l1;
-                  v0[k] = vl;
-                } else {
-                  break;
-                }
-              }
-            }
-          }
-          Pm1 = Pj;
-          // ---- row value, argmin change log -------------------------------------------------
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            eo[k] = v0[k];
-            const int nop = F0[k].y;
-            if (act[k] & (nop != op[k])) *lgp[k]++ = ((uint32_t)j << 16) | (uint32_t)nop;
-            op[k] = nop;
-          }
-          if (chain_out && lane == 31) eout_buf[evbase + q] = eo[K - 1];
-        }
-        evbase += nev;
-        if (__any_sync(FULL, ovf)) {
-          ovf = true;
-          break;
-        }
-      }
-      if (!ovf) {
+      const int32_t Pc = carry + cnt32;
+      carry = __shfl_sync(FULL, Pc, 31);
+      // previous pass's top layer at the support rows: e(j-1) of support row number t is its
+      // value at support row t-1 (constant over zero rows), 0 before the first
+      int32_t Ec = 0;
+      const int nev = __popc(evmask);
+      if (chain_in && lane < nev) Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
+      for (int q = 0; evmask; ++q) {
+        const int i = __ffs(evmask) - 1;
+        evmask &= evmask - 1;
+        const int j = jb + 1 + i;
+        // ring lines around both ends (positions fixed by the previous row)
+        int2 L1[K], L2[K], L3[K], L4[K], G1[K], G2[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          if (!act[k]) continue;
-          const int mk = ps * L + 32 * k + lane + 1;
-          logn[ps * L + 32 * k + lane] =
-              (int)(lgp[k] - (logs + (size_t)(ps * L + 32 * k + lane) * (N + 1)));
-          const long long V = TN + (long long)eo[k];   // V_m = T_N + e_m(N)
-          if (p.cbb) p.cbb[(int64_t)e * (M + 1) + mk] = V;
-          if (mk == M) p.cost[e] = V;
+          L1[k] = rg.ld(k, b[k] - 1);
+          L2[k] = rg.ld(k, b[k] - 2);
+          L3[k] = rg.ld(k, b[k] - 3);
+          L4[k] = rg.ld(k, b[k] - 4);
+          G1[k] = rg.ld(k, f[k] + 1);
+          G2[k] = rg.ld(k, f[k] + 2);
         }
+        // e_{m-1}(j-1): from the lane below (its value at the previous support row);
+        // lane 0 slot 0 from the previous pass (or e_0 = 0)
+        int32_t in[K];
+        const int32_t t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
+        int32_t ext = 0;
+        if (chain_in) ext = __shfl_sync(FULL, Ec, q);
+        in[0] = lane ? t0 : ext;
+        if constexpr (K == 2) {
+          const int32_t t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
+          in[1] = lane ? t1 : t0;
+        }
+        const int32_t Pj = __shfl_sync(FULL, Pc, i);
+        ++ev_e;
+        // ---- push line j: up to four back pops decided from the loaded lines ---------------
+        int bj[K], top[K];
+        bool more[K], skip[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          bj[k] = in[k] + j * Pm1;
+          // deltas of the back lines from the new point (j, bj)
+          const int s0 = B0[k].y - j, c0 = B0[k].x - bj[k];
+          const int s1 = L1[k].y - j, c1 = L1[k].x - bj[k];
+          const int s2 = L2[k].y - j, c2 = L2[k].x - bj[k];
+          const int s3 = L3[k].y - j, c3 = L3[k].x - bj[k];
+          const int s4 = L4[k].y - j, c4 = L4[k].x - bj[k];
+          // a line that overtakes the back line only beyond x = P_N = n is never optimal at a
+          // query (x <= n): it is neither pushed nor allowed to pop.
+          // x(back, new) > n  <=>  bj - B0.b > n (j - B0.s)  <=>  -c0 > -n s0
+          skip[k] = (b[k] >= f[k]) & (c0 < n32 * s0);
+          const int sz = skip[k] ? 0 : b[k] - f[k];   // deque size - 1, before the push
+          const int p1 = (sz >= 1) & pop_test(s1, c1, s0, c0);
+          const int p2 = p1 & (sz >= 2) & pop_test(s2, c2, s1, c1);
+          const int p3 = p2 & (sz >= 3) & pop_test(s3, c3, s2, c2);
+          const int p4 = p3 & (sz >= 4) & pop_test(s4, c4, s3, c3);
+          top[k] = b[k] - (p1 + p2 + p3 + p4);   // position of the new second-to-back line
+          more[k] = act[k] & (p4 != 0);
+        }
+        bool anymore = more[0];
+        if constexpr (K == 2) anymore |= more[1];
+        if (__any_sync(FULL, anymore)) {   // rare: more than four pops
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (!more[k]) continue;
+            int cs = L4[k].y - j, cb = L4[k].x - bj[k];
+            while (top[k] - f[k] >= 1) {
+              const int2 l1 = rg.ld(k, top[k] - 1);
+              const int ls = l1.y - j, lb = l1.x - bj[k];
+              if (pop_test(ls, lb, cs, cb)) {
+                --top[k];
+                cs = ls;
+                cb = lb;
+              } else {
+                break;
+              }
+            }
+          }
+        }
+        int v0[K], v1[K], v2[K];
+        bool q2[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int nb = skip[k] ? b[k] : top[k] + 1;
+          pops_e += (unsigned)(b[k] - top[k]);
+          const int2 nl = make_int2(bj[k], j);
+          if (!skip[k]) rg.st(k, nb, nl);
+          const int d = nb - f[k];
+          const bool fresh = !skip[k];
+          const int2 F1 = (fresh & (d == 1)) ? nl : G1[k];   // lines f+1 / f+2 popped or new
+          const int2 F2 = (fresh & (d == 2)) ? nl : G2[k];
+          F0[k] = (fresh & (d == 0)) ? nl : F0[k];         // the deque was empty
+          B0[k] = skip[k] ? B0[k] : nl;
+          b[k] = nb;
+          ovf |= act[k] & (d >= RING::cap(k));
+          // ---- query x = P_j: up to one front pop decided from the loaded lines -------------
+          v0[k] = F0[k].x - F0[k].y * Pj;
+          v1[k] = F1.x - F1.y * Pj;
+          v2[k] = F2.x - F2.y * Pj;
+          const bool q1 = act[k] & (d >= 1) & (v1[k] < v0[k]);
+          q2[k] = q1 & (d >= 2) & (v2[k] < v1[k]);
+          const bool one = q1 & !q2[k];
+          f[k] += one;
+          F0[k] = one ? F1 : (q2[k] ? F2 : F0[k]);
+          v0[k] = one ? v1[k] : (q2[k] ? v2[k] : v0[k]);
+        }
+        bool anyq2 = q2[0];
+        if constexpr (K == 2) anyq2 |= q2[1];
+        if (__any_sync(FULL, anyq2)) {   // rare: the front moves by two or more
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (!q2[k]) continue;
+            f[k] += 2;   // F0 = line f+2 already
+            while (f[k] < b[k]) {
+              const int2 l1 = rg.ld(k, f[k] + 1);
+              const int vl = l1.x - l1.y * Pj;
+              if (vl < v0[k]) {
+                ++f[k];
+                F0[k] = l1;
+                v0[k] = vl;
+              } else {
+                break;
+              }
+            }
+          }
+        }
+        Pm1 = Pj;
+        // ---- row value, argmin change log ---------------------------------------------------
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          eo[k] = v0[k];
+          const int nop = F0[k].y;
+          if (act[k] & (nop != op[k])) {
+            lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop;
+            ++cnt[k];
+          }
+          op[k] = nop;
+        }
+        if (chain_out && lane == 31) eout_buf[evbase + q] = eo[K - 1];
       }
-      __syncwarp();   // chained e-row and logs visible to the whole warp
+      evbase += nev;
+      if (__any_sync(FULL, ovf)) {
+        ovf = true;
+        break;
+      }
     }
+    if (!ovf) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (!act[k]) continue;
+        const int mk = ps * L + 32 * k + lane + 1;
+        logn[ps * L + 32 * k + lane] = cnt[k];
+        const long long V = TN + (long long)eo[k];   // V_m = T_N + e_m(N)
+        if (p.cbb) p.cbb[(int64_t)e * (M + 1) + mk] = V;
+        if (mk == M) p.cost[e] = V;
+      }
+    }
+    __syncwarp();   // chained e-row and logs visible to the whole warp
+  }
   return ovf;
 }
 
 template <typename WT, int K>
 __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
-  extern __shared__ __align__(16) int2 ring[];   // slot rings [HC0][32] | [HC1][32] lines (b, s)
+  __shared__ __align__(16) int2 sring[(K == 2 ? HC0 + HC1 : HC0) * 32];   // [slot][pos][lane]
   const int lane = threadIdx.x;
   const int N = p.N, M = p.M;
   constexpr int L = 32 * K;
@@ -408,10 +420,6 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
   int32_t* ebuf0 = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M) + hull_cnt_bytes(M));
   int32_t* ebuf1 = ebuf0 + hull_align(4 * (size_t)(N + 1)) / 4;
-  // ring of slot 0: [HC0][32] lines, then slot 1: [HC1][32] lines (256 B per position)
-  int hm[K];
-  hm[0] = HC0 - 1;
-  if constexpr (K == 2) hm[1] = HC1 - 1;
   unsigned long long pops = 0, events = 0;
   int done_entries = 0;
 
@@ -454,20 +462,17 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
 #ifdef SP_HULL_FORCE_GLOBAL   // experiment: every entry on a global ring
     bool ovf = true;
 #else
-    bool ovf = hull_dp<WT, K, false>(p, we, e, TN, n32, ring, HC0 * 32, hm, logs, logn, ebuf0,
-                                     ebuf1, pops_e, ev_e);
+    bool ovf = hull_dp<WT, K>(p, we, e, TN, n32, SRing<HC0, HC1>{sring}, logs, logn, ebuf0, ebuf1,
+                              pops_e, ev_e);
 #endif
     if (ovf) {   // retry with a global overflow ring from the pool (rare)
       int g = -1;
       if (lane == 0) g = pool_acquire(p);
       g = __shfl_sync(FULL, g, 0);
       if (g >= 0) {
-        int hg[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) hg[k] = HCG - 1;
         pops_e = ev_e = 0;
-        ovf = hull_dp<WT, K, true>(p, we, e, TN, n32, p.gring + (size_t)g * K * HCG * 32,
-                                   HCG * 32, hg, logs, logn, ebuf0, ebuf1, pops_e, ev_e);
+        ovf = hull_dp<WT, K>(p, we, e, TN, n32, GRing<HCG>{p.gring + (size_t)g * K * HCG * 32},
+                             logs, logn, ebuf0, ebuf1, pops_e, ev_e);
         __syncwarp();
         if (lane == 0) pool_release(p, g);
       }

@@ -58,8 +58,15 @@ constexpr int HC0 = SP_HULL_CAP0, HC1 = SP_HULL_CAP1;
 // overflow ring of HCG lines per layer, taken from a pool of HPOOL rings (a 64-bit occupancy mask
 // in the workspace head); only if that overflows too (or the pool is busy) does it go to the
 // divide-and-conquer kernel.
-constexpr int HCG = 2048;
-constexpr int HPOOL = 32;
+#ifndef SP_HULL_HCG
+#define SP_HULL_HCG 2048
+#endif
+#ifndef SP_HULL_POOL
+#define SP_HULL_POOL 32
+#endif
+constexpr int HCG = SP_HULL_HCG;
+constexpr int HPOOL = SP_HULL_POOL;
+static_assert(HPOOL >= 1 && HPOOL <= 64, "the pool's occupancy mask is one 64-bit word");
 static_assert((HC0 & (HC0 - 1)) == 0 && (HC1 & (HC1 - 1)) == 0, "ring capacities: powers of two");
 
 __host__ __device__ __forceinline__ size_t hull_align(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -459,7 +466,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
 
     // ---- a4: all layers in lockstep, one support row per step --------------------------------
     unsigned pops_e = 0, ev_e = 0;
-#ifdef SP_HULL_FORCE_GLOBAL   // experiment: every entry on a global ring
+#ifdef SP_HULL_FORCE_GLOBAL   // experiment: every entry through the global-ring retry
     bool ovf = true;
 #else
     bool ovf = hull_dp<WT, K>(p, we, e, TN, n32, SRing<HC0, HC1>{sring}, logs, logn, ebuf0, ebuf1,

@@ -153,3 +153,19 @@ def test_hull_frontier(dev):
             assert r["fn"][e, m - 1] == k
             assert r["fpos"][e, m - 1, :k].tolist() == rp.tolist()
             assert (r["fpos"][e, m - 1, k:] == 0).all()
+
+
+def test_hull_vs_dc_every_w5_entry(dev):
+    """All 16384 W5 entries (the bench launch): hull kernel (incl. its global-ring retries) vs the
+    divide-and-conquer kernel alone (SP_NO_HULL) -- identical positions, counts and V_0..V_M."""
+    cfg = wl.CONFIGS["W5"]
+    H = wl.make_dense_hist(cfg, seed=0, device=dev)
+    a = sp.place_checkpoints(H, cfg.M, cost_by_budget=True)
+    os.environ["SP_NO_HULL"] = "1"
+    try:
+        b = sp.place_checkpoints(H, cfg.M, cost_by_budget=True)
+    finally:
+        del os.environ["SP_NO_HULL"]
+    torch.cuda.synchronize()
+    for x, y, name in zip(a, b, ("pos", "npos", "cost", "cbb")):
+        assert torch.equal(x, y), name

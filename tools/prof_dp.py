@@ -16,11 +16,14 @@ ap.add_argument("--workload", default="W5")
 ap.add_argument("--M", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--lcp", action="store_true")
+ap.add_argument("--plus1", action="store_true", help="add 1 to every bin (full support, K = N)")
 a = ap.parse_args()
 cfg = wl.scaled(wl.CONFIGS[a.workload], a.entries)
 M = a.M or cfg.M
 dev = torch.device("cuda:0")
 H = wl.make_dense_hist(cfg, seed=0, device=dev) if cfg.dense_n else wl.uniform_hist(a.entries, cfg.N, dev)
+if a.plus1:
+    H[:, 1:] += 1
 ws = torch.empty(sp.place_checkpoints_workspace_bytes(a.entries, cfg.N, M), dtype=torch.uint8, device=dev)
 for r in range(a.reps):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -32,7 +32,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc (-O2, no fast-math)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-pthread",
-                               "-o", _LIB, _SRC])
+                               "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 
@@ -62,6 +62,9 @@ def lib():
         L.or_clip_to_blocks.argtypes = [_i32p, _c_i32, _c_i32, _i32p]
         L.or_sqrt_positions.argtypes = [_c_i32, _i32p]
         L.or_log_positions.argtypes = [_c_i32, _c_i32, _i32p]
+        L.or_gamma_hist.argtypes = [_i32p, _c_i64, _c_i32, ctypes.c_double, _f64p]
+        L.or_gamma_variance_term.argtypes = [ctypes.c_double, _c_i64, _c_i32]
+        L.or_gamma_variance_term.restype = ctypes.c_double
         L.or_place_batch.argtypes = [_i32p, _c_i32, _c_i32, _c_i32, _c_int, _i32p, _i32p, _i64p,
                                      _vp, _c_int]
         L.or_eval_batch.argtypes = [_i32p, _c_i32, _c_i32, _i32p, _i32p, _c_i32, _c_i32, _c_int,
@@ -257,3 +260,16 @@ def log_positions(N, M):
     if k < 0:
         raise ValueError("log_positions: bad N/M")
     return out[:k].copy()
+
+
+def gamma_hist(depths, N, gamma):
+    """f2: Thm 4's exponentially weighted histogram of the depth stream (definition)."""
+    d = np.ascontiguousarray(depths, dtype=np.int32)
+    p = np.zeros(N + 1, np.float64)
+    _check(lib().or_gamma_hist(d if d.size else np.zeros(1, np.int32), d.size, N, gamma, p),
+           "or_gamma_hist")
+    return p
+
+
+def gamma_variance_term(gamma, t, N):
+    return lib().or_gamma_variance_term(gamma, t, N)

@@ -9,6 +9,7 @@
  */
 #include "sp_oracle.h"
 
+#include <math.h>
 #include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
@@ -499,4 +500,34 @@ int or_eval_batch(const int32_t* hist, int32_t n_entries, int32_t N, const int32
                 cost, worst, 0, 0};
   if (run_threads(eval_worker, &J, nthreads)) return -3;
   return J.err;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* f2: the exponentially weighted empirical histogram of Thm 4, written out as its */
+/* definition: p_t = (1 - g) / (1 - g^t) * sum_{s=1..t} g^(t-s) e_{T_s}, 0 < g < 1, and the   */
+/* plain empirical distribution (1/t) sum_s e_{T_s} for g = 1 (Thm 3's estimator).  Depths are */
+/* clamped to [0, N] (S:327 design decision; bin 0 = miss).  O(t) per call, long double.      */
+/* ------------------------------------------------------------------------------------------ */
+int or_gamma_hist(const int32_t* depths, int64_t t, int32_t N, double gamma, double* p) {
+  if (N < 1 || t < 1 || !(gamma > 0.0 && gamma <= 1.0)) return -1;
+  long double* acc = (long double*)calloc((size_t)N + 1, sizeof(long double));
+  if (!acc) return -3;
+  for (int64_t s = 1; s <= t; ++s) {
+    int32_t d = depths[s - 1];
+    if (d < 0) d = 0;
+    if (d > N) d = N;
+    acc[d] += powl((long double)gamma, (long double)(t - s));   /* gamma^(t-s) e_{T_s} */
+  }
+  long double norm;
+  if (gamma == 1.0) norm = 1.0L / (long double)t;
+  else norm = (1.0L - (long double)gamma) / (1.0L - powl((long double)gamma, (long double)t));
+  for (int32_t d = 0; d <= N; ++d) p[d] = (double)(acc[d] * norm);
+  free(acc);
+  return 0;
+}
+
+/* Thm 4's variance term sqrt(N (1-g)/(1+g) (1+g^t)/(1-g^t)), closed form. */
+double or_gamma_variance_term(double gamma, int64_t t, int32_t N) {
+  const long double g = gamma, gt = powl(g, (long double)t);
+  return (double)sqrtl((long double)N * (1.0L - g) / (1.0L + g) * (1.0L + gt) / (1.0L - gt));
 }

@@ -92,6 +92,13 @@ int or_eval_batch(const int32_t* hist, int32_t n_entries, int32_t N, const int32
                   const int32_t* n_positions, int32_t n_sets, int32_t max_pos, int broadcast,
                   int64_t* cost, int32_t* worst, int nthreads);
 
+/* f2: Thm 4's exponentially weighted empirical histogram, definitional O(t N):
+ * p[d] = (1-g)/(1-g^t) sum_{s<=t} g^(t-s) [T_s = d]  (g = 1: empirical frequencies).
+ * depths[t] in arrival order, clamped to [0, N]; p[N+1] normalised (sums to 1). */
+int or_gamma_hist(const int32_t* depths, int64_t t, int32_t N, double gamma, double* p);
+/* Thm 4's variance term sqrt(N (1-g)/(1+g) (1+g^t)/(1-g^t)). */
+double or_gamma_variance_term(double gamma, int64_t t, int32_t N);
+
 #ifdef __cplusplus
 }
 #endif

@@ -192,6 +192,30 @@ sp_status sp_clip_to_blocks(const int32_t* positions /*[E][max_pos]*/,
                             int32_t max_pos, int32_t B, int32_t* out_positions /*[E][max_pos]*/,
                             int32_t* out_n /*[E]*/, sp_stream_t stream);
 
+/* ------------------------------------------------------------------------------------------
+ * f2 -- Thm 4's exponentially weighted empirical overlap histogram, batched over
+ * entries; the estimator the paper re-solves the placement from (g = 0.99):
+ *   p_t = (1 - g) / (1 - g^t) sum_{s=1..t} g^(t-s) e_{T_s}      (g = 1: the empirical law, Thm 3)
+ * State per entry e (device, caller-owned, zero-initialised for a fresh estimator):
+ *   W     double [E][N+1]  weights relative to the epoch tau: decayed weights w = W g^(t - tau)
+ *   t     int64  [E]       observations so far;   tau  int64 [E]   reference epoch
+ * sp_gamma_observe appends one batch of observations GROUPED BY ENTRY, in arrival order within
+ * each entry: obs_off int64 [E+1] (CSR offsets), depth int32 [obs_off[E]] (e.g. sp_overlap_hist's
+ * lcp_out); depths are clamped to [0, N] (bin 0 = miss).  Each observation adds g^-(t+1-tau) to
+ * W[e][depth]; the row is rescaled (tau = t) before exponents pass 2^64.  fp64 atomics: the
+ * summation order (not the value) of equal-depth observations in one batch is unspecified.
+ * W can be handed to sp_place_checkpoints (SP_W_PROB_F64) directly: it differs from p_t by a
+ * positive per-entry factor, and the placement is scale-invariant.
+ * sp_gamma_snapshot writes p_t (double [E][N+1], sums to 1; all zero when t = 0).
+ * Errors: BAD_LENGTH (N < 1, N > SP_MAX_N, E < 0), BAD_ARGUMENT (g outside (0, 1], NULL), CUDA.
+ * ---------------------------------------------------------------------------------------- */
+sp_status sp_gamma_observe(double* W, int64_t* t, int64_t* tau, const int64_t* obs_off,
+                           const int32_t* depth, int32_t n_entries, int32_t N, double gamma,
+                           sp_stream_t stream);
+sp_status sp_gamma_snapshot(const double* W, const int64_t* t, const int64_t* tau,
+                            int32_t n_entries, int32_t N, double gamma, double* p_out,
+                            sp_stream_t stream);
+
 /* Host-side helpers for the Table 1 baselines.  out_host must hold M (resp.
  * floor(N/B)) ints.  Return the number of positions written, or a negative sp_status. */
 int32_t sp_balanced_positions(int32_t N, int32_t M, int32_t* out_host);

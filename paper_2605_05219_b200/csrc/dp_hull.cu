@@ -417,8 +417,6 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   __shared__ __align__(16) int2 sring[(K == 2 ? HC0 + HC1 : HC0) * 32];   // [slot][pos][lane]
   const int lane = threadIdx.x;
   const int N = p.N, M = p.M;
-  constexpr int L = 32 * K;
-  const int passes = (M + L - 1) / L;
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
   unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
   unsigned* ectr = reinterpret_cast<unsigned*>(p.ws + SP_WS_ENTRY_CTR_OFF);

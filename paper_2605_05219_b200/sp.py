@@ -54,6 +54,9 @@ SYMBOLS = {
     "sp_log_positions": (_i32, [_i32, _i32, _vp]),
     "sp_balanced_positions": (_i32, [_i32, _i32, _vp]),
     "sp_block_positions": (_i32, [_i32, _i32, _vp]),
+    "sp_gamma_observe": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, ctypes.c_double,
+                                        _vp]),
+    "sp_gamma_snapshot": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, ctypes.c_double, _vp, _vp]),
     "sp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sp_last_error_string": (ctypes.c_char_p, []),
     "sp_version": (ctypes.c_char_p, []),
@@ -337,3 +340,44 @@ def baseline_sets(N, budgets=(), blocks=(), device="cuda"):
             pos[i, :len(s)] = torch.tensor(s, dtype=torch.int32)
     npos = torch.tensor([len(s) for s in sets], dtype=torch.int32)
     return pos.to(device), npos.to(device), labels
+
+
+# ---------------------------------------------------------------------------------------------
+# f2: Thm 4's exponentially weighted histogram
+# ---------------------------------------------------------------------------------------------
+class GammaEstimator:
+    """Device state of E per-entry estimators (W [E][N+1] f64, t [E], tau [E] int64)."""
+
+    def __init__(self, n_entries, N, gamma=0.99, device="cuda"):
+        self.N, self.gamma = N, float(gamma)
+        self.W = torch.zeros(n_entries, N + 1, dtype=torch.float64, device=device)
+        self.t = torch.zeros(n_entries, dtype=torch.int64, device=device)
+        self.tau = torch.zeros(n_entries, dtype=torch.int64, device=device)
+
+    def observe(self, obs_off, depth, stream=None):
+        """Append one batch: obs_off int64 [E+1] CSR offsets, depth int32 (grouped by entry,
+        arrival order within an entry)."""
+        gamma_observe(self.W, self.t, self.tau, obs_off, depth, self.gamma, stream)
+
+    def snapshot(self, out=None, stream=None):
+        return gamma_snapshot(self.W, self.t, self.tau, self.gamma, out, stream)
+
+
+def gamma_observe(W, t, tau, obs_off, depth, gamma, stream=None):
+    E, N = W.shape[0], W.shape[1] - 1
+    st = lib().sp_gamma_observe(_dev(W, torch.float64, "W"), _dev(t, torch.int64, "t"),
+                                _dev(tau, torch.int64, "tau"), _dev(obs_off, torch.int64, "obs_off"),
+                                _dev(depth, torch.int32, "depth"), E, N, float(gamma),
+                                _stream(stream, W.device))
+    _check(st, "sp_gamma_observe")
+
+
+def gamma_snapshot(W, t, tau, gamma, out=None, stream=None):
+    E, N = W.shape[0], W.shape[1] - 1
+    if out is None:
+        out = torch.empty_like(W)
+    st = lib().sp_gamma_snapshot(_dev(W, torch.float64, "W"), _dev(t, torch.int64, "t"),
+                                 _dev(tau, torch.int64, "tau"), E, N, float(gamma),
+                                 _dev(out, torch.float64, "p_out"), _stream(stream, W.device))
+    _check(st, "sp_gamma_snapshot")
+    return out

@@ -62,6 +62,8 @@ def lib():
         L.or_clip_to_blocks.argtypes = [_i32p, _c_i32, _c_i32, _i32p]
         L.or_sqrt_positions.argtypes = [_c_i32, _i32p]
         L.or_log_positions.argtypes = [_c_i32, _c_i32, _i32p]
+        L.or_match_longest_prefix.argtypes = [_i32p, _i64p, _c_i32, _vp, _i32p, _i64p, _c_i64,
+                                              _i32p, _i32p]
         L.or_gamma_hist.argtypes = [_i32p, _c_i64, _c_i32, ctypes.c_double, _f64p]
         L.or_gamma_variance_term.argtypes = [ctypes.c_double, _c_i64, _c_i32]
         L.or_gamma_variance_term.restype = ctypes.c_double
@@ -273,3 +275,20 @@ def gamma_hist(depths, N, gamma):
 
 def gamma_variance_term(gamma, t, N):
     return lib().or_gamma_variance_term(gamma, t, N)
+
+
+def match_longest_prefix(entry_tokens, entry_off, req_tokens, req_off, insertion=None):
+    """f4: (match_entry [R] int32, -1 = none; match_depth [R] int32) by brute force."""
+    et = np.ascontiguousarray(entry_tokens, dtype=np.int32)
+    eo = np.ascontiguousarray(entry_off, dtype=np.int64)
+    rt = np.ascontiguousarray(req_tokens, dtype=np.int32)
+    ro = np.ascontiguousarray(req_off, dtype=np.int64)
+    E, R = eo.size - 1, ro.size - 1
+    me = np.zeros(max(R, 1), np.int32)
+    md = np.zeros(max(R, 1), np.int32)
+    ins = None if insertion is None else np.ascontiguousarray(insertion, dtype=np.int64)
+    _check(lib().or_match_longest_prefix(et if et.size else np.zeros(1, np.int32), eo, E,
+                                         _ptr(ins) if ins is not None else None,
+                                         rt if rt.size else np.zeros(1, np.int32), ro, R, me, md),
+           "or_match_longest_prefix")
+    return me[:R].copy(), md[:R].copy()

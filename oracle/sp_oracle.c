@@ -531,3 +531,38 @@ double or_gamma_variance_term(double gamma, int64_t t, int32_t N) {
   const long double g = gamma, gt = powl(g, (long double)t);
   return (double)sqrtl((long double)N * (1.0L - g) / (1.0L + g) * (1.0L + gt) / (1.0L - gt));
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* f4: longest-prefix match of each request against ALL cached entries (the trie remark of     */
+/* P:189-190; SPEC match_longest_prefix S:375-383), by brute force: the literal LCP loop against */
+/* every entry, keeping the maximum; ties -> the most recent insertion (largest insertion[e],  */
+/* entry index when insertion == NULL; equal insertion values -> larger entry index); a maximum */
+/* of 0 -> no match (entry -1, depth 0).                                                      */
+/* ------------------------------------------------------------------------------------------ */
+int or_match_longest_prefix(const int32_t* ent_tok, const int64_t* ent_off, int32_t E,
+                            const int64_t* insertion, const int32_t* req_tok,
+                            const int64_t* req_off, int64_t R, int32_t* match_entry,
+                            int32_t* match_depth) {
+  if (E < 0 || R < 0) return -1;
+  for (int64_t r = 0; r < R; ++r) {
+    const int32_t* q = req_tok + req_off[r];
+    const int64_t ql = req_off[r + 1] - req_off[r];
+    int64_t best = 0;
+    int32_t who = -1;
+    for (int32_t e = 0; e < E; ++e) {
+      const int32_t* x = ent_tok + ent_off[e];
+      const int64_t xl = ent_off[e + 1] - ent_off[e];
+      int64_t t = 0;
+      while (t < ql && t < xl && q[t] == x[t]) ++t;
+      if (t == 0) continue;
+      if (t > best) { best = t; who = e; continue; }
+      if (t == best) {
+        const int64_t iw = insertion ? insertion[who] : who, ie = insertion ? insertion[e] : e;
+        if (ie > iw || (ie == iw && e > who)) who = e;
+      }
+    }
+    match_entry[r] = who;
+    match_depth[r] = (int32_t)best;
+  }
+  return 0;
+}

@@ -99,6 +99,14 @@ int or_gamma_hist(const int32_t* depths, int64_t t, int32_t N, double gamma, dou
 /* Thm 4's variance term sqrt(N (1-g)/(1+g) (1+g^t)/(1-g^t)). */
 double or_gamma_variance_term(double gamma, int64_t t, int32_t N);
 
+/* f4: longest-prefix match of each request against all cached entries,
+ * brute force.  Ties -> most recent insertion (insertion[e], or the entry index when NULL; equal
+ * values -> larger index); no match (max LCP 0) -> entry -1, depth 0.  Depth is the raw LCP. */
+int or_match_longest_prefix(const int32_t* ent_tok, const int64_t* ent_off, int32_t E,
+                            const int64_t* insertion, const int32_t* req_tok,
+                            const int64_t* req_off, int64_t R, int32_t* match_entry,
+                            int32_t* match_depth);
+
 #ifdef __cplusplus
 }
 #endif

@@ -216,6 +216,30 @@ sp_status sp_gamma_snapshot(const double* W, const int64_t* t, const int64_t* ta
                             int32_t n_entries, int32_t N, double gamma, double* p_out,
                             sp_stream_t stream);
 
+/* ------------------------------------------------------------------------------------------
+ * f4 -- longest-prefix search over ALL cached entries (the trie remark of P:189-190: a request
+ * reuses the deepest cached prefix; SPEC match_longest_prefix S:375-383): for each request, the
+ * entry e maximising LCP(entry_e, request); ties -> the most recent insertion (largest
+ * insertion[e]; the entry index when insertion is NULL; equal values -> larger index);
+ * maximum 0 -> no match.
+ * sp_prefix_index_build sorts the entries by tokens (device merge sort) and builds a sparse
+ * table for range "most recent" queries, into the caller's index buffer of
+ * sp_prefix_index_workspace_bytes(E) bytes (device).  Rebuild whenever the cache changes.
+ * sp_match_longest_prefix: one warp per request, O(log E) warp-cooperative comparisons:
+ *   match_entry int32 [R] (-1 = no match), match_depth int32 [R] (the raw LCP; clamp to N
+ *   before feeding a histogram, as sp_overlap_hist does).
+ * Token layout as sp_overlap_hist (int32 CSR, int64 offsets).  Errors: BAD_LENGTH (E < 0,
+ * R < 0), BAD_ARGUMENT (NULL), WORKSPACE, CUDA.
+ * ---------------------------------------------------------------------------------------- */
+size_t sp_prefix_index_workspace_bytes(int32_t n_entries);
+sp_status sp_prefix_index_build(const int32_t* entry_tokens, const int64_t* entry_off,
+                                int32_t n_entries, const int64_t* insertion, void* index,
+                                size_t index_bytes, sp_stream_t stream);
+sp_status sp_match_longest_prefix(const int32_t* entry_tokens, const int64_t* entry_off,
+                                  int32_t n_entries, const void* index, const int32_t* req_tokens,
+                                  const int64_t* req_off, int64_t n_requests,
+                                  int32_t* match_entry, int32_t* match_depth, sp_stream_t stream);
+
 /* Host-side helpers for the Table 1 baselines.  out_host must hold M (resp.
  * floor(N/B)) ints.  Return the number of positions written, or a negative sp_status. */
 int32_t sp_balanced_positions(int32_t N, int32_t M, int32_t* out_host);

@@ -54,6 +54,10 @@ SYMBOLS = {
     "sp_log_positions": (_i32, [_i32, _i32, _vp]),
     "sp_balanced_positions": (_i32, [_i32, _i32, _vp]),
     "sp_block_positions": (_i32, [_i32, _i32, _vp]),
+    "sp_prefix_index_workspace_bytes": (_sz, [_i32]),
+    "sp_prefix_index_build": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _sz, _vp]),
+    "sp_match_longest_prefix": (ctypes.c_int, [_vp, _vp, _i32, _vp, _vp, _vp, _i64, _vp, _vp,
+                                               _vp]),
     "sp_gamma_observe": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, ctypes.c_double,
                                         _vp]),
     "sp_gamma_snapshot": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, ctypes.c_double, _vp, _vp]),
@@ -381,3 +385,43 @@ def gamma_snapshot(W, t, tau, gamma, out=None, stream=None):
                                  _dev(out, torch.float64, "p_out"), _stream(stream, W.device))
     _check(st, "sp_gamma_snapshot")
     return out
+
+
+# ---------------------------------------------------------------------------------------------
+# f4: longest-prefix search over all cached entries
+# ---------------------------------------------------------------------------------------------
+class PrefixIndex:
+    """Sorted-token index of a set of cached entries (device).  Rebuild when the cache changes."""
+
+    def __init__(self, entry_tokens, entry_off, insertion=None, stream=None):
+        self.entry_tokens, self.entry_off = entry_tokens, entry_off
+        self.E = entry_off.numel() - 1
+        dev = entry_off.device
+        nb = int(lib().sp_prefix_index_workspace_bytes(self.E))
+        self.ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+        ins = None if insertion is None else _dev(insertion, torch.int64, "insertion")
+        tok = _dev(entry_tokens, torch.int32, "entry_tokens") if entry_tokens.numel() else None
+        st = lib().sp_prefix_index_build(tok, _dev(entry_off, torch.int64, "entry_off"), self.E,
+                                         ins, _dev(self.ws, torch.uint8, "index"), nb,
+                                         _stream(stream, dev))
+        _check(st, "sp_prefix_index_build")
+
+    def match(self, req_tokens, req_off, out_entry=None, out_depth=None, stream=None):
+        """Returns (match_entry [R] int32, -1 = none; match_depth [R] int32, the raw LCP)."""
+        R = req_off.numel() - 1
+        dev = req_off.device
+        if out_entry is None:
+            out_entry = torch.empty(max(R, 0), dtype=torch.int32, device=dev)
+        if out_depth is None:
+            out_depth = torch.empty(max(R, 0), dtype=torch.int32, device=dev)
+        if R == 0:
+            return out_entry, out_depth
+        tok = _dev(self.entry_tokens, torch.int32, "entry_tokens") if self.entry_tokens.numel() else None
+        st = lib().sp_match_longest_prefix(
+            tok, _dev(self.entry_off, torch.int64, "entry_off"), self.E,
+            _dev(self.ws, torch.uint8, "index"),
+            _dev(req_tokens, torch.int32, "req_tokens") if req_tokens.numel() else None,
+            _dev(req_off, torch.int64, "req_off"), R, _dev(out_entry, torch.int32, "match_entry"),
+            _dev(out_depth, torch.int32, "match_depth"), _stream(stream, dev))
+        _check(st, "sp_match_longest_prefix")
+        return out_entry, out_depth

@@ -172,12 +172,21 @@ __device__ __forceinline__ int log_lookup_lane(const uint32_t* lg, int cnt, int 
 // SRing addresses a shared array (LDS/STS with compile-time masks); GRing a global overflow ring.
 template <int C0, int C1>
 struct SRing {
-  int2* base;   // the kernel's __shared__ ring array
-  __device__ __forceinline__ int idx(int k, int pos) const {
-    return (k ? C0 * 32 : 0) + ((pos & ((k ? C1 : C0) - 1)) << 5) + lane_id();
+  // shared-window address of the ring array + 8 lane (32-bit, no generic-address conversion)
+  uint32_t base;
+  __device__ __forceinline__ uint32_t addr(int k, int pos) const {
+    const uint32_t m = (uint32_t)((k ? C1 : C0) - 1);
+    return (((uint32_t)pos & m) << 8) + (base + (k ? (uint32_t)C0 * 256u : 0u));
   }
-  __device__ __forceinline__ int2 ld(int k, int pos) const { return base[idx(k, pos)]; }
-  __device__ __forceinline__ void st(int k, int pos, int2 v) const { base[idx(k, pos)] = v; }
+  __device__ __forceinline__ int2 ld(int k, int pos) const {
+    int2 v;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr(k, pos)));
+    return v;
+  }
+  __device__ __forceinline__ void st(int k, int pos, int2 v) const {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr(k, pos)), "r"(v.x), "r"(v.y)
+                 : "memory");
+  }
   static constexpr int cap(int k) { return k ? C1 : C0; }
 };
 template <int C>
@@ -284,6 +293,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           in[1] = lane ? t1 : t0;
         }
         const int32_t Pj = __shfl_sync(FULL, Pc, i);
+        const int32_t nPj = -Pj;
         ++ev_e;
         // ---- push line j: up to four back pops decided from the loaded lines ---------------
         int bj[K], top[K];
@@ -346,9 +356,9 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           b[k] = nb;
           ovf |= act[k] & (d >= RING::cap(k));
           // ---- query x = P_j: up to one front pop decided from the loaded lines -------------
-          v0[k] = F0[k].x - F0[k].y * Pj;
-          v1[k] = F1.x - F1.y * Pj;
-          v2[k] = F2.x - F2.y * Pj;
+          v0[k] = F0[k].x + F0[k].y * nPj;
+          v1[k] = F1.x + F1.y * nPj;
+          v2[k] = F2.x + F2.y * nPj;
           const bool q1 = act[k] & (d >= 1) & (v1[k] < v0[k]);
           q2[k] = q1 & (d >= 2) & (v2[k] < v1[k]);
           const bool one = q1 & !q2[k];
@@ -415,6 +425,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
 template <typename WT, int K>
 __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   __shared__ __align__(16) int2 sring[(K == 2 ? HC0 + HC1 : HC0) * 32];   // [slot][pos][lane]
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
   const int lane = threadIdx.x;
   const int N = p.N, M = p.M;
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
@@ -467,7 +478,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
 #ifdef SP_HULL_FORCE_GLOBAL   // experiment: every entry through the global-ring retry
     bool ovf = true;
 #else
-    bool ovf = hull_dp<WT, K>(p, we, e, TN, n32, SRing<HC0, HC1>{sring}, logs, logn, ebuf0, ebuf1,
+    bool ovf = hull_dp<WT, K>(p, we, e, TN, n32, SRing<HC0, HC1>{sbase + 8u * (uint32_t)lane}, logs, logn, ebuf0, ebuf1,
                               pops_e, ev_e);
 #endif
     if (ovf) {   // retry with a global overflow ring from the pool (rare)

@@ -11,6 +11,7 @@
 // P(x) = chunk prefix + a <= 32-bin partial sum (L1/L2-resident row).  One warp per placement.
 // Count types are exact in int64; fp64 weights are accumulated in double-double.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -175,6 +176,129 @@ __global__ void __launch_bounds__(EV_NT)
   }
 }
 
+// ---- int32 counts: the whole prefix row in shared memory ----------------------------------
+// One 512-thread CTA per entry (persistent over entries).  The row is read in rounds of 16K
+// bins: warp w owns 1024 consecutive bins, lane l holds bins 32u + l (u < 32) -- all 32 loads of
+// a lane are issued before any is used, so a round keeps the whole 128 KB segment in flight.
+// Each warp scans its segment in place (prefix relative to the segment start, int32) and the
+// segment offsets (int64) go to woff[], so P(x) = seg[x] + woff[x >> 10]: one shared lookup per
+// query instead of a 32-bin partial sum.  A segment whose own total reaches 2^31 (never on W5)
+// makes the entry use exact int64 partial sums from global memory instead.
+constexpr int EP_NT = 512;
+constexpr int EP_NW = EP_NT / 32;
+
+__global__ void __launch_bounds__(EP_NT)
+    eval_p32_kernel(const int32_t* __restrict__ w, int E, int N,
+                    const int32_t* __restrict__ positions, const int32_t* __restrict__ npos,
+                    int S, int max_pos, int broadcast, int64_t* __restrict__ cost,
+                    int32_t* __restrict__ worst) {
+  extern __shared__ __align__(16) int32_t seg[];   // [nseg * 1024] in-segment prefixes
+  __shared__ long long woff[65];                     // exclusive segment offsets
+  __shared__ long long wtot[EP_NW], tsum[EP_NW];
+  __shared__ long long sh_carry, sh_TN;
+  __shared__ int sh_big;
+  const int lane = lane_id(), wid = warp_id();
+  const int nseg = (N + 1 + 1023) / 1024;
+  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+    const int32_t* we = w + (int64_t)e * (N + 1);
+    long long tpart = 0;
+    int big = 0;
+    if (threadIdx.x == 0) sh_carry = 0;
+    for (int r0 = 0; r0 < nseg; r0 += EP_NW) {   // one round: segments r0 .. r0 + 31
+      const int sg = r0 + wid;
+      const int b0 = sg * 1024;
+      int32_t v[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int t = b0 + 32 * u + lane;
+        v[u] = (sg < nseg && t >= 1 && t <= N) ? __ldcs(we + t) : 0;
+      }
+      int run32 = 0;
+      long long ls = 0;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int t = b0 + 32 * u + lane;
+        tpart += (long long)t * v[u];
+        ls += v[u];
+        int inc = v[u];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, inc, o);
+          if (lane >= o) inc += y;
+        }
+        // exact while the segment total < 2^31 (checked below)
+        if (sg < nseg) seg[b0 + 32 * u + lane] = run32 + inc;
+        run32 += __shfl_sync(FULL, inc, 31);
+      }
+      const long long run = warp_sum(ls);
+      big |= run >= (1ll << 31);
+      if (lane == 0) wtot[wid] = sg < nseg ? run : 0;
+      __syncthreads();
+      if (wid == 0) {   // exclusive scan of this round's segment totals
+        const long long c0 = sh_carry;
+        const long long x = wtot[lane];
+        long long inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long y = __shfl_up_sync(FULL, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (r0 + lane < nseg) woff[r0 + lane] = c0 + inc - x;
+        if (lane == 31) sh_carry = c0 + inc;
+      }
+      __syncthreads();
+    }
+    tpart = warp_sum(tpart);
+    big = __any_sync(FULL, big);
+    if (lane == 0) tsum[wid] = tpart;
+    if (threadIdx.x == 0) sh_big = 0;
+    __syncthreads();
+    if (lane == 0 && big) sh_big = 1;
+    if (threadIdx.x == 0) {
+      long long tn = 0;
+      for (int q = 0; q < EP_NW; ++q) tn += tsum[q];
+      sh_TN = tn;
+    }
+    __syncthreads();
+    const long long TN = sh_TN;
+    const bool exact32 = !sh_big;
+    auto Pof = [&](int x) -> long long {
+      if (x <= 0) return 0;
+      if (exact32) return (long long)seg[x] + woff[x >> 10];
+      long long s = woff[x >> 10];   // a huge segment: sum its bins from global memory
+      for (int t = max((x >> 10) << 10, 1); t <= x; ++t) s += we[t];
+      return s;
+    };
+    for (int q = wid; q < S; q += EP_NW) {
+      const int64_t set = broadcast ? q : (int64_t)e * S + q;
+      const int32_t* pc = positions + set * max_pos;
+      const int k = npos[set];
+      bool ok = k >= 0 && k <= max_pos;
+      long long acc = 0;
+      int gmax = 0;
+      if (ok) {
+        for (int i = lane; i <= k; i += 32) {   // gap i: (c_i, c_{i+1})
+          const int ci = i == 0 ? 0 : pc[i - 1];
+          const int cn = i == k ? N + 1 : pc[i];
+          if (cn <= ci || cn > N + 1 || (i > 0 && ci < 1)) ok = false;
+          gmax = max(gmax, cn - ci);
+          if (i >= 1 && ok) acc += (long long)ci * (Pof(cn - 1) - Pof(ci - 1));
+        }
+      }
+      ok = __all_sync(FULL, ok);
+      acc = warp_sum(acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gmax = max(gmax, __shfl_xor_sync(FULL, gmax, o));
+      if (lane == 0) {
+        const int64_t oi = (int64_t)e * S + q;
+        cost[oi] = ok ? TN - acc : -1;
+        if (worst) worst[oi] = ok ? gmax - 1 : -SP_ERR_BAD_POSITIONS;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace sp
 
 extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type wtype,
@@ -194,7 +318,16 @@ extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type w
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = n_entries < sms * 8 ? n_entries : sms * 8;
   cudaStream_t st = (cudaStream_t)stream;
-  if (wtype == SP_W_COUNTS_I32)
+  if (wtype == SP_W_COUNTS_I32 && !getenv("SP_EVAL_CHUNKED")) {
+    const int nseg = (N + 1 + 1023) / 1024;
+    const size_t dyn = (size_t)nseg * 1024 * 4;
+    cudaFuncSetAttribute(sp::eval_p32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)dyn);
+    const int g2 = n_entries < sms ? n_entries : sms;
+    sp::eval_p32_kernel<<<g2, sp::EP_NT, dyn, st>>>((const int32_t*)weights, n_entries, N,
+                                                    positions, n_positions, n_sets, max_pos,
+                                                    broadcast, (int64_t*)cost, worst_case);
+  } else if (wtype == SP_W_COUNTS_I32)
     sp::eval_kernel<int32_t><<<grid, sp::EV_NT, 0, st>>>(
         (const int32_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
         broadcast, (int64_t*)cost, worst_case);

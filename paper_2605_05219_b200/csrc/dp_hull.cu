@@ -189,6 +189,33 @@ struct SRing {
   }
   static constexpr int cap(int k) { return k ? C1 : C0; }
 };
+// 6-byte lines: intercepts int32 [slot][pos][lane] (128 B per position) and s uint16
+// [slot][pos][lane] (64 B per position) in two arrays -- 25% less shared memory per layer than
+// int2 lines (more warps per SM) for a second LDS per line.
+template <int C0, int C1>
+struct SRing6 {
+  uint32_t bbase, sbase;   // shared addresses of the two arrays + 4 lane / + 2 lane
+  __device__ __forceinline__ int2 ld(int k, int pos) const {
+    const uint32_t q = (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
+    const uint32_t ab = (q << 7) + bbase + (k ? (uint32_t)C0 * 128u : 0u);
+    const uint32_t as = (q << 6) + sbase + (k ? (uint32_t)C0 * 64u : 0u);
+    int2 v;
+    unsigned short sv;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.x) : "r"(ab));
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sv) : "r"(as));
+    v.y = sv;
+    return v;
+  }
+  __device__ __forceinline__ void st(int k, int pos, int2 v) const {
+    const uint32_t q = (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
+    const uint32_t ab = (q << 7) + bbase + (k ? (uint32_t)C0 * 128u : 0u);
+    const uint32_t as = (q << 6) + sbase + (k ? (uint32_t)C0 * 64u : 0u);
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(ab), "r"(v.x) : "memory");
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(as), "h"((unsigned short)v.y) : "memory");
+  }
+  static constexpr int cap(int k) { return k ? C1 : C0; }
+};
+
 template <int C>
 struct GRing {
   int2* base;   // one ring of the global pool
@@ -424,9 +451,17 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
 
 template <typename WT, int K>
 __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
+  const int lane = threadIdx.x;
+#ifndef SP_HULL_RING6
   __shared__ __align__(16) int2 sring[(K == 2 ? HC0 + HC1 : HC0) * 32];   // [slot][pos][lane]
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
-  const int lane = threadIdx.x;
+  const SRing<HC0, HC1> srg{sbase + 8u * (uint32_t)lane};
+#else   // 6-byte lines: 12 instead of 9 warps/SM, measured no faster (49.2 vs 48.6 ms on W5)
+  __shared__ __align__(16) int32_t sring_b[(K == 2 ? HC0 + HC1 : HC0) * 32];
+  __shared__ __align__(16) uint16_t sring_s[(K == 2 ? HC0 + HC1 : HC0) * 32];
+  const SRing6<HC0, HC1> srg{(uint32_t)__cvta_generic_to_shared(sring_b) + 4u * (uint32_t)lane,
+                             (uint32_t)__cvta_generic_to_shared(sring_s) + 2u * (uint32_t)lane};
+#endif
   const int N = p.N, M = p.M;
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
   unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
@@ -478,7 +513,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
 #ifdef SP_HULL_FORCE_GLOBAL   // experiment: every entry through the global-ring retry
     bool ovf = true;
 #else
-    bool ovf = hull_dp<WT, K>(p, we, e, TN, n32, SRing<HC0, HC1>{sbase + 8u * (uint32_t)lane}, logs, logn, ebuf0, ebuf1,
+    bool ovf = hull_dp<WT, K>(p, we, e, TN, n32, srg, logs, logn, ebuf0, ebuf1,
                               pops_e, ev_e);
 #endif
     if (ovf) {   // retry with a global overflow ring from the pool (rare)

@@ -62,7 +62,7 @@ constexpr int HC0 = SP_HULL_CAP0, HC1 = SP_HULL_CAP1;
 #define SP_HULL_HCG 2048
 #endif
 #ifndef SP_HULL_POOL
-#define SP_HULL_POOL 32
+#define SP_HULL_POOL 64
 #endif
 constexpr int HCG = SP_HULL_HCG;
 constexpr int HPOOL = SP_HULL_POOL;
@@ -78,7 +78,7 @@ __host__ __device__ __forceinline__ int hull_passes(int M) {
 __host__ __device__ __forceinline__ int hull_layers_padded(int M) {
   return hull_passes(M) * 32 * hull_K(M);
 }
-// slot: argmin logs uint32 [layer][N+1] | log counts int32 [layer] | e-row buffers 2 x int32[N+1]
+// slot: argmin logs uint32 [layer][N+1] | log counts int32 [layer] | e-row buffers 2 x VT[N+1]
 __host__ __device__ __forceinline__ size_t hull_log_bytes(int N, int M) {
   return hull_align((size_t)hull_layers_padded(M) * (N + 1) * 4);
 }
@@ -86,7 +86,7 @@ __host__ __device__ __forceinline__ size_t hull_cnt_bytes(int M) {
   return hull_align((size_t)hull_layers_padded(M) * 4);
 }
 __host__ __device__ __forceinline__ size_t hull_slot_bytes(int N, int M) {
-  return hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(4 * (size_t)(N + 1));
+  return hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(8 * (size_t)(N + 1));
 }
 __host__ __device__ __forceinline__ size_t hull_smem_bytes(int) { return 0; }   // static rings
 
@@ -103,11 +103,12 @@ struct HullParams {
   int32_t* fb;      // fallback entry list
   uint8_t* slots;   // per-warp slots
   size_t slot;
-  int2* gring;      // HPOOL global overflow rings, [ring][slot][HCG][32] lines
+  void* gring;      // HPOOL global overflow rings, [ring][slot][HCG][32] lines (16 B each)
+  int32_t* wide;    // entries for the int64 instantiation
 };
 
 __host__ __device__ __forceinline__ size_t hull_pool_bytes(int M) {
-  return (size_t)HPOOL * hull_K(M) * HCG * 32 * sizeof(int2);
+  return (size_t)HPOOL * hull_K(M) * HCG * 32 * 16;   // sized for Line<long long>
 }
 
 // claim / return a global overflow ring (lane 0 only)
@@ -168,79 +169,89 @@ __device__ __forceinline__ int log_lookup_lane(const uint32_t* lg, int cnt, int 
   return (int)(__ldcg(lg + lo) & 0xffffu);
 }
 
-// Ring storage policies: slot k's ring has C_k positions of 32 lines (256 B), [slot][pos][lane].
-// SRing addresses a shared array (LDS/STS with compile-time masks); GRing a global overflow ring.
+// A hull line: intercept b_s (value type VT) and s.
+template <typename VT>
+struct Line {
+  VT b;
+  int s;
+};
+
+// Ring storage policies, [slot][pos][lane] so that every lane has its own banks.
+// SRing: shared memory, int32 lines packed as int2 (256 B per position) or int64 lines as an int64
+// array (256 B per position) plus an int32 array (128 B per position); LDS/STS on 32-bit shared
+// addresses with compile-time masks.  GRing: a global overflow ring from the pool.
+template <typename VT, int C0, int C1>
+struct SRing;
 template <int C0, int C1>
-struct SRing {
-  // shared-window address of the ring array + 8 lane (32-bit, no generic-address conversion)
-  uint32_t base;
+struct SRing<int, C0, C1> {
+  uint32_t base;   // shared address of the ring array + 8 lane
   __device__ __forceinline__ uint32_t addr(int k, int pos) const {
     const uint32_t m = (uint32_t)((k ? C1 : C0) - 1);
     return (((uint32_t)pos & m) << 8) + (base + (k ? (uint32_t)C0 * 256u : 0u));
   }
-  __device__ __forceinline__ int2 ld(int k, int pos) const {
-    int2 v;
-    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr(k, pos)));
+  __device__ __forceinline__ Line<int> ld(int k, int pos) const {
+    Line<int> v;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.b), "=r"(v.s) : "r"(addr(k, pos)));
     return v;
   }
-  __device__ __forceinline__ void st(int k, int pos, int2 v) const {
-    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr(k, pos)), "r"(v.x), "r"(v.y)
+  __device__ __forceinline__ void st(int k, int pos, Line<int> v) const {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr(k, pos)), "r"(v.b), "r"(v.s)
                  : "memory");
   }
   static constexpr int cap(int k) { return k ? C1 : C0; }
+  static constexpr size_t bytes() { return (size_t)(C0 + C1) * 256; }
 };
-// 6-byte lines: intercepts int32 [slot][pos][lane] (128 B per position) and s uint16
-// [slot][pos][lane] (64 B per position) in two arrays -- 25% less shared memory per layer than
-// int2 lines (more warps per SM) for a second LDS per line.
 template <int C0, int C1>
-struct SRing6 {
-  uint32_t bbase, sbase;   // shared addresses of the two arrays + 4 lane / + 2 lane
-  __device__ __forceinline__ int2 ld(int k, int pos) const {
-    const uint32_t q = (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
-    const uint32_t ab = (q << 7) + bbase + (k ? (uint32_t)C0 * 128u : 0u);
-    const uint32_t as = (q << 6) + sbase + (k ? (uint32_t)C0 * 64u : 0u);
-    int2 v;
-    unsigned short sv;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.x) : "r"(ab));
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sv) : "r"(as));
-    v.y = sv;
+struct SRing<long long, C0, C1> {
+  uint32_t bb, sb;   // shared addresses of the intercept array + 8 lane and the s array + 4 lane
+  __device__ __forceinline__ uint32_t q(int k, int pos) const {
+    return (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
+  }
+  __device__ __forceinline__ Line<long long> ld(int k, int pos) const {
+    const uint32_t x = q(k, pos);
+    Line<long long> v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v.b) : "r"((x << 8) + bb + (k ? C0 * 256u : 0u)));
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.s) : "r"((x << 7) + sb + (k ? C0 * 128u : 0u)));
     return v;
   }
-  __device__ __forceinline__ void st(int k, int pos, int2 v) const {
-    const uint32_t q = (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
-    const uint32_t ab = (q << 7) + bbase + (k ? (uint32_t)C0 * 128u : 0u);
-    const uint32_t as = (q << 6) + sbase + (k ? (uint32_t)C0 * 64u : 0u);
-    asm volatile("st.shared.b32 [%0], %1;" ::"r"(ab), "r"(v.x) : "memory");
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(as), "h"((unsigned short)v.y) : "memory");
+  __device__ __forceinline__ void st(int k, int pos, Line<long long> v) const {
+    const uint32_t x = q(k, pos);
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"((x << 8) + bb + (k ? C0 * 256u : 0u)), "l"(v.b)
+                 : "memory");
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"((x << 7) + sb + (k ? C0 * 128u : 0u)), "r"(v.s)
+                 : "memory");
   }
   static constexpr int cap(int k) { return k ? C1 : C0; }
+  static constexpr size_t bytes() { return (size_t)(C0 + C1) * 384; }
 };
 
-template <int C>
+template <typename VT, int C>
 struct GRing {
-  int2* base;   // one ring of the global pool
+  Line<VT>* base;   // one ring of the global pool
   __device__ __forceinline__ int idx(int k, int pos) const {
     return k * C * 32 + ((pos & (C - 1)) << 5) + lane_id();
   }
-  __device__ __forceinline__ int2 ld(int k, int pos) const { return base[idx(k, pos)]; }
-  __device__ __forceinline__ void st(int k, int pos, int2 v) const { base[idx(k, pos)] = v; }
+  __device__ __forceinline__ Line<VT> ld(int k, int pos) const { return base[idx(k, pos)]; }
+  __device__ __forceinline__ void st(int k, int pos, Line<VT> v) const { base[idx(k, pos)] = v; }
   static constexpr int cap(int) { return C; }
 };
 
 // back-pop test with the new point (j, bj) as origin: for the pair (A, Bk) of consecutive hull
 // lines (A below Bk), with A' = A - new and Bk' = Bk - new in (s, b) coordinates, Bk goes iff it is
 // not strictly below the segment A -> new, i.e. cross(A', Bk') = A'.s Bk'.b - A'.b Bk'.s <= 0.
-// |b'| < 2^30, |s'| < 2^16: products < 2^46 in int64, exact.
-__device__ __forceinline__ bool pop_test(int as, int ab, int ks, int kb) {
-  return (long long)as * kb <= (long long)ab * ks;
+// |s'| < 2^16 and |b'| <= n N: < 2^30 on the int32 path, < 2^46 on the int64 path (guards in
+// the kernel), so both products are exact in int64.
+template <typename VT>
+__device__ __forceinline__ bool pop_test(int as, VT ab, int ks, VT kb) {
+  return (long long)as * (long long)kb <= (long long)ab * (long long)ks;
 }
 
 // a4 for one entry: all layers in lockstep, one support row per step.  Returns true when a ring
 // overflowed (the entry's results are then invalid).
-template <typename WT, int K, class RING>
+template <typename WT, typename VT, int K, class RING>
 __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
-                                        long long TN, int n32, const RING rg, uint32_t* logs,
-                                        int32_t* logn, int32_t* ebuf0, int32_t* ebuf1,
+                                        long long TN, VT nV, const RING rg, uint32_t* logs,
+                                        int32_t* logn, VT* ebuf0, VT* ebuf1,
                                         unsigned& pops_e, unsigned& ev_e) {
   const int lane = lane_id();
   const int N = p.N, M = p.M;
@@ -248,16 +259,17 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
   const int passes = (M + L - 1) / L;
   bool ovf = false;
   for (int ps = 0; ps < passes && !ovf; ++ps) {
-    const int32_t* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
-    int32_t* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
+    const VT* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
+    VT* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
     const bool chain_in = ps > 0, chain_out = ps + 1 < passes;
     // Per slot: deque [f, b] (monotone counters; ring position = counter mod capacity).  In
     // registers: the back line B0 (the last one pushed) and the front line F0; the four lines
     // below the back and the two above the front are loaded from the ring at the top of every
     // support row (positions known a row ahead, so the loads overlap the shuffle).  A line is
     // int2 (x = intercept b_s, y = s).  eo = e_m(j) (the running row value), op = opt_m(j).
-    int f[K], b[K], eo[K], op[K], cnt[K];
-    int2 B0[K], F0[K];
+    int f[K], b[K], op[K], cnt[K];
+    VT eo[K];
+    Line<VT> B0[K], F0[K];
     bool act[K];
     uint32_t* lg[K];
 #pragma unroll
@@ -271,26 +283,26 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       cnt[k] = 1;
       lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * (N + 1);
       if (act[k]) lg[k][0] = (1u << 16) | 1u;
-      B0[k] = F0[k] = make_int2(0, 1);
+      B0[k] = F0[k] = Line<VT>{0, 1};
     }
-    int32_t carry = 0, Pm1 = 0;
+    VT carry = 0, Pm1 = 0;
     int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
     for (int jb = 0; jb < N; jb += 32) {
       const int jr = jb + 1 + lane;
-      const int32_t craw = jr <= N ? (int32_t)we[jr] : 0;
+      const VT craw = jr <= N ? (VT)we[jr] : (VT)0;
       unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
       if (evmask == 0) continue;                          // 32 zero rows: nothing changes
-      int32_t cnt32 = craw;
+      VT cnt32 = craw;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(FULL, cnt32, o);
+        const VT y = __shfl_up_sync(FULL, cnt32, o);
         if (lane >= o) cnt32 += y;
       }
-      const int32_t Pc = carry + cnt32;
+      const VT Pc = carry + cnt32;
       carry = __shfl_sync(FULL, Pc, 31);
       // previous pass's top layer at the support rows: e(j-1) of support row number t is its
       // value at support row t-1 (constant over zero rows), 0 before the first
-      int32_t Ec = 0;
+      VT Ec = 0;
       const int nev = __popc(evmask);
       if (chain_in && lane < nev) Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
       for (int q = 0; evmask; ++q) {
@@ -298,7 +310,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         evmask &= evmask - 1;
         const int j = jb + 1 + i;
         // ring lines around both ends (positions fixed by the previous row)
-        int2 L1[K], L2[K], L3[K], L4[K], G1[K], G2[K];
+        Line<VT> L1[K], L2[K], L3[K], L4[K], G1[K], G2[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           L1[k] = rg.ld(k, b[k] - 1);
@@ -310,34 +322,34 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         }
         // e_{m-1}(j-1): from the lane below (its value at the previous support row);
         // lane 0 slot 0 from the previous pass (or e_0 = 0)
-        int32_t in[K];
-        const int32_t t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
-        int32_t ext = 0;
+        VT in[K];
+        const VT t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
+        VT ext = 0;
         if (chain_in) ext = __shfl_sync(FULL, Ec, q);
         in[0] = lane ? t0 : ext;
         if constexpr (K == 2) {
-          const int32_t t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
+          const VT t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
           in[1] = lane ? t1 : t0;
         }
-        const int32_t Pj = __shfl_sync(FULL, Pc, i);
-        const int32_t nPj = -Pj;
+        const VT Pj = __shfl_sync(FULL, Pc, i);
+        const VT nPj = -Pj;
         ++ev_e;
         // ---- push line j: up to four back pops decided from the loaded lines ---------------
-        int bj[K], top[K];
+        VT bj[K];
+        int top[K];
         bool more[K], skip[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          bj[k] = in[k] + j * Pm1;
+          bj[k] = in[k] + (VT)j * Pm1;
           // deltas of the back lines from the new point (j, bj)
-          const int s0 = B0[k].y - j, c0 = B0[k].x - bj[k];
-          const int s1 = L1[k].y - j, c1 = L1[k].x - bj[k];
-          const int s2 = L2[k].y - j, c2 = L2[k].x - bj[k];
-          const int s3 = L3[k].y - j, c3 = L3[k].x - bj[k];
-          const int s4 = L4[k].y - j, c4 = L4[k].x - bj[k];
+          const int s0 = B0[k].s - j, s1 = L1[k].s - j, s2 = L2[k].s - j;
+          const int s3 = L3[k].s - j, s4 = L4[k].s - j;
+          const VT c0 = B0[k].b - bj[k], c1 = L1[k].b - bj[k], c2 = L2[k].b - bj[k];
+          const VT c3 = L3[k].b - bj[k], c4 = L4[k].b - bj[k];
           // a line that overtakes the back line only beyond x = P_N = n is never optimal at a
           // query (x <= n): it is neither pushed nor allowed to pop.
           // x(back, new) > n  <=>  bj - B0.b > n (j - B0.s)  <=>  -c0 > -n s0
-          skip[k] = (b[k] >= f[k]) & (c0 < n32 * s0);
+          skip[k] = (b[k] >= f[k]) & (c0 < nV * (VT)s0);
           const int sz = skip[k] ? 0 : b[k] - f[k];   // deque size - 1, before the push
           const int p1 = (sz >= 1) & pop_test(s1, c1, s0, c0);
           const int p2 = p1 & (sz >= 2) & pop_test(s2, c2, s1, c1);
@@ -352,10 +364,12 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
 #pragma unroll
           for (int k = 0; k < K; ++k) {
             if (!more[k]) continue;
-            int cs = L4[k].y - j, cb = L4[k].x - bj[k];
+            int cs = L4[k].s - j;
+            VT cb = L4[k].b - bj[k];
             while (top[k] - f[k] >= 1) {
-              const int2 l1 = rg.ld(k, top[k] - 1);
-              const int ls = l1.y - j, lb = l1.x - bj[k];
+              const Line<VT> l1 = rg.ld(k, top[k] - 1);
+              const int ls = l1.s - j;
+              const VT lb = l1.b - bj[k];
               if (pop_test(ls, lb, cs, cb)) {
                 --top[k];
                 cs = ls;
@@ -366,26 +380,26 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
             }
           }
         }
-        int v0[K], v1[K], v2[K];
+        VT v0[K], v1[K], v2[K];
         bool q2[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const int nb = skip[k] ? b[k] : top[k] + 1;
           pops_e += (unsigned)(b[k] - top[k]);
-          const int2 nl = make_int2(bj[k], j);
+          const Line<VT> nl{bj[k], j};
           if (!skip[k]) rg.st(k, nb, nl);
           const int d = nb - f[k];
           const bool fresh = !skip[k];
-          const int2 F1 = (fresh & (d == 1)) ? nl : G1[k];   // lines f+1 / f+2 popped or new
-          const int2 F2 = (fresh & (d == 2)) ? nl : G2[k];
+          const Line<VT> F1 = (fresh & (d == 1)) ? nl : G1[k];   // lines f+1 / f+2 popped or new
+          const Line<VT> F2 = (fresh & (d == 2)) ? nl : G2[k];
           F0[k] = (fresh & (d == 0)) ? nl : F0[k];         // the deque was empty
           B0[k] = skip[k] ? B0[k] : nl;
           b[k] = nb;
           ovf |= act[k] & (d >= RING::cap(k));
           // ---- query x = P_j: up to one front pop decided from the loaded lines -------------
-          v0[k] = F0[k].x + F0[k].y * nPj;
-          v1[k] = F1.x + F1.y * nPj;
-          v2[k] = F2.x + F2.y * nPj;
+          v0[k] = F0[k].b + (VT)F0[k].s * nPj;
+          v1[k] = F1.b + (VT)F1.s * nPj;
+          v2[k] = F2.b + (VT)F2.s * nPj;
           const bool q1 = act[k] & (d >= 1) & (v1[k] < v0[k]);
           q2[k] = q1 & (d >= 2) & (v2[k] < v1[k]);
           const bool one = q1 & !q2[k];
@@ -401,8 +415,8 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
             if (!q2[k]) continue;
             f[k] += 2;   // F0 = line f+2 already
             while (f[k] < b[k]) {
-              const int2 l1 = rg.ld(k, f[k] + 1);
-              const int vl = l1.x - l1.y * Pj;
+              const Line<VT> l1 = rg.ld(k, f[k] + 1);
+              const VT vl = l1.b + (VT)l1.s * nPj;
               if (vl < v0[k]) {
                 ++f[k];
                 F0[k] = l1;
@@ -418,7 +432,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           eo[k] = v0[k];
-          const int nop = F0[k].y;
+          const int nop = F0[k].s;
           if (act[k] & (nop != op[k])) {
             lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop;
             ++cnt[k];
@@ -449,36 +463,46 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
   return ovf;
 }
 
-template <typename WT, int K>
+// VT = int: every entry first; those beyond the int32 guard but within the int64 one are listed
+// for the VT = long long instantiation (launched next, same slots); the rest for the D&C kernel.
+template <typename WT, int K, typename VT>
 __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
+  constexpr bool WIDE = sizeof(VT) == 8;
   const int lane = threadIdx.x;
 #ifndef SP_HULL_RING6
-  __shared__ __align__(16) int2 sring[(K == 2 ? HC0 + HC1 : HC0) * 32];   // [slot][pos][lane]
+  constexpr int NPOS = HC0 + (K == 2 ? HC1 : 0);   // ring positions of this warp
+  __shared__ __align__(16) uint8_t sring[NPOS * (WIDE ? 384 : 256)];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
-  const SRing<HC0, HC1> srg{sbase + 8u * (uint32_t)lane};
-#else   // 6-byte lines: 12 instead of 9 warps/SM, measured no faster (49.2 vs 48.6 ms on W5)
-  __shared__ __align__(16) int32_t sring_b[(K == 2 ? HC0 + HC1 : HC0) * 32];
-  __shared__ __align__(16) uint16_t sring_s[(K == 2 ? HC0 + HC1 : HC0) * 32];
-  const SRing6<HC0, HC1> srg{(uint32_t)__cvta_generic_to_shared(sring_b) + 4u * (uint32_t)lane,
-                             (uint32_t)__cvta_generic_to_shared(sring_s) + 2u * (uint32_t)lane};
+  SRing<VT, HC0, HC1> srg;
+  if constexpr (WIDE) {
+    srg.bb = sbase + 8u * (uint32_t)lane;
+    srg.sb = sbase + (uint32_t)NPOS * 256u + 4u * (uint32_t)lane;
+  } else {
+    srg.base = sbase + 8u * (uint32_t)lane;
+  }
+#else
+#error "SP_HULL_RING6 is not maintained for the generic value type"
 #endif
   const int N = p.N, M = p.M;
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
   unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
-  unsigned* ectr = reinterpret_cast<unsigned*>(p.ws + SP_WS_ENTRY_CTR_OFF);
+  unsigned* wide_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_WIDE_COUNT_OFF);
+  unsigned* ectr = reinterpret_cast<unsigned*>(p.ws + (WIDE ? SP_WS_WIDE_CTR_OFF : SP_WS_ENTRY_CTR_OFF));
+  const int n_items = WIDE ? (int)*reinterpret_cast<volatile unsigned*>(wide_n) : p.E;
   uint8_t* slot = p.slots + (size_t)blockIdx.x * p.slot;
   uint32_t* logs = reinterpret_cast<uint32_t*>(slot);
   int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
-  int32_t* ebuf0 = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M) + hull_cnt_bytes(M));
-  int32_t* ebuf1 = ebuf0 + hull_align(4 * (size_t)(N + 1)) / 4;
+  VT* ebuf0 = reinterpret_cast<VT*>(slot + hull_log_bytes(N, M) + hull_cnt_bytes(M));
+  VT* ebuf1 = ebuf0 + hull_align(8 * (size_t)(N + 1)) / sizeof(VT);
   unsigned long long pops = 0, events = 0;
   int done_entries = 0;
 
   for (;;) {
-    int e = 0;
-    if (lane == 0) e = (int)atomicAdd(ectr, 1u);
-    e = __shfl_sync(FULL, e, 0);
-    if (e >= p.E) break;
+    int it = 0;
+    if (lane == 0) it = (int)atomicAdd(ectr, 1u);
+    it = __shfl_sync(FULL, it, 0);
+    if (it >= n_items) break;
+    const int e = WIDE ? p.wide[it] : it;
     const WT* we = reinterpret_cast<const WT*>(p.w) + (int64_t)e * (N + 1);
 
     // ---- a3 pre-pass: n = P_N, T_N, first non-zero bin, sign / size guards ---------------
@@ -486,7 +510,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
     int bad = 0, tfirst = INT_MAX;
     for (int t = lane + 1; t <= N; t += 32) {
       const long long c = (long long)we[t];
-      bad |= (c < 0) | (c >= (1ll << 30));
+      bad |= (c < 0) | (c >= (1ll << 40));
       if (!bad) {
         n += c;
         TN += (long long)t * c;
@@ -498,23 +522,29 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
     TN = warp_sum(TN);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) tfirst = min(tfirst, __shfl_xor_sync(FULL, tfirst, o));
-    // exact-int32 guard 2 n N < 2^31 (the D&C kernel's "narrow" condition); else fall back
-    if (bad || n >= (1ll << 30) / N) {
-      if (lane == 0) p.fb[atomicAdd(fb_n, 1u)] = e;
+    // int32 path: 2 n N < 2^31 (the D&C kernel's "narrow" condition: every intercept, candidate
+    // and difference exact in int32); int64 path: n N < 2^46 (differences < 2^46, cross products
+    // < 2^62); otherwise (or negative counts) the D&C kernel
+    const bool narrow = !bad && n < (1ll << 30) / N;
+    const bool wide_ok = !bad && n < (1ll << 46) / N;
+    if (!WIDE && !narrow) {
+      if (lane == 0) {
+        if (wide_ok) p.wide[atomicAdd(wide_n, 1u)] = e;
+        else p.fb[atomicAdd(fb_n, 1u)] = e;
+      }
       continue;
     }
     if (lane == 0) {
       if (p.cbb) p.cbb[(int64_t)e * (M + 1)] = TN;   // V_0 = T_N
     }
-    const int n32 = (int)n;   // P_N; n N < 2^30, so n (j - s) fits int32
+    const VT nV = (VT)n;   // P_N; n N < 2^30 (int) / 2^46 (long long), so n (j - s) fits VT
 
     // ---- a4: all layers in lockstep, one support row per step --------------------------------
     unsigned pops_e = 0, ev_e = 0;
 #ifdef SP_HULL_FORCE_GLOBAL   // experiment: every entry through the global-ring retry
     bool ovf = true;
 #else
-    bool ovf = hull_dp<WT, K>(p, we, e, TN, n32, srg, logs, logn, ebuf0, ebuf1,
-                              pops_e, ev_e);
+    bool ovf = hull_dp<WT, VT, K>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1, pops_e, ev_e);
 #endif
     if (ovf) {   // retry with a global overflow ring from the pool (rare)
       int g = -1;
@@ -522,8 +552,9 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
       g = __shfl_sync(FULL, g, 0);
       if (g >= 0) {
         pops_e = ev_e = 0;
-        ovf = hull_dp<WT, K>(p, we, e, TN, n32, GRing<HCG>{p.gring + (size_t)g * K * HCG * 32},
-                             logs, logn, ebuf0, ebuf1, pops_e, ev_e);
+        Line<VT>* gr = reinterpret_cast<Line<VT>*>(p.gring) + (size_t)g * K * HCG * 32;
+        ovf = hull_dp<WT, VT, K>(p, we, e, TN, nV, GRing<VT, HCG>{gr}, logs, logn, ebuf0, ebuf1,
+                                 pops_e, ev_e);
         __syncwarp();
         if (lane == 0) pool_release(p, g);
       }
@@ -587,33 +618,39 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   if (lane == 0) {
     atomicAdd(&stats->hull_pops, pops);
     atomicAdd(&stats->entries_hull, (unsigned long long)done_entries);
-    atomicAdd(&stats->entries_i32, (unsigned long long)done_entries);
+    atomicAdd(WIDE ? &stats->entries_i64 : &stats->entries_i32, (unsigned long long)done_entries);
     atomicAdd(&stats->hull_event_rows, events);
   }
 }
 
-template <typename WT, int K>
-static int hull_grid_t(int E, int M) {
+template <typename WT, int K, typename VT>
+static int hull_grid_t(int E) {
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t dyn = hull_smem_bytes(M);
-  cudaFuncSetAttribute(dp_hull_kernel<WT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_hull_kernel<WT, K>, 32, dyn);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_hull_kernel<WT, K, VT>, 32, 0);
   if (occ < 1) occ = 1;
   long g = (long)sms * occ;
   if (g > E) g = E;
   return (int)(g < 1 ? 1 : g);
 }
 
+template <typename WT, int K>
+static void hull_launch_t(const HullParams& p, int gn, cudaStream_t st) {
+  dp_hull_kernel<WT, K, int><<<gn, 32, 0, st>>>(p);
+  // the int64 instantiation on the listed entries (its warps exit at once when the list is empty)
+  dp_hull_kernel<WT, K, long long><<<hull_grid_t<WT, K, long long>(p.E), 32, 0, st>>>(p);
+}
+
 }  // namespace sp
 
+// the int32 instantiation has the largest grid; the int64 one uses a prefix of its slots
 int sp_hull_grid(int E, int N, int M, int wtype) {
   (void)N;
   const bool k2 = sp::hull_K(M) == 2;
   if (wtype == SP_W_COUNTS_I64)
-    return k2 ? sp::hull_grid_t<int64_t, 2>(E, M) : sp::hull_grid_t<int64_t, 1>(E, M);
-  return k2 ? sp::hull_grid_t<int32_t, 2>(E, M) : sp::hull_grid_t<int32_t, 1>(E, M);
+    return k2 ? sp::hull_grid_t<int64_t, 2, int>(E) : sp::hull_grid_t<int64_t, 1, int>(E);
+  return k2 ? sp::hull_grid_t<int32_t, 2, int>(E) : sp::hull_grid_t<int32_t, 1, int>(E);
 }
 
 size_t sp_hull_slot_bytes(int N, int M) { return sp::hull_slot_bytes(N, M); }
@@ -621,10 +658,11 @@ size_t sp_hull_pool_bytes(int M) { return sp::hull_pool_bytes(M); }
 
 cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
                            int32_t* npos, int64_t* cost, int64_t* cbb, int32_t* fpos,
-                           int32_t* fn, uint8_t* ws, int32_t* fb, uint8_t* pool,
+                           int32_t* fn, uint8_t* ws, int32_t* fb, int32_t* wide, uint8_t* pool,
                            uint8_t* slots, int grid, cudaStream_t st) {
   sp::HullParams p;
-  p.gring = reinterpret_cast<int2*>(pool);
+  p.gring = pool;
+  p.wide = wide;
   p.w = weights;
   p.E = E;
   p.N = N;
@@ -639,14 +677,13 @@ cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, 
   p.fb = fb;
   p.slots = slots;
   p.slot = sp::hull_slot_bytes(N, M);
-  const size_t dyn = sp::hull_smem_bytes(M);
   const bool k2 = sp::hull_K(M) == 2;
   if (wtype == SP_W_COUNTS_I64) {
-    if (k2) sp::dp_hull_kernel<int64_t, 2><<<grid, 32, dyn, st>>>(p);
-    else sp::dp_hull_kernel<int64_t, 1><<<grid, 32, dyn, st>>>(p);
+    if (k2) sp::hull_launch_t<int64_t, 2>(p, grid, st);
+    else sp::hull_launch_t<int64_t, 1>(p, grid, st);
   } else {
-    if (k2) sp::dp_hull_kernel<int32_t, 2><<<grid, 32, dyn, st>>>(p);
-    else sp::dp_hull_kernel<int32_t, 1><<<grid, 32, dyn, st>>>(p);
+    if (k2) sp::hull_launch_t<int32_t, 2>(p, grid, st);
+    else sp::hull_launch_t<int32_t, 1>(p, grid, st);
   }
   return cudaGetLastError();
 }

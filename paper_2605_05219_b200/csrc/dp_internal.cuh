@@ -10,13 +10,16 @@
 #define SP_WS_FB_COUNT_OFF 192    // unsigned: entries handed from the hull kernel to the D&C
 #define SP_WS_ENTRY_CTR_OFF 200   // unsigned: next entry for the hull kernel's warps
 #define SP_WS_POOL_OFF 208        // uint64: occupancy mask of the hull kernel's overflow rings
+#define SP_WS_WIDE_COUNT_OFF 216  // unsigned: entries listed for the int64 hull instantiation
+#define SP_WS_WIDE_CTR_OFF 220    // unsigned: next listed entry for the int64 instantiation
 
-// Workspace after the head:  fallback list int32[E] | overflow-ring pool | hull slots | D&C slots
+// Workspace after the head:  fallback list int32[E] | int64-path list int32[E] | overflow-ring pool
+// | hull slots | D&C slots
 // (each 256-B aligned)
 int sp_hull_grid(int E, int N, int M, int wtype);
 size_t sp_hull_slot_bytes(int N, int M);
 size_t sp_hull_pool_bytes(int M);
 cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
                            int32_t* npos, int64_t* cost, int64_t* cbb, int32_t* fpos,
-                           int32_t* fn, uint8_t* ws, int32_t* fb, uint8_t* pool,
+                           int32_t* fn, uint8_t* ws, int32_t* fb, int32_t* wide, uint8_t* pool,
                            uint8_t* slots, int grid, cudaStream_t st);

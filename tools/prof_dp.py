@@ -17,8 +17,15 @@ ap.add_argument("--M", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--lcp", action="store_true")
 ap.add_argument("--plus1", action="store_true", help="add 1 to every bin (full support, K = N)")
+ap.add_argument("--dense-n", type=int, nargs=2, default=None, help="draws per entry (lo hi)")
+ap.add_argument("--no-hull", action="store_true", help="D&C kernel only (SP_NO_HULL)")
 a = ap.parse_args()
 cfg = wl.scaled(wl.CONFIGS[a.workload], a.entries)
+if a.dense_n:
+    import dataclasses
+    cfg = dataclasses.replace(cfg, dense_n=tuple(a.dense_n))
+if a.no_hull:
+    os.environ["SP_NO_HULL"] = "1"
 M = a.M or cfg.M
 dev = torch.device("cuda:0")
 H = wl.make_dense_hist(cfg, seed=0, device=dev) if cfg.dense_n else wl.uniform_hist(a.entries, cfg.N, dev)

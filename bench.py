@@ -26,7 +26,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DP cells/s (entries*N*M)"
-TRAFFIC_JSON = "r01b_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
+TRAFFIC_JSON = "r01c_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
 UNIT = "cells/s"
 
 
@@ -455,7 +455,7 @@ def run_ours(args):
                               "eval": eval_ms / K},
         "roofline": {"bound": "alu", "kernel": "dp_hull_kernel", "achieved": achieved,
                      "peak": peak, "unit": "Gupd/s", "frac": achieved / peak,
-                     "traffic": traffic.get("dp_hull_kernel<int, 2>", {}).get("traffic_bytes"),
+                     "traffic": traffic.get("dp_hull_kernel<int, 2, int>", {}).get("traffic_bytes"),
                      "work": f"{updates} hull updates per launch = {stats['hull_event_rows']} "
                              f"support rows x M (support rows = {stats['hull_event_rows'] / max(1, stats['entries_hull']) / N:.3f} "
                              f"of N per entry; zero-count rows are exact no-ops); "

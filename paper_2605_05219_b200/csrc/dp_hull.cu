@@ -305,6 +305,9 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       VT Ec = 0;
       const int nev = __popc(evmask);
       if (chain_in && lane < nev) Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
+#ifdef SP_HULL_UNROLL2
+#pragma unroll 2
+#endif
       for (int q = 0; evmask; ++q) {
         const int i = __ffs(evmask) - 1;
         evmask &= evmask - 1;

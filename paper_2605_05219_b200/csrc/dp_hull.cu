@@ -39,6 +39,7 @@
 // row <= j by a warp-cooperative 32-way search.  Outputs per entry: V_m = T_N + e_m(N) for every
 // m (cost_by_budget), the rule-B backtrack (positions, count), the f3 frontier.
 #include <climits>
+#include <type_traits>
 
 #include "common.cuh"
 #include "dp_internal.cuh"
@@ -95,8 +96,8 @@ struct HullParams {
   int E, N, M;
   int32_t* pos;
   int32_t* npos;
-  int64_t* cost;
-  int64_t* cbb;
+  void* cost;       // int64 [E] (count weights) or double [E] (fp64 weights)
+  void* cbb;        // same type, [E][M+1], or NULL
   int32_t* fpos;
   int32_t* fn;
   uint8_t* ws;      // workspace head (stats + counters)
@@ -225,6 +226,57 @@ struct SRing<long long, C0, C1> {
   static constexpr size_t bytes() { return (size_t)(C0 + C1) * 384; }
 };
 
+template <int C0, int C1>
+struct SRing<double, C0, C1> {
+  uint32_t bb, sb;   // as SRing<long long>: double intercepts + 8 lane, s + 4 lane
+  __device__ __forceinline__ uint32_t q(int k, int pos) const {
+    return (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
+  }
+  __device__ __forceinline__ Line<double> ld(int k, int pos) const {
+    const uint32_t x = q(k, pos);
+    Line<double> v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v.b) : "r"((x << 8) + bb + (k ? C0 * 256u : 0u)));
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.s) : "r"((x << 7) + sb + (k ? C0 * 128u : 0u)));
+    return v;
+  }
+  __device__ __forceinline__ void st(int k, int pos, Line<double> v) const {
+    const uint32_t x = q(k, pos);
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"((x << 8) + bb + (k ? C0 * 256u : 0u)), "d"(v.b)
+                 : "memory");
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"((x << 7) + sb + (k ? C0 * 128u : 0u)), "r"(v.s)
+                 : "memory");
+  }
+  static constexpr int cap(int k) { return k ? C1 : C0; }
+};
+
+// double-double sums for the fp64 path (prefix sums rounded once, T_N, the definitional cost)
+struct hdd {
+  double hi, lo;
+};
+__device__ __forceinline__ hdd hdd_add(hdd a, hdd b) {
+  const double s = a.hi + b.hi, bb = s - a.hi;
+  double err = (a.hi - (s - bb)) + (b.hi - bb);
+  err += a.lo + b.lo;
+  const double h = s + err;
+  return hdd{h, err - (h - s)};
+}
+__device__ __forceinline__ hdd hdd_prod(double a, double b) {
+  const double p = a * b;
+  return hdd{p, fma(a, b, -p)};
+}
+__device__ __forceinline__ hdd hdd_shfl_up(hdd v, int o) {
+  return hdd{__shfl_up_sync(FULL, v.hi, o), __shfl_up_sync(FULL, v.lo, o)};
+}
+__device__ __forceinline__ hdd hdd_shfl(hdd v, int l) {
+  return hdd{__shfl_sync(FULL, v.hi, l), __shfl_sync(FULL, v.lo, l)};
+}
+__device__ __forceinline__ hdd hdd_warp_sum(hdd v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    v = hdd_add(v, hdd{__shfl_xor_sync(FULL, v.hi, o), __shfl_xor_sync(FULL, v.lo, o)});
+  return v;
+}
+
 template <typename VT, int C>
 struct GRing {
   Line<VT>* base;   // one ring of the global pool
@@ -245,12 +297,21 @@ template <typename VT>
 __device__ __forceinline__ bool pop_test(int as, VT ab, int ks, VT kb) {
   return (long long)as * (long long)kb <= (long long)ab * (long long)ks;
 }
+// fp64 weights: the same test in double (reading R10: a misjudged near-collinear triple moves a
+// value by rounding only, so the placement stays optimal to ~M eps relative)
+template <>
+__device__ __forceinline__ bool pop_test<double>(int as, double ab, int ks, double kb) {
+  return (double)as * kb <= ab * (double)ks;
+}
 
 // a4 for one entry: all layers in lockstep, one support row per step.  Returns true when a ring
 // overflowed (the entry's results are then invalid).
+template <typename VT>
+using HullCT = typename std::conditional<std::is_same<VT, double>::value, double, long long>::type;
+
 template <typename WT, typename VT, int K, class RING>
 __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
-                                        long long TN, VT nV, const RING rg, uint32_t* logs,
+                                        HullCT<VT> TN, VT nV, const RING rg, uint32_t* logs,
                                         int32_t* logn, VT* ebuf0, VT* ebuf1,
                                         unsigned& pops_e, unsigned& ev_e) {
   const int lane = lane_id();
@@ -286,20 +347,35 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       B0[k] = F0[k] = Line<VT>{0, 1};
     }
     VT carry = 0, Pm1 = 0;
+    hdd carry_dd{0.0, 0.0};
     int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
     for (int jb = 0; jb < N; jb += 32) {
       const int jr = jb + 1 + lane;
       const VT craw = jr <= N ? (VT)we[jr] : (VT)0;
       unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
       if (evmask == 0) continue;                          // 32 zero rows: nothing changes
-      VT cnt32 = craw;
+      VT Pc;
+      if constexpr (std::is_same<VT, double>::value) {
+        // P_j from a double-double scan, rounded once (reading R10)
+        hdd inc{craw, 0.0};
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const VT y = __shfl_up_sync(FULL, cnt32, o);
-        if (lane >= o) cnt32 += y;
+        for (int o = 1; o < 32; o <<= 1) {
+          const hdd y = hdd_shfl_up(inc, o);
+          if (lane >= o) inc = hdd_add(inc, y);
+        }
+        const hdd full = hdd_add(carry_dd, inc);
+        Pc = full.hi + full.lo;
+        carry_dd = hdd_shfl(full, 31);
+      } else {
+        VT cnt32 = craw;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const VT y = __shfl_up_sync(FULL, cnt32, o);
+          if (lane >= o) cnt32 += y;
+        }
+        Pc = carry + cnt32;
+        carry = __shfl_sync(FULL, Pc, 31);
       }
-      const VT Pc = carry + cnt32;
-      carry = __shfl_sync(FULL, Pc, 31);
       // previous pass's top layer at the support rows: e(j-1) of support row number t is its
       // value at support row t-1 (constant over zero rows), 0 before the first
       VT Ec = 0;
@@ -456,9 +532,9 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         if (!act[k]) continue;
         const int mk = ps * L + 32 * k + lane + 1;
         logn[ps * L + 32 * k + lane] = cnt[k];
-        const long long V = TN + (long long)eo[k];   // V_m = T_N + e_m(N)
-        if (p.cbb) p.cbb[(int64_t)e * (M + 1) + mk] = V;
-        if (mk == M) p.cost[e] = V;
+        const HullCT<VT> V = TN + (HullCT<VT>)eo[k];   // V_m = T_N + e_m(N)
+        if (p.cbb) reinterpret_cast<HullCT<VT>*>(p.cbb)[(int64_t)e * (M + 1) + mk] = V;
+        if (mk == M) reinterpret_cast<HullCT<VT>*>(p.cost)[e] = V;
       }
     }
     __syncwarp();   // chained e-row and logs visible to the whole warp
@@ -470,14 +546,15 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
 // for the VT = long long instantiation (launched next, same slots); the rest for the D&C kernel.
 template <typename WT, int K, typename VT>
 __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
-  constexpr bool WIDE = sizeof(VT) == 8;
+  constexpr bool F64 = std::is_same<VT, double>::value;
+  constexpr bool WIDE = std::is_same<VT, long long>::value;
   const int lane = threadIdx.x;
 #ifndef SP_HULL_RING6
   constexpr int NPOS = HC0 + (K == 2 ? HC1 : 0);   // ring positions of this warp
-  __shared__ __align__(16) uint8_t sring[NPOS * (WIDE ? 384 : 256)];
+  __shared__ __align__(16) uint8_t sring[NPOS * (sizeof(VT) == 8 ? 384 : 256)];
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
   SRing<VT, HC0, HC1> srg;
-  if constexpr (WIDE) {
+  if constexpr (sizeof(VT) == 8) {
     srg.bb = sbase + 8u * (uint32_t)lane;
     srg.sb = sbase + (uint32_t)NPOS * 256u + 4u * (uint32_t)lane;
   } else {
@@ -509,38 +586,66 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
     const WT* we = reinterpret_cast<const WT*>(p.w) + (int64_t)e * (N + 1);
 
     // ---- a3 pre-pass: n = P_N, T_N, first non-zero bin, sign / size guards ---------------
-    long long n = 0, TN = 0;
-    int bad = 0, tfirst = INT_MAX;
-    for (int t = lane + 1; t <= N; t += 32) {
-      const long long c = (long long)we[t];
-      bad |= (c < 0) | (c >= (1ll << 40));
-      if (!bad) {
-        n += c;
-        TN += (long long)t * c;
+    using CT = HullCT<VT>;
+    CT TN;
+    VT nV;
+    int tfirst = INT_MAX;
+    if constexpr (F64) {
+      hdd nd{0.0, 0.0}, td{0.0, 0.0};
+      int bad = 0;
+      for (int t = lane + 1; t <= N; t += 32) {
+        const double c = (double)we[t];
+        bad |= !(c >= 0.0) || isinf(c);
+        nd = hdd_add(nd, hdd{c, 0.0});
+        td = hdd_add(td, hdd_prod((double)t, c));
+        if (c > 0.0 && t < tfirst) tfirst = t;
       }
-      if (c > 0 && t < tfirst) tfirst = t;
-    }
-    bad = __any_sync(FULL, bad);
-    n = warp_sum(n);
-    TN = warp_sum(TN);
+      bad = __any_sync(FULL, bad);
+      nd = hdd_warp_sum(nd);
+      td = hdd_warp_sum(td);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tfirst = min(tfirst, __shfl_xor_sync(FULL, tfirst, o));
-    // int32 path: 2 n N < 2^31 (the D&C kernel's "narrow" condition: every intercept, candidate
-    // and difference exact in int32); int64 path: n N < 2^46 (differences < 2^46, cross products
-    // < 2^62); otherwise (or negative counts) the D&C kernel
-    const bool narrow = !bad && n < (1ll << 30) / N;
-    const bool wide_ok = !bad && n < (1ll << 46) / N;
-    if (!WIDE && !narrow) {
-      if (lane == 0) {
-        if (wide_ok) p.wide[atomicAdd(wide_n, 1u)] = e;
-        else p.fb[atomicAdd(fb_n, 1u)] = e;
+      for (int o = 16; o > 0; o >>= 1) tfirst = min(tfirst, __shfl_xor_sync(FULL, tfirst, o));
+      if (bad) {   // negative / non-finite weights: the D&C kernel reports the entry
+        if (lane == 0) p.fb[atomicAdd(fb_n, 1u)] = e;
+        continue;
       }
-      continue;
+      TN = td.hi + td.lo;
+      nV = nd.hi + nd.lo;
+    } else {
+      long long n = 0, tn = 0;
+      int bad = 0;
+      for (int t = lane + 1; t <= N; t += 32) {
+        const long long c = (long long)we[t];
+        bad |= (c < 0) | (c >= (1ll << 40));
+        if (!bad) {
+          n += c;
+          tn += (long long)t * c;
+        }
+        if (c > 0 && t < tfirst) tfirst = t;
+      }
+      bad = __any_sync(FULL, bad);
+      n = warp_sum(n);
+      tn = warp_sum(tn);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tfirst = min(tfirst, __shfl_xor_sync(FULL, tfirst, o));
+      // int32 path: 2 n N < 2^31 (the D&C kernel's "narrow" condition: every intercept,
+      // candidate and difference exact in int32); int64 path: n N < 2^46 (differences < 2^46,
+      // cross products < 2^62); otherwise (or negative counts) the D&C kernel
+      const bool narrow = !bad && n < (1ll << 30) / N;
+      const bool wide_ok = !bad && n < (1ll << 46) / N;
+      if (!WIDE && !narrow) {
+        if (lane == 0) {
+          if (wide_ok) p.wide[atomicAdd(wide_n, 1u)] = e;
+          else p.fb[atomicAdd(fb_n, 1u)] = e;
+        }
+        continue;
+      }
+      TN = tn;
+      nV = (VT)n;   // P_N; n N < 2^30 (int) / 2^46 (long long), so n (j - s) fits VT
     }
     if (lane == 0) {
-      if (p.cbb) p.cbb[(int64_t)e * (M + 1)] = TN;   // V_0 = T_N
+      if (p.cbb) reinterpret_cast<CT*>(p.cbb)[(int64_t)e * (M + 1)] = TN;   // V_0 = T_N
     }
-    const VT nV = (VT)n;   // P_N; n N < 2^30 (int) / 2^46 (long long), so n (j - s) fits VT
 
     // ---- a4: all layers in lockstep, one support row per step --------------------------------
     unsigned pops_e = 0, ev_e = 0;
@@ -593,6 +698,20 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
         p.npos[e] = k;
       }
       for (int q = k + lane; q < M; q += 32) out[q] = 0;
+      if constexpr (F64) {
+        // a7: report the definitional cost sum_t w_t (t - l(t)) of the returned placement in
+        // double-double (reading R10; the DP's own V_M carries ~M N eps P_N absolute rounding)
+        __syncwarp();
+        hdd acc{0.0, 0.0};
+        int ptr = 0;   // positions <= t (t increases per lane)
+        for (int t = lane + 1; t <= N; t += 32) {
+          while (ptr < k && out[ptr] <= t) ++ptr;
+          const double wt = (double)we[t];
+          if (wt != 0.0) acc = hdd_add(acc, hdd_prod(wt, (double)(t - (ptr ? out[ptr - 1] : 0))));
+        }
+        acc = hdd_warp_sum(acc);
+        if (lane == 0) reinterpret_cast<double*>(p.cost)[e] = acc.hi + acc.lo;
+      }
     }
     if (p.fpos) {
       for (int mb = lane + 1; mb <= M; mb += 32) {
@@ -621,7 +740,8 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   if (lane == 0) {
     atomicAdd(&stats->hull_pops, pops);
     atomicAdd(&stats->entries_hull, (unsigned long long)done_entries);
-    atomicAdd(WIDE ? &stats->entries_i64 : &stats->entries_i32, (unsigned long long)done_entries);
+    atomicAdd(F64 ? &stats->entries_f64 : WIDE ? &stats->entries_i64 : &stats->entries_i32,
+              (unsigned long long)done_entries);
     atomicAdd(&stats->hull_event_rows, events);
   }
 }
@@ -640,9 +760,13 @@ static int hull_grid_t(int E) {
 
 template <typename WT, int K>
 static void hull_launch_t(const HullParams& p, int gn, cudaStream_t st) {
-  dp_hull_kernel<WT, K, int><<<gn, 32, 0, st>>>(p);
-  // the int64 instantiation on the listed entries (its warps exit at once when the list is empty)
-  dp_hull_kernel<WT, K, long long><<<hull_grid_t<WT, K, long long>(p.E), 32, 0, st>>>(p);
+  if constexpr (std::is_same<WT, double>::value) {
+    dp_hull_kernel<double, K, double><<<gn, 32, 0, st>>>(p);
+  } else {
+    dp_hull_kernel<WT, K, int><<<gn, 32, 0, st>>>(p);
+    // the int64 instantiation on the listed entries (its warps exit at once if the list is empty)
+    dp_hull_kernel<WT, K, long long><<<hull_grid_t<WT, K, long long>(p.E), 32, 0, st>>>(p);
+  }
 }
 
 }  // namespace sp
@@ -651,6 +775,8 @@ static void hull_launch_t(const HullParams& p, int gn, cudaStream_t st) {
 int sp_hull_grid(int E, int N, int M, int wtype) {
   (void)N;
   const bool k2 = sp::hull_K(M) == 2;
+  if (wtype == SP_W_PROB_F64)
+    return k2 ? sp::hull_grid_t<double, 2, double>(E) : sp::hull_grid_t<double, 1, double>(E);
   if (wtype == SP_W_COUNTS_I64)
     return k2 ? sp::hull_grid_t<int64_t, 2, int>(E) : sp::hull_grid_t<int64_t, 1, int>(E);
   return k2 ? sp::hull_grid_t<int32_t, 2, int>(E) : sp::hull_grid_t<int32_t, 1, int>(E);
@@ -660,7 +786,7 @@ size_t sp_hull_slot_bytes(int N, int M) { return sp::hull_slot_bytes(N, M); }
 size_t sp_hull_pool_bytes(int M) { return sp::hull_pool_bytes(M); }
 
 cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
-                           int32_t* npos, int64_t* cost, int64_t* cbb, int32_t* fpos,
+                           int32_t* npos, void* cost, void* cbb, int32_t* fpos,
                            int32_t* fn, uint8_t* ws, int32_t* fb, int32_t* wide, uint8_t* pool,
                            uint8_t* slots, int grid, cudaStream_t st) {
   sp::HullParams p;
@@ -681,7 +807,10 @@ cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, 
   p.slots = slots;
   p.slot = sp::hull_slot_bytes(N, M);
   const bool k2 = sp::hull_K(M) == 2;
-  if (wtype == SP_W_COUNTS_I64) {
+  if (wtype == SP_W_PROB_F64) {
+    if (k2) sp::hull_launch_t<double, 2>(p, grid, st);
+    else sp::hull_launch_t<double, 1>(p, grid, st);
+  } else if (wtype == SP_W_COUNTS_I64) {
     if (k2) sp::hull_launch_t<int64_t, 2>(p, grid, st);
     else sp::hull_launch_t<int64_t, 1>(p, grid, st);
   } else {

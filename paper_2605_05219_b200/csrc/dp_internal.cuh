@@ -20,6 +20,6 @@ int sp_hull_grid(int E, int N, int M, int wtype);
 size_t sp_hull_slot_bytes(int N, int M);
 size_t sp_hull_pool_bytes(int M);
 cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
-                           int32_t* npos, int64_t* cost, int64_t* cbb, int32_t* fpos,
+                           int32_t* npos, void* cost, void* cbb, int32_t* fpos,
                            int32_t* fn, uint8_t* ws, int32_t* fb, int32_t* wide, uint8_t* pool,
                            uint8_t* slots, int grid, cudaStream_t st);

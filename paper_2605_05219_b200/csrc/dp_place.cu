@@ -1552,8 +1552,9 @@ extern "C" size_t sp_place_checkpoints_workspace_bytes(int32_t n_entries, int32_
   if (n_entries == 0) return 0;
   size_t hull = 0;
   if (M > 0) {
-    const int gh = std::max(sp_hull_grid(n_entries, N, M, SP_W_COUNTS_I32),
-                            sp_hull_grid(n_entries, N, M, SP_W_COUNTS_I64));
+    const int gh = std::max(std::max(sp_hull_grid(n_entries, N, M, SP_W_COUNTS_I32),
+                                     sp_hull_grid(n_entries, N, M, SP_W_COUNTS_I64)),
+                            sp_hull_grid(n_entries, N, M, SP_W_PROB_F64));
     hull = 2 * sp::align256(4 * (size_t)n_entries) + sp::align256(sp_hull_pool_bytes(M)) +
            (size_t)gh * sp_hull_slot_bytes(N, M);
   }
@@ -1602,9 +1603,9 @@ static sp_status place_impl(const void* weights, sp_weight_type wtype,
   if (wtype == SP_W_COUNTS_I32) grid = dp_grid_t<int32_t>(n_entries, N);
   else if (wtype == SP_W_COUNTS_I64) grid = dp_grid_t<int64_t>(n_entries, N);
   else grid = dp_grid_t<double>(n_entries, N);
-  // count weights: the hull kernel (dp_hull.cu) solves every entry it can on the exact-int32
-  // path and lists the rest (int64 range, negative counts, ring overflow) for the D&C kernel
-  const bool use_hull = wtype != SP_W_PROB_F64 && M > 0 && !getenv("SP_NO_HULL");
+  // the hull kernels (dp_hull.cu: int32 / int64 for counts, double for fp64 weights) solve every
+  // entry they can and list the rest (bad weights, nN >= 2^46, ring overflow) for the D&C kernel
+  const bool use_hull = M > 0 && !getenv("SP_NO_HULL");
   const int hgrid = use_hull ? sp_hull_grid(n_entries, N, M, wtype) : 0;
   const size_t fb_off = SP_WS_STATS_BYTES;
   const size_t wide_off = fb_off + (use_hull ? sp::align256(4 * (size_t)n_entries) : 0);
@@ -1636,8 +1637,8 @@ static sp_status place_impl(const void* weights, sp_weight_type wtype,
   if (cudaMemsetAsync(workspace, 0, SP_WS_STATS_BYTES, st) != cudaSuccess) SP_CHECK_LAUNCH();
   if (use_hull) {
     const cudaError_t he = sp_hull_launch(
-        weights, wtype, n_entries, N, M, positions, n_positions, (int64_t*)cost,
-        (int64_t*)cost_by_budget, fpos, fn, (uint8_t*)workspace,
+        weights, wtype, n_entries, N, M, positions, n_positions, cost, cost_by_budget, fpos, fn,
+        (uint8_t*)workspace,
         reinterpret_cast<int32_t*>((uint8_t*)workspace + fb_off),
         reinterpret_cast<int32_t*>((uint8_t*)workspace + wide_off), (uint8_t*)workspace + pool_off,
         (uint8_t*)workspace + hull_off, hgrid, st);

@@ -191,3 +191,26 @@ def test_hull_int64_path_large_counts(dev):
     for k in ("pos", "npos", "cost", "cbb"):
         assert (a[k] == b[k]).all(), k
     check(H, 64, a, rows=[0, 7, 50])
+
+
+def test_hull_f64_path_vs_exact(dev):
+    """fp64 weights (a7) on the double hull instantiation: W5-shaped rows scaled to
+    probabilities (w = c / n, non-dyadic n) -- the returned placement's definitional cost equals
+    the exact optimum V_int / n to 1e-12 relative (reading R10), V_0..V_M track it, and the D&C
+    kernel agrees."""
+    cfg = wl.scaled(wl.CONFIGS["W5"], 24)
+    H = wl.make_dense_hist(cfg, seed=11).numpy().astype(np.int64)
+    W = H / H.sum(1, keepdims=True)
+    r = place(W, 64, dev, dtype=torch.float64)
+    assert r["stats"]["entries_f64"] == 24 and r["stats"]["entries_hull"] >= 20
+    ri = place(H, 64, dev)                      # exact integer optimum
+    n = H.sum(1).astype(np.float64)
+    exact = ri["cost"] / n
+    assert (np.abs(r["cost"] - exact) <= 1e-12 * exact).all()
+    assert (np.abs(r["cbb"] - ri["cbb"] / n[:, None]) <= 1e-10 * (ri["cbb"] / n[:, None]) + 1e-15).all()
+    os.environ["SP_NO_HULL"] = "1"
+    try:
+        d = place(W, 64, dev, dtype=torch.float64)
+    finally:
+        del os.environ["SP_NO_HULL"]
+    assert (np.abs(d["cost"] - r["cost"]) <= 1e-12 * exact).all()

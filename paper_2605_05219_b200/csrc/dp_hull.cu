@@ -55,6 +55,14 @@ namespace sp {
 #define SP_HULL_CAP1 32
 #endif
 constexpr int HC0 = SP_HULL_CAP0, HC1 = SP_HULL_CAP1;
+// the int64 instantiation serves accumulated (large-count) rows, whose hulls are larger
+#ifndef SP_HULL_WCAP0
+#define SP_HULL_WCAP0 128
+#endif
+#ifndef SP_HULL_WCAP1
+#define SP_HULL_WCAP1 64
+#endif
+constexpr int HW0 = SP_HULL_WCAP0, HW1 = SP_HULL_WCAP1;
 // An entry whose hull outgrows a shared ring is re-run at once by the same warp on a global
 // overflow ring of HCG lines per layer, taken from a pool of HPOOL rings (a 64-bit occupancy mask
 // in the workspace head); only if that overflows too (or the pool is busy) does it go to the
@@ -554,10 +562,11 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   constexpr bool WIDE = std::is_same<VT, long long>::value;
   const int lane = threadIdx.x;
 #ifndef SP_HULL_RING6
-  constexpr int NPOS = HC0 + (K == 2 ? HC1 : 0);   // ring positions of this warp
-  __shared__ __align__(16) uint8_t sring[NPOS * (sizeof(VT) == 8 ? 384 : 256)];
+  constexpr int C0 = WIDE ? HW0 : HC0, C1 = WIDE ? HW1 : HC1;
+  constexpr int NPOS = C0 + (K == 2 ? C1 : 0);   // ring positions of this warp
+  extern __shared__ __align__(16) uint8_t sring[];   // NPOS * (256 | 384) bytes (ring_bytes)
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
-  SRing<VT, HC0, HC1> srg;
+  SRing<VT, C0, C1> srg;
   if constexpr (sizeof(VT) == 8) {
     srg.bb = sbase + 8u * (uint32_t)lane;
     srg.sb = sbase + (uint32_t)NPOS * 256u + 4u * (uint32_t)lane;
@@ -750,12 +759,22 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   }
 }
 
+template <int K, typename VT>
+static constexpr size_t ring_bytes() {
+  constexpr bool W = std::is_same<VT, long long>::value;
+  constexpr int NPOS = (W ? HW0 : HC0) + (K == 2 ? (W ? HW1 : HC1) : 0);
+  return (size_t)NPOS * (sizeof(VT) == 8 ? 384 : 256);
+}
+
 template <typename WT, int K, typename VT>
 static int hull_grid_t(int E) {
   int dev = 0, sms = 148, occ = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_hull_kernel<WT, K, VT>, 32, 0);
+  constexpr size_t dyn = ring_bytes<K, VT>();
+  cudaFuncSetAttribute(dp_hull_kernel<WT, K, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)dyn);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_hull_kernel<WT, K, VT>, 32, dyn);
   if (occ < 1) occ = 1;
   long g = (long)sms * occ;
   if (g > E) g = E;
@@ -765,11 +784,12 @@ static int hull_grid_t(int E) {
 template <typename WT, int K>
 static void hull_launch_t(const HullParams& p, int gn, cudaStream_t st) {
   if constexpr (std::is_same<WT, double>::value) {
-    dp_hull_kernel<double, K, double><<<gn, 32, 0, st>>>(p);
+    dp_hull_kernel<double, K, double><<<gn, 32, ring_bytes<K, double>(), st>>>(p);
   } else {
-    dp_hull_kernel<WT, K, int><<<gn, 32, 0, st>>>(p);
+    dp_hull_kernel<WT, K, int><<<gn, 32, ring_bytes<K, int>(), st>>>(p);
     // the int64 instantiation on the listed entries (its warps exit at once if the list is empty)
-    dp_hull_kernel<WT, K, long long><<<hull_grid_t<WT, K, long long>(p.E), 32, 0, st>>>(p);
+    dp_hull_kernel<WT, K, long long><<<hull_grid_t<WT, K, long long>(p.E), 32,
+                                       ring_bytes<K, long long>(), st>>>(p);
   }
 }
 

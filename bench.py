@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--merge", default="sparse", choices=["sparse", "allreduce"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="entry blocks of the pipelined e2e")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle wall time")
     return ap.parse_args()
@@ -397,13 +398,53 @@ def run_ours(args):
             o_bcost.copy_(bcost, non_blocking=True)
             o_cbb.copy_(cbb, non_blocking=True)
 
-        e2e_step()
+        run_e2e = e2e_step
+        if world == 1 and args.e2e_chunks > 1:
+            # pipelined through the same ABI calls: the request tokens of entry block c+1 cross
+            # PCIe (copy stream) while blocks <= c run LCP -> DP -> evaluation (compute stream);
+            # requests are grouped by entry, so a block's requests and tokens are contiguous
+            C = args.e2e_chunks
+            h_ent_np = h_ent.numpy()
+            eb = [E_own * c // C for c in range(C + 1)]
+            rb = [int(np.searchsorted(h_ent_np, x, side="left")) for x in eb]
+            tb = [int(h_off[r]) for r in rb]
+            cstream = torch.cuda.Stream(dev)
+            cev = [ev() for _ in range(C)]
+
+            def e2e_pipelined():
+                req_off.copy_(h_off, non_blocking=True)
+                req_entry.copy_(h_ent, non_blocking=True)
+                cstream.wait_stream(stream)
+                with torch.cuda.stream(cstream):
+                    for c in range(C):
+                        req_tokens[tb[c]:tb[c + 1]].copy_(h_tok[tb[c]:tb[c + 1]], non_blocking=True)
+                        cev[c].record(cstream)
+                for c in range(C):
+                    stream.wait_event(cev[c])
+                    r0, r1, a0, a1 = rb[c], rb[c + 1], eb[c], eb[c + 1]
+                    if r1 > r0:
+                        sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], req_tokens,
+                                        req_off[r0:r1 + 1], req_entry[r0:r1], N, hist=hist,
+                                        lcp_out=lcp[r0:r1], n_entries=E_tot, stream=stream)
+                    sp.place_checkpoints(hist[a0:a1], M, positions=positions[a0:a1],
+                                         n_positions=npos[a0:a1], cost=cost[a0:a1],
+                                         cost_by_budget=cbb[a0:a1], workspace=ws, stream=stream)
+                    sp.expected_recompute(hist[a0:a1], bpos, bnpos, broadcast=True,
+                                          cost=bcost[a0:a1], worst=bworst[a0:a1], stream=stream)
+                    o_pos[a0:a1].copy_(positions[a0:a1], non_blocking=True)
+                    o_npos[a0:a1].copy_(npos[a0:a1], non_blocking=True)
+                    o_cost[a0:a1].copy_(cost[a0:a1], non_blocking=True)
+                    o_bcost[a0:a1].copy_(bcost[a0:a1], non_blocking=True)
+                    o_cbb[a0:a1].copy_(cbb[a0:a1], non_blocking=True)
+
+            run_e2e = e2e_pipelined
+        run_e2e()
         torch.cuda.synchronize()
         barrier()
         a, b = ev(), ev()
         a.record(stream)
         for _ in range(args.steps):
-            e2e_step()
+            run_e2e()
         b.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -413,7 +454,10 @@ def run_ours(args):
         e_ms = float(e_ms)
         e2e = {"value": E_tot * N * M * args.steps / (e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": bi * world, "d2h_bytes_per_step": bo * world,
-               "ms_per_step": e_ms / args.steps}
+               "ms_per_step": e_ms / args.steps,
+               "pipeline": (f"{args.e2e_chunks} entry blocks, H2D on a copy stream overlapped "
+                            f"with LCP/DP/eval" if world == 1 and args.e2e_chunks > 1
+                            else "serial")}
 
     # ---- numbers -------------------------------------------------------------------------
     tok_all = torch.tensor([tokens_examined, lcp_bytes], dtype=torch.float64, device=dev)

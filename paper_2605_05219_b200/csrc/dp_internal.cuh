@@ -14,12 +14,13 @@
 #define SP_WS_WIDE_CTR_OFF 220    // unsigned: next listed entry for the int64 instantiation
 
 // Workspace after the head:  fallback list int32[E] | int64-path list int32[E] | overflow-ring pool
-// | hull slots | D&C slots
+// | ordering scratch (support counts, radix sort) | hull slots | D&C slots
 // (each 256-B aligned)
 int sp_hull_grid(int E, int N, int M, int wtype);
 size_t sp_hull_slot_bytes(int N, int M);
 size_t sp_hull_pool_bytes(int M);
+size_t sp_hull_order_bytes(int E);
 cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
                            int32_t* npos, void* cost, void* cbb, int32_t* fpos,
                            int32_t* fn, uint8_t* ws, int32_t* fb, int32_t* wide, uint8_t* pool,
-                           uint8_t* slots, int grid, cudaStream_t st);
+                           uint8_t* order_ws, uint8_t* slots, int grid, cudaStream_t st);

@@ -20,6 +20,7 @@ ap.add_argument("--plus1", action="store_true", help="add 1 to every bin (full s
 ap.add_argument("--dense-n", type=int, nargs=2, default=None, help="draws per entry (lo hi)")
 ap.add_argument("--no-hull", action="store_true", help="D&C kernel only (SP_NO_HULL)")
 ap.add_argument("--f64", action="store_true", help="fp64 weights w = c / n (a7)")
+ap.add_argument("--sort-support", action="store_true", help="rows permuted by support, largest first")
 a = ap.parse_args()
 cfg = wl.scaled(wl.CONFIGS[a.workload], a.entries)
 if a.dense_n:
@@ -32,6 +33,8 @@ dev = torch.device("cuda:0")
 H = wl.make_dense_hist(cfg, seed=0, device=dev) if cfg.dense_n else wl.uniform_hist(a.entries, cfg.N, dev)
 if a.plus1:
     H[:, 1:] += 1
+if a.sort_support:
+    H = H[torch.argsort((H[:, 1:] > 0).sum(1), descending=True)].contiguous()
 if a.f64:
     H = (H.double() / H.sum(1, keepdim=True).double()).contiguous()
 ws = torch.empty(sp.place_checkpoints_workspace_bytes(a.entries, cfg.N, M), dtype=torch.uint8, device=dev)

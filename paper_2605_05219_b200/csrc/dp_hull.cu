@@ -288,6 +288,35 @@ __device__ __forceinline__ hdd hdd_warp_sum(hdd v) {
   return v;
 }
 
+// 6-byte int32 lines (intercepts int32 [pos][lane], s uint16 [pos][lane]): 25% less shared
+// memory per layer (12 instead of 9 warps/SM) for a second LDS per line; the default for the int32
+// instantiation (W5: 43.2 -> 42.0 ms; -DSP_HULL_RING8 restores int2 lines)
+template <int C0, int C1>
+struct SRing6 {
+  uint32_t bb, sb;   // shared addresses: intercept array + 4 lane, s array + 2 lane
+  __device__ __forceinline__ uint32_t q(int k, int pos) const {
+    return (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
+  }
+  __device__ __forceinline__ Line<int> ld(int k, int pos) const {
+    const uint32_t x = q(k, pos);
+    Line<int> v;
+    unsigned short sv;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.b) : "r"((x << 7) + bb + (k ? C0 * 128u : 0u)));
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sv) : "r"((x << 6) + sb + (k ? C0 * 64u : 0u)));
+    v.s = sv;
+    return v;
+  }
+  __device__ __forceinline__ void st(int k, int pos, Line<int> v) const {
+    const uint32_t x = q(k, pos);
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"((x << 7) + bb + (k ? C0 * 128u : 0u)), "r"(v.b)
+                 : "memory");
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"((x << 6) + sb + (k ? C0 * 64u : 0u)),
+                 "h"((unsigned short)v.s)
+                 : "memory");
+  }
+  static constexpr int cap(int k) { return k ? C1 : C0; }
+};
+
 template <typename VT, int C>
 struct GRing {
   Line<VT>* base;   // one ring of the global pool
@@ -564,21 +593,28 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   constexpr bool F64 = std::is_same<VT, double>::value;
   constexpr bool WIDE = std::is_same<VT, long long>::value;
   const int lane = threadIdx.x;
-#ifndef SP_HULL_RING6
   constexpr int C0 = WIDE ? HW0 : HC0, C1 = WIDE ? HW1 : HC1;
   constexpr int NPOS = C0 + (K == 2 ? C1 : 0);   // ring positions of this warp
-  extern __shared__ __align__(16) uint8_t sring[];   // NPOS * (256 | 384) bytes (ring_bytes)
+  extern __shared__ __align__(16) uint8_t sring[];   // ring_bytes<K, VT>()
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
-  SRing<VT, C0, C1> srg;
+#ifndef SP_HULL_RING8
+  using SR = typename std::conditional<std::is_same<VT, int>::value, SRing6<C0, C1>,
+                                       SRing<VT, C0, C1>>::type;
+#else
+  using SR = SRing<VT, C0, C1>;
+#endif
+  SR srg;
   if constexpr (sizeof(VT) == 8) {
     srg.bb = sbase + 8u * (uint32_t)lane;
     srg.sb = sbase + (uint32_t)NPOS * 256u + 4u * (uint32_t)lane;
   } else {
-    srg.base = sbase + 8u * (uint32_t)lane;
-  }
+#ifndef SP_HULL_RING8
+    srg.bb = sbase + 4u * (uint32_t)lane;
+    srg.sb = sbase + (uint32_t)NPOS * 128u + 2u * (uint32_t)lane;
 #else
-#error "SP_HULL_RING6 is not maintained for the generic value type"
+    srg.base = sbase + 8u * (uint32_t)lane;
 #endif
+  }
   const int N = p.N, M = p.M;
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
   unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
@@ -786,7 +822,11 @@ template <int K, typename VT>
 static constexpr size_t ring_bytes() {
   constexpr bool W = std::is_same<VT, long long>::value;
   constexpr int NPOS = (W ? HW0 : HC0) + (K == 2 ? (W ? HW1 : HC1) : 0);
+#ifndef SP_HULL_RING8
+  return (size_t)NPOS * (sizeof(VT) == 8 ? 384 : 192);
+#else
   return (size_t)NPOS * (sizeof(VT) == 8 ? 384 : 256);
+#endif
 }
 
 template <typename WT, int K, typename VT>

@@ -389,9 +389,12 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
     VT carry = 0, Pm1 = 0;
     hdd carry_dd{0.0, 0.0};
     int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
+    // the counts of the next 32-row chunk are loaded one chunk ahead (HBM latency off the path)
+    VT cnext = 1 + lane <= N ? (VT)we[1 + lane] : (VT)0;
     for (int jb = 0; jb < N; jb += 32) {
       const int jr = jb + 1 + lane;
-      const VT craw = jr <= N ? (VT)we[jr] : (VT)0;
+      const VT craw = cnext;
+      cnext = jr + 32 <= N ? (VT)we[jr + 32] : (VT)0;
       unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
       if (evmask == 0) continue;                          // 32 zero rows: nothing changes
       VT Pc;
@@ -645,6 +648,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
     if constexpr (F64) {
       hdd nd{0.0, 0.0}, td{0.0, 0.0};
       int bad = 0;
+#pragma unroll 8
       for (int t = lane + 1; t <= N; t += 32) {
         const double c = (double)we[t];
         bad |= !(c >= 0.0) || isinf(c);
@@ -666,6 +670,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
     } else {
       long long n = 0, tn = 0;
       int bad = 0;
+#pragma unroll 8
       for (int t = lane + 1; t <= N; t += 32) {
         const long long c = (long long)we[t];
         bad |= (c < 0) | (c >= (1ll << 40));
@@ -809,6 +814,7 @@ __global__ void __launch_bounds__(256) support_count_kernel(const WT* __restrict
   for (int e = blockIdx.x * 8 + warp_id(); e < E; e += nw) {
     const WT* we = w + (int64_t)e * (N + 1);
     int c = 0;
+#pragma unroll 8
     for (int t = lane + 1; t <= N; t += 32) c += __ldcs(we + t) != WT(0);
     c = warp_sum(c);
     if (lane == 0) {

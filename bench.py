@@ -515,9 +515,10 @@ def run_ours(args):
                          "traffic": traffic.get("lcp_hist_kernel", {}).get("traffic_bytes"),
                          "algorithmic_bytes": lcp_bytes_all / world},
         "dp_paths": {k: v for k, v in stats.items()},
-        # per step: lcp_hist, dp_hull<int32>, dp_hull<int64> (its list; exits at once when
-        # empty), dp_place (the D&C list; ditto), eval (+ accumulate_depths for the sparse merge)
-        "gpu_launches": K * (5 + (1 if world > 1 and args.merge == "sparse" else 0)),
+        # per step: lcp_hist, support_count (+ CUB's radix-sort kernels), dp_hull<int32>,
+        # dp_hull<int64> (its list; exits at once when empty), dp_place (the D&C list; ditto),
+        # eval (+ accumulate_depths for the sparse merge).  Counted: our kernels only.
+        "gpu_launches": K * (6 + (1 if world > 1 and args.merge == "sparse" else 0)),
         "clocks": clk,
         "e2e": e2e,
     }

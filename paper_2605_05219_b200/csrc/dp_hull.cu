@@ -90,8 +90,14 @@ __host__ __device__ __forceinline__ int hull_layers_padded(int M) {
   return hull_passes(M) * 32 * hull_K(M);
 }
 // slot: argmin logs uint32 [layer][N+1] | log counts int32 [layer] | e-row buffers 2 x VT[N+1]
+// argmin-log capacity per layer: opt changes at a fraction of the support rows (W5: ~500 of
+// ~5170); an entry that fills a log goes to the D&C kernel (never on W5)
+__host__ __device__ __forceinline__ int hull_log_cap(int N) {
+  const int c = (N + 1 + 7) / 8;
+  return c < 1024 ? (N + 1 < 1024 ? N + 1 : 1024) : c;
+}
 __host__ __device__ __forceinline__ size_t hull_log_bytes(int N, int M) {
-  return hull_align((size_t)hull_layers_padded(M) * (N + 1) * 4);
+  return hull_align((size_t)hull_layers_padded(M) * hull_log_cap(N) * 4);
 }
 __host__ __device__ __forceinline__ size_t hull_cnt_bytes(int M) {
   return hull_align((size_t)hull_layers_padded(M) * 4);
@@ -117,6 +123,7 @@ struct HullParams {
   void* gring;      // HPOOL global overflow rings, [ring][slot][HCG][32] lines (16 B each)
   int32_t* wide;    // entries for the int64 instantiation
   const int32_t* order;   // processing order of the entries (largest support first), or NULL
+  int logcap;             // argmin-log entries usable per layer (hull_log_cap(N); tests lower it)
 };
 
 __host__ __device__ __forceinline__ size_t hull_pool_bytes(int M) {
@@ -353,9 +360,11 @@ template <typename WT, typename VT, int K, class RING>
 __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
                                         HullCT<VT> TN, VT nV, const RING rg, uint32_t* logs,
                                         int32_t* logn, VT* ebuf0, VT* ebuf1,
-                                        unsigned& pops_e, unsigned& ev_e) {
+                                        unsigned& pops_e, unsigned& ev_e, bool& logfull) {
   const int lane = lane_id();
   const int N = p.N, M = p.M;
+  const int LC = p.logcap;   // <= hull_log_cap(N), the allocated stride
+  logfull = false;
   constexpr int L = 32 * K;
   const int passes = (M + L - 1) / L;
   bool ovf = false;
@@ -382,7 +391,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       eo[k] = 0;   // e_m(0) = 0 (reading R1)
       op[k] = 1;   // opt_m(1) = 1 whatever the row type: logged up front
       cnt[k] = 1;
-      lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * (N + 1);
+      lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * LC;
       if (act[k]) lg[k][0] = (1u << 16) | 1u;
       B0[k] = F0[k] = Line<VT>{0, 1};
     }
@@ -560,7 +569,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           eo[k] = v0[k];
           const int nop = F0[k].s;
           if (act[k] & (nop != op[k])) {
-            lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop;
+            if (cnt[k] < LC) lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop;
             ++cnt[k];
           }
           op[k] = nop;
@@ -568,7 +577,11 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         if (chain_out && lane == 31) eout_buf[evbase + q] = eo[K - 1];
       }
       evbase += nev;
-      if (__any_sync(FULL, ovf)) {
+      bool full = false;
+#pragma unroll
+      for (int k = 0; k < K; ++k) full |= cnt[k] > LC;
+      logfull = __any_sync(FULL, full);
+      if (__any_sync(FULL, ovf) || logfull) {
         ovf = true;
         break;
       }
@@ -706,12 +719,14 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
 
     // ---- a4: all layers in lockstep, one support row per step --------------------------------
     unsigned pops_e = 0, ev_e = 0;
+    bool logfull = false;
 #ifdef SP_HULL_FORCE_GLOBAL   // experiment: every entry through the global-ring retry
     bool ovf = true;
 #else
-    bool ovf = hull_dp<WT, VT, K>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1, pops_e, ev_e);
+    bool ovf = hull_dp<WT, VT, K>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1, pops_e, ev_e,
+                                  logfull);
 #endif
-    if (ovf) {   // retry with a global overflow ring from the pool (rare)
+    if (ovf && !logfull) {   // retry with a global overflow ring from the pool (rare)
       int g = -1;
       if (lane == 0) g = pool_acquire(p);
       g = __shfl_sync(FULL, g, 0);
@@ -719,7 +734,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
         pops_e = ev_e = 0;
         Line<VT>* gr = reinterpret_cast<Line<VT>*>(p.gring) + (size_t)g * K * HCG * 32;
         ovf = hull_dp<WT, VT, K>(p, we, e, TN, nV, GRing<VT, HCG>{gr}, logs, logn, ebuf0, ebuf1,
-                                 pops_e, ev_e);
+                                 pops_e, ev_e, logfull);
         __syncwarp();
         if (lane == 0) pool_release(p, g);
       }
@@ -739,7 +754,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
       int k = 0, j = N, m = M;
       while (m > 0 && j >= tfirst) {   // P_j > 0  <=>  j >= first non-zero bin
         const int ls = hull_layer_slot(K, m);
-        const int s = log_lookup_warp(logs + (size_t)ls * (N + 1), logn[ls], j);
+        const int s = log_lookup_warp(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
         if (lane == 0) out[k] = s;
         ++k;
         j = s - 1;
@@ -776,7 +791,7 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
         int k = 0, j = N, m = mb;
         while (m > 0 && j >= tfirst) {
           const int ls = hull_layer_slot(K, m);
-          const int s = log_lookup_lane(logs + (size_t)ls * (N + 1), logn[ls], j);
+          const int s = log_lookup_lane(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
           fo[k++] = s;
           j = s - 1;
           --m;
@@ -930,6 +945,11 @@ cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, 
   p.fb = fb;
   p.slots = slots;
   p.slot = sp::hull_slot_bytes(N, M);
+  p.logcap = sp::hull_log_cap(N);
+  if (const char* lc = getenv("SP_HULL_LOGCAP")) {   // test hook: force the log-full fallback
+    const int v = atoi(lc);
+    if (v >= 1 && v < p.logcap) p.logcap = v;
+  }
   const bool k2 = sp::hull_K(M) == 2;
   if (wtype == SP_W_PROB_F64) {
     if (k2) sp::hull_launch_t<double, 2>(p, grid, st);

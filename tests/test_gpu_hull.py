@@ -96,30 +96,27 @@ def test_hull_sparse_ties_and_plateaus(dev):
 
 
 def test_hull_overflow_falls_back_exactly(dev):
-    """Uniform mass: the layer-1 hull holds ~N/2 lines.  At N = 3000 it outgrows the shared ring
-    but fits a global overflow ring (solved by the hull kernel on its retry); at N = 6000 it
-    outgrows that too and the D&C kernel solves the entry.  Mixed in one batch with dense
-    entries, an int64-range entry and a bad entry."""
-    N, M = 3000, 40
-    H = dense(8, N, seed=1).astype(np.int64)
-    H[2, 1:] = 1                              # shared-ring overflow -> global ring
-    H[5, 1:] = 3                              # shared-ring overflow -> global ring
-    H[6] *= 400000 // max(1, H[6].sum())       # 2 n N >= 2^31: the int64 hull instantiation
-    assert H[6].sum() * N * 2 >= 2 ** 31
-    r = place(H, M, dev, dtype=torch.int64)
-    assert r["stats"]["entries_hull"] == 8 and r["stats"]["entries_i64"] == 1
-    check(H, M, r)
-    Hb = H.copy()
-    Hb[3, 9] = -1
-    r = place(Hb, M, dev, dtype=torch.int64)
-    assert r["npos"][3] == -sp.SP_ERR_BAD_ARGUMENT
-    check(Hb, M, r, rows=[0, 1, 2, 4, 5, 6, 7])
-    N = 20000
-    H = dense(3, N, seed=2)
-    H[1, 1:] = 1                              # may outgrow the global ring too -> D&C
-    r = place(H, 8, dev)
-    assert r["stats"]["entries_hull"] >= 2
-    check(H, 8, r)
+    """Uniform mass: the layer-1 hull holds ~N/2 lines and opt changes every other row.  At
+    N = 1000 the hull outgrows the shared ring but fits a global overflow ring (solved by the
+    hull kernel on its retry); at N = 3000 its argmin log fills too (capacity max(1024, N/8))
+    and the D&C kernel solves it.  Mixed in one batch with dense entries, an int64-range entry
+    (int64 hull instantiation) and a bad entry (D&C)."""
+    M = 40
+    for N, uniform_on_hull in ((1000, True), (3000, False)):
+        H = dense(8, N, seed=1).astype(np.int64)
+        H[2, 1:] = 1
+        H[5, 1:] = 3
+        H[6] *= (2 ** 31 // N) // max(1, H[6].sum()) + 1   # 2 n N >= 2^31: int64 instantiation
+        assert H[6].sum() * N * 2 >= 2 ** 31
+        r = place(H, M, dev, dtype=torch.int64)
+        assert r["stats"]["entries_hull"] == (8 if uniform_on_hull else 6)
+        assert r["stats"]["entries_i64"] == 1
+        check(H, M, r)
+        Hb = H.copy()
+        Hb[3, 9] = -1
+        r = place(Hb, M, dev, dtype=torch.int64)
+        assert r["npos"][3] == -sp.SP_ERR_BAD_ARGUMENT
+        check(Hb, M, r, rows=[0, 1, 2, 4, 5, 6, 7])
 
 
 def test_hull_matches_dc_kernel_w5_rows(dev):
@@ -214,3 +211,16 @@ def test_hull_f64_path_vs_exact(dev):
     finally:
         del os.environ["SP_NO_HULL"]
     assert (np.abs(d["cost"] - r["cost"]) <= 1e-12 * exact).all()
+
+
+def test_hull_log_full_falls_back(dev):
+    """Entries whose argmin-change log fills (forced with a tiny capacity) are solved by the
+    D&C kernel instead -- same outputs as the oracle."""
+    H = dense(10, 700, seed=21)
+    os.environ["SP_HULL_LOGCAP"] = "3"
+    try:
+        r = place(H, 40, dev)
+    finally:
+        del os.environ["SP_HULL_LOGCAP"]
+    assert r["stats"]["entries_hull"] < 10
+    check(H, 40, r, algo="naive")

@@ -213,6 +213,8 @@ struct SRing<int, C0, C1> {
     asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.b), "=r"(v.s) : "r"(addr(k, pos)));
     return v;
   }
+  __device__ __forceinline__ Line<int> ld_back(int k, int b, int t) const { return ld(k, b - t); }
+  __device__ __forceinline__ Line<int> ld_front(int k, int f, int t) const { return ld(k, f + t); }
   __device__ __forceinline__ void st(int k, int pos, Line<int> v) const {
     asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr(k, pos)), "r"(v.b), "r"(v.s)
                  : "memory");
@@ -225,6 +227,12 @@ struct SRing<long long, C0, C1> {
   uint32_t bb, sb;   // shared addresses of the intercept array + 8 lane and the s array + 4 lane
   __device__ __forceinline__ uint32_t q(int k, int pos) const {
     return (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
+  }
+  __device__ __forceinline__ Line<long long> ld_back(int k, int b, int t) const {
+    return ld(k, b - t);
+  }
+  __device__ __forceinline__ Line<long long> ld_front(int k, int f, int t) const {
+    return ld(k, f + t);
   }
   __device__ __forceinline__ Line<long long> ld(int k, int pos) const {
     const uint32_t x = q(k, pos);
@@ -249,6 +257,12 @@ struct SRing<double, C0, C1> {
   uint32_t bb, sb;   // as SRing<long long>: double intercepts + 8 lane, s + 4 lane
   __device__ __forceinline__ uint32_t q(int k, int pos) const {
     return (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
+  }
+  __device__ __forceinline__ Line<double> ld_back(int k, int b, int t) const {
+    return ld(k, b - t);
+  }
+  __device__ __forceinline__ Line<double> ld_front(int k, int f, int t) const {
+    return ld(k, f + t);
   }
   __device__ __forceinline__ Line<double> ld(int k, int pos) const {
     const uint32_t x = q(k, pos);
@@ -295,6 +309,58 @@ __device__ __forceinline__ hdd hdd_warp_sum(hdd v) {
   return v;
 }
 
+// Mirrored 6-byte int32 rings (-DSP_HULL_RINGM experiment; measured slower on W5, 45.6 vs 41.0
+// ms: the guard rows cost two warps/SM and the mirrored stores outweigh the saved addressing).  A position row holds
+// the 32 lanes' intercepts (int32, 128 B) then their s (uint16, 64 B): 192 B.  Each slot's ring
+// has 4 guard rows before position 0 mirroring positions C-4..C-1 and 2 after position C-1
+// mirroring 0..1, so the four lines below the back and the two above the front are read at
+// constant offsets from one base address per end (no per-load wrap arithmetic); a push whose
+// position has a mirror writes it too.
+template <int C0, int C1>
+struct SRingM {
+  uint32_t b0;       // shared address of slot 0's position-0 intercept of this lane
+  uint32_t ds;       // s address - intercept address (per lane: 128 - 2 lane)
+  static constexpr uint32_t ROW = 192;
+  __device__ __forceinline__ uint32_t pos0(int k) const {
+    return b0 + (k ? (uint32_t)(C0 + 6) * ROW : 0u);
+  }
+  __device__ __forceinline__ uint32_t at(int k, int pos) const {
+    return pos0(k) + ((uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1)) * ROW;
+  }
+  __device__ __forceinline__ Line<int> lda(uint32_t a) const {
+    Line<int> v;
+    unsigned short sv;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.b) : "r"(a));
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sv) : "r"(a + ds));
+    v.s = sv;
+    return v;
+  }
+  __device__ __forceinline__ void sta(uint32_t a, Line<int> v) const {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v.b) : "memory");
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a + ds), "h"((unsigned short)v.s) : "memory");
+  }
+  __device__ __forceinline__ Line<int> ld(int k, int pos) const { return lda(at(k, pos)); }
+  // line b - t (t = 1..4) / f + t (t = 1..2): one base per end, constant offsets
+  __device__ __forceinline__ Line<int> ld_back(int k, int b, int t) const {
+    return lda(at(k, b) - (uint32_t)t * ROW);
+  }
+  __device__ __forceinline__ Line<int> ld_front(int k, int f, int t) const {
+    return lda(at(k, f) + (uint32_t)t * ROW);
+  }
+  __device__ __forceinline__ void st(int k, int pos, Line<int> v) const {
+    const int C = k ? C1 : C0;
+    const int q = pos & (C - 1);
+    const uint32_t a = pos0(k) + (uint32_t)q * ROW;
+    sta(a, v);
+    if (q >= C - 4) sta(a - (uint32_t)C * ROW, v);   // guard rows -4..-1
+    if (q <= 1) sta(a + (uint32_t)C * ROW, v);       // guard rows C, C+1
+  }
+  static constexpr int cap(int k) { return k ? C1 : C0; }
+  static constexpr size_t bytes(int K) {
+    return (size_t)(C0 + 6 + (K == 2 ? C1 + 6 : 0)) * ROW;
+  }
+};
+
 // 6-byte int32 lines (intercepts int32 [pos][lane], s uint16 [pos][lane]): 25% less shared
 // memory per layer (12 instead of 9 warps/SM) for a second LDS per line; the default for the int32
 // instantiation (W5: 43.2 -> 42.0 ms; -DSP_HULL_RING8 restores int2 lines)
@@ -304,6 +370,8 @@ struct SRing6 {
   __device__ __forceinline__ uint32_t q(int k, int pos) const {
     return (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
   }
+  __device__ __forceinline__ Line<int> ld_back(int k, int b, int t) const { return ld(k, b - t); }
+  __device__ __forceinline__ Line<int> ld_front(int k, int f, int t) const { return ld(k, f + t); }
   __device__ __forceinline__ Line<int> ld(int k, int pos) const {
     const uint32_t x = q(k, pos);
     Line<int> v;
@@ -331,6 +399,8 @@ struct GRing {
     return k * C * 32 + ((pos & (C - 1)) << 5) + lane_id();
   }
   __device__ __forceinline__ Line<VT> ld(int k, int pos) const { return base[idx(k, pos)]; }
+  __device__ __forceinline__ Line<VT> ld_back(int k, int b, int t) const { return ld(k, b - t); }
+  __device__ __forceinline__ Line<VT> ld_front(int k, int f, int t) const { return ld(k, f + t); }
   __device__ __forceinline__ void st(int k, int pos, Line<VT> v) const { base[idx(k, pos)] = v; }
   static constexpr int cap(int) { return C; }
 };
@@ -444,12 +514,12 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         Line<VT> L1[K], L2[K], L3[K], L4[K], G1[K], G2[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          L1[k] = rg.ld(k, b[k] - 1);
-          L2[k] = rg.ld(k, b[k] - 2);
-          L3[k] = rg.ld(k, b[k] - 3);
-          L4[k] = rg.ld(k, b[k] - 4);
-          G1[k] = rg.ld(k, f[k] + 1);
-          G2[k] = rg.ld(k, f[k] + 2);
+          L1[k] = rg.ld_back(k, b[k], 1);
+          L2[k] = rg.ld_back(k, b[k], 2);
+          L3[k] = rg.ld_back(k, b[k], 3);
+          L4[k] = rg.ld_back(k, b[k], 4);
+          G1[k] = rg.ld_front(k, f[k], 1);
+          G2[k] = rg.ld_front(k, f[k], 2);
         }
         // e_{m-1}(j-1): from the lane below (its value at the previous support row);
         // lane 0 slot 0 from the previous pass (or e_0 = 0)
@@ -605,7 +675,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
 // VT = int: every entry first; those beyond the int32 guard but within the int64 one are listed
 // for the VT = long long instantiation (launched next, same slots); the rest for the D&C kernel.
 template <typename WT, int K, typename VT>
-__global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
+__global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
   constexpr bool F64 = std::is_same<VT, double>::value;
   constexpr bool WIDE = std::is_same<VT, long long>::value;
   const int lane = threadIdx.x;
@@ -613,22 +683,28 @@ __global__ void __launch_bounds__(32) dp_hull_kernel(HullParams p) {
   constexpr int NPOS = C0 + (K == 2 ? C1 : 0);   // ring positions of this warp
   extern __shared__ __align__(16) uint8_t sring[];   // ring_bytes<K, VT>()
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
-#ifndef SP_HULL_RING8
-  using SR = typename std::conditional<std::is_same<VT, int>::value, SRing6<C0, C1>,
+#if defined(SP_HULL_RING8)
+  using SR = SRing<VT, C0, C1>;
+#elif defined(SP_HULL_RINGM)
+  using SR = typename std::conditional<std::is_same<VT, int>::value, SRingM<C0, C1>,
                                        SRing<VT, C0, C1>>::type;
 #else
-  using SR = SRing<VT, C0, C1>;
+  using SR = typename std::conditional<std::is_same<VT, int>::value, SRing6<C0, C1>,
+                                       SRing<VT, C0, C1>>::type;
 #endif
   SR srg;
   if constexpr (sizeof(VT) == 8) {
     srg.bb = sbase + 8u * (uint32_t)lane;
     srg.sb = sbase + (uint32_t)NPOS * 256u + 4u * (uint32_t)lane;
   } else {
-#ifndef SP_HULL_RING8
+#if defined(SP_HULL_RING8)
+    srg.base = sbase + 8u * (uint32_t)lane;
+#elif defined(SP_HULL_RINGM)
+    srg.b0 = sbase + 4u * 192u + 4u * (uint32_t)lane;
+    srg.ds = 128u - 2u * (uint32_t)lane;
+#else
     srg.bb = sbase + 4u * (uint32_t)lane;
     srg.sb = sbase + (uint32_t)NPOS * 128u + 2u * (uint32_t)lane;
-#else
-    srg.base = sbase + 8u * (uint32_t)lane;
 #endif
   }
   const int N = p.N, M = p.M;
@@ -843,10 +919,13 @@ template <int K, typename VT>
 static constexpr size_t ring_bytes() {
   constexpr bool W = std::is_same<VT, long long>::value;
   constexpr int NPOS = (W ? HW0 : HC0) + (K == 2 ? (W ? HW1 : HC1) : 0);
-#ifndef SP_HULL_RING8
-  return (size_t)NPOS * (sizeof(VT) == 8 ? 384 : 192);
+  if constexpr (sizeof(VT) == 8) return (size_t)NPOS * 384;
+#if defined(SP_HULL_RING8)
+  return (size_t)NPOS * 256;
+#elif defined(SP_HULL_RINGM)
+  return SRingM<HC0, HC1>::bytes(K);
 #else
-  return (size_t)NPOS * (sizeof(VT) == 8 ? 384 : 256);
+  return (size_t)NPOS * 192;
 #endif
 }
 

@@ -309,61 +309,10 @@ __device__ __forceinline__ hdd hdd_warp_sum(hdd v) {
   return v;
 }
 
-// Mirrored 6-byte int32 rings (-DSP_HULL_RINGM experiment; measured slower on W5, 45.6 vs 41.0
-// ms: the guard rows cost two warps/SM and the mirrored stores outweigh the saved addressing).  A position row holds
-// the 32 lanes' intercepts (int32, 128 B) then their s (uint16, 64 B): 192 B.  Each slot's ring
-// has 4 guard rows before position 0 mirroring positions C-4..C-1 and 2 after position C-1
-// mirroring 0..1, so the four lines below the back and the two above the front are read at
-// constant offsets from one base address per end (no per-load wrap arithmetic); a push whose
-// position has a mirror writes it too.
-template <int C0, int C1>
-struct SRingM {
-  uint32_t b0;       // shared address of slot 0's position-0 intercept of this lane
-  uint32_t ds;       // s address - intercept address (per lane: 128 - 2 lane)
-  static constexpr uint32_t ROW = 192;
-  __device__ __forceinline__ uint32_t pos0(int k) const {
-    return b0 + (k ? (uint32_t)(C0 + 6) * ROW : 0u);
-  }
-  __device__ __forceinline__ uint32_t at(int k, int pos) const {
-    return pos0(k) + ((uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1)) * ROW;
-  }
-  __device__ __forceinline__ Line<int> lda(uint32_t a) const {
-    Line<int> v;
-    unsigned short sv;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.b) : "r"(a));
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sv) : "r"(a + ds));
-    v.s = sv;
-    return v;
-  }
-  __device__ __forceinline__ void sta(uint32_t a, Line<int> v) const {
-    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v.b) : "memory");
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a + ds), "h"((unsigned short)v.s) : "memory");
-  }
-  __device__ __forceinline__ Line<int> ld(int k, int pos) const { return lda(at(k, pos)); }
-  // line b - t (t = 1..4) / f + t (t = 1..2): one base per end, constant offsets
-  __device__ __forceinline__ Line<int> ld_back(int k, int b, int t) const {
-    return lda(at(k, b) - (uint32_t)t * ROW);
-  }
-  __device__ __forceinline__ Line<int> ld_front(int k, int f, int t) const {
-    return lda(at(k, f) + (uint32_t)t * ROW);
-  }
-  __device__ __forceinline__ void st(int k, int pos, Line<int> v) const {
-    const int C = k ? C1 : C0;
-    const int q = pos & (C - 1);
-    const uint32_t a = pos0(k) + (uint32_t)q * ROW;
-    sta(a, v);
-    if (q >= C - 4) sta(a - (uint32_t)C * ROW, v);   // guard rows -4..-1
-    if (q <= 1) sta(a + (uint32_t)C * ROW, v);       // guard rows C, C+1
-  }
-  static constexpr int cap(int k) { return k ? C1 : C0; }
-  static constexpr size_t bytes(int K) {
-    return (size_t)(C0 + 6 + (K == 2 ? C1 + 6 : 0)) * ROW;
-  }
-};
-
 // 6-byte int32 lines (intercepts int32 [pos][lane], s uint16 [pos][lane]): 25% less shared
-// memory per layer (12 instead of 9 warps/SM) for a second LDS per line; the default for the int32
-// instantiation (W5: 43.2 -> 42.0 ms; -DSP_HULL_RING8 restores int2 lines)
+// memory per layer than int2 lines (12 instead of 9 warps/SM) for a second LDS per line -- the
+// int32 instantiation's rings (W5: 43.2 -> 42.0 ms).  Measured and dropped: mirrored guard rows
+// for constant-offset loads (45.6 ms: two fewer warps/SM, extra stores).
 template <int C0, int C1>
 struct SRing6 {
   uint32_t bb, sb;   // shared addresses: intercept array + 4 lane, s array + 2 lane
@@ -503,9 +452,6 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       VT Ec = 0;
       const int nev = __popc(evmask);
       if (chain_in && lane < nev) Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
-#ifdef SP_HULL_UNROLL2
-#pragma unroll 2
-#endif
       for (int q = 0; evmask; ++q) {
         const int i = __ffs(evmask) - 1;
         evmask &= evmask - 1;
@@ -683,29 +629,15 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
   constexpr int NPOS = C0 + (K == 2 ? C1 : 0);   // ring positions of this warp
   extern __shared__ __align__(16) uint8_t sring[];   // ring_bytes<K, VT>()
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
-#if defined(SP_HULL_RING8)
-  using SR = SRing<VT, C0, C1>;
-#elif defined(SP_HULL_RINGM)
-  using SR = typename std::conditional<std::is_same<VT, int>::value, SRingM<C0, C1>,
-                                       SRing<VT, C0, C1>>::type;
-#else
   using SR = typename std::conditional<std::is_same<VT, int>::value, SRing6<C0, C1>,
                                        SRing<VT, C0, C1>>::type;
-#endif
   SR srg;
   if constexpr (sizeof(VT) == 8) {
     srg.bb = sbase + 8u * (uint32_t)lane;
     srg.sb = sbase + (uint32_t)NPOS * 256u + 4u * (uint32_t)lane;
   } else {
-#if defined(SP_HULL_RING8)
-    srg.base = sbase + 8u * (uint32_t)lane;
-#elif defined(SP_HULL_RINGM)
-    srg.b0 = sbase + 4u * 192u + 4u * (uint32_t)lane;
-    srg.ds = 128u - 2u * (uint32_t)lane;
-#else
     srg.bb = sbase + 4u * (uint32_t)lane;
     srg.sb = sbase + (uint32_t)NPOS * 128u + 2u * (uint32_t)lane;
-#endif
   }
   const int N = p.N, M = p.M;
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
@@ -796,12 +728,8 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
     // ---- a4: all layers in lockstep, one support row per step --------------------------------
     unsigned pops_e = 0, ev_e = 0;
     bool logfull = false;
-#ifdef SP_HULL_FORCE_GLOBAL   // experiment: every entry through the global-ring retry
-    bool ovf = true;
-#else
     bool ovf = hull_dp<WT, VT, K>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1, pops_e, ev_e,
                                   logfull);
-#endif
     if (ovf && !logfull) {   // retry with a global overflow ring from the pool (rare)
       int g = -1;
       if (lane == 0) g = pool_acquire(p);
@@ -920,13 +848,7 @@ static constexpr size_t ring_bytes() {
   constexpr bool W = std::is_same<VT, long long>::value;
   constexpr int NPOS = (W ? HW0 : HC0) + (K == 2 ? (W ? HW1 : HC1) : 0);
   if constexpr (sizeof(VT) == 8) return (size_t)NPOS * 384;
-#if defined(SP_HULL_RING8)
-  return (size_t)NPOS * 256;
-#elif defined(SP_HULL_RINGM)
-  return SRingM<HC0, HC1>::bytes(K);
-#else
   return (size_t)NPOS * 192;
-#endif
 }
 
 template <typename WT, int K, typename VT>

@@ -309,34 +309,35 @@ __device__ __forceinline__ hdd hdd_warp_sum(hdd v) {
   return v;
 }
 
-// 6-byte int32 lines (intercepts int32 [pos][lane], s uint16 [pos][lane]): 25% less shared
-// memory per layer than int2 lines (12 instead of 9 warps/SM) for a second LDS per line -- the
-// int32 instantiation's rings (W5: 43.2 -> 42.0 ms).  Measured and dropped: mirrored guard rows
-// for constant-offset loads (45.6 ms: two fewer warps/SM, extra stores).
+// The int32 instantiation's rings: 6-byte lines, interleaved -- a position row holds the 32
+// lanes' intercepts (int32, 128 B) then their s (uint16, 64 B), 192 B per row.  25% less shared
+// memory than int2 lines (12 instead of 9 warps/SM: W5 43.2 -> 42.0 ms), and one IMAD (FMA pipe,
+// the ALU pipe is the busier one) forms a row address with the s address at a per-lane constant
+// offset (40.9 -> 38.9 ms vs separate intercept / s arrays).  Measured and dropped: mirrored
+// guard rows for constant-offset loads (two fewer warps/SM, extra stores: slower).
 template <int C0, int C1>
-struct SRing6 {
-  uint32_t bb, sb;   // shared addresses: intercept array + 4 lane, s array + 2 lane
-  __device__ __forceinline__ uint32_t q(int k, int pos) const {
-    return (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
+struct SRingI {
+  uint32_t b0;   // shared address of slot 0, row 0, this lane's intercept
+  uint32_t ds;   // s address - intercept address: 128 - 2 lane
+  __device__ __forceinline__ uint32_t at(int k, int pos) const {
+    const uint32_t q = (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
+    return q * 192u + b0 + (k ? (uint32_t)C0 * 192u : 0u);
   }
-  __device__ __forceinline__ Line<int> ld_back(int k, int b, int t) const { return ld(k, b - t); }
-  __device__ __forceinline__ Line<int> ld_front(int k, int f, int t) const { return ld(k, f + t); }
   __device__ __forceinline__ Line<int> ld(int k, int pos) const {
-    const uint32_t x = q(k, pos);
+    const uint32_t a = at(k, pos);
     Line<int> v;
     unsigned short sv;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.b) : "r"((x << 7) + bb + (k ? C0 * 128u : 0u)));
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sv) : "r"((x << 6) + sb + (k ? C0 * 64u : 0u)));
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.b) : "r"(a));
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sv) : "r"(a + ds));
     v.s = sv;
     return v;
   }
+  __device__ __forceinline__ Line<int> ld_back(int k, int b, int t) const { return ld(k, b - t); }
+  __device__ __forceinline__ Line<int> ld_front(int k, int f, int t) const { return ld(k, f + t); }
   __device__ __forceinline__ void st(int k, int pos, Line<int> v) const {
-    const uint32_t x = q(k, pos);
-    asm volatile("st.shared.b32 [%0], %1;" ::"r"((x << 7) + bb + (k ? C0 * 128u : 0u)), "r"(v.b)
-                 : "memory");
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"((x << 6) + sb + (k ? C0 * 64u : 0u)),
-                 "h"((unsigned short)v.s)
-                 : "memory");
+    const uint32_t a = at(k, pos);
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v.b) : "memory");
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a + ds), "h"((unsigned short)v.s) : "memory");
   }
   static constexpr int cap(int k) { return k ? C1 : C0; }
 };
@@ -629,15 +630,15 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
   constexpr int NPOS = C0 + (K == 2 ? C1 : 0);   // ring positions of this warp
   extern __shared__ __align__(16) uint8_t sring[];   // ring_bytes<K, VT>()
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
-  using SR = typename std::conditional<std::is_same<VT, int>::value, SRing6<C0, C1>,
+  using SR = typename std::conditional<std::is_same<VT, int>::value, SRingI<C0, C1>,
                                        SRing<VT, C0, C1>>::type;
   SR srg;
   if constexpr (sizeof(VT) == 8) {
     srg.bb = sbase + 8u * (uint32_t)lane;
     srg.sb = sbase + (uint32_t)NPOS * 256u + 4u * (uint32_t)lane;
   } else {
-    srg.bb = sbase + 4u * (uint32_t)lane;
-    srg.sb = sbase + (uint32_t)NPOS * 128u + 2u * (uint32_t)lane;
+    srg.b0 = sbase + 4u * (uint32_t)lane;
+    srg.ds = 128u - 2u * (uint32_t)lane;
   }
   const int N = p.N, M = p.M;
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);

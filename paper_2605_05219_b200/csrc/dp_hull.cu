@@ -376,7 +376,9 @@ __device__ __forceinline__ bool pop_test<double>(int as, double ab, int ks, doub
 template <typename VT>
 using HullCT = typename std::conditional<std::is_same<VT, double>::value, double, long long>::type;
 
-template <typename WT, typename VT, int K, class RING>
+// ALLACT: every slot of every pass holds a layer (M a multiple of 32 K) -- the per-slot "active"
+// predicates vanish at compile time
+template <typename WT, typename VT, int K, bool ALLACT, class RING>
 __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
                                         HullCT<VT> TN, VT nV, const RING rg, uint32_t* logs,
                                         int32_t* logn, VT* ebuf0, VT* ebuf1,
@@ -405,7 +407,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int mk = ps * L + 32 * k + lane + 1;
-      act[k] = mk <= M;
+      act[k] = ALLACT || mk <= M;
       f[k] = 0;
       b[k] = -1;
       eo[k] = 0;   // e_m(0) = 0 (reading R1)
@@ -729,8 +731,11 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
     // ---- a4: all layers in lockstep, one support row per step --------------------------------
     unsigned pops_e = 0, ev_e = 0;
     bool logfull = false;
-    bool ovf = hull_dp<WT, VT, K>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1, pops_e, ev_e,
-                                  logfull);
+    const bool fullm = M % (32 * K) == 0;
+    bool ovf = fullm ? hull_dp<WT, VT, K, true>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1,
+                                                pops_e, ev_e, logfull)
+                     : hull_dp<WT, VT, K, false>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1,
+                                                 pops_e, ev_e, logfull);
     if (ovf && !logfull) {   // retry with a global overflow ring from the pool (rare)
       int g = -1;
       if (lane == 0) g = pool_acquire(p);
@@ -738,8 +743,8 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
       if (g >= 0) {
         pops_e = ev_e = 0;
         Line<VT>* gr = reinterpret_cast<Line<VT>*>(p.gring) + (size_t)g * K * HCG * 32;
-        ovf = hull_dp<WT, VT, K>(p, we, e, TN, nV, GRing<VT, HCG>{gr}, logs, logn, ebuf0, ebuf1,
-                                 pops_e, ev_e, logfull);
+        ovf = hull_dp<WT, VT, K, false>(p, we, e, TN, nV, GRing<VT, HCG>{gr}, logs, logn, ebuf0,
+                                        ebuf1, pops_e, ev_e, logfull);
         __syncwarp();
         if (lane == 0) pool_release(p, g);
       }

@@ -355,6 +355,14 @@ struct GRing {
   static constexpr int cap(int) { return C; }
 };
 
+// value of the dummy front line (above every candidate)
+template <typename VT>
+__device__ __forceinline__ VT hull_inf() {
+  if constexpr (std::is_same<VT, double>::value) return HUGE_VAL;
+  else if constexpr (std::is_same<VT, long long>::value) return LLONG_MAX;
+  else return INT_MAX;
+}
+
 // back-pop test with the new point (j, bj) as origin: for the pair (A, Bk) of consecutive hull
 // lines (A below Bk), with A' = A - new and Bk' = Bk - new in (s, b) coordinates, Bk goes iff it is
 // not strictly below the segment A -> new, i.e. cross(A', Bk') = A'.s Bk'.b - A'.b Bk'.s <= 0.
@@ -409,13 +417,16 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       const int mk = ps * L + 32 * k + lane + 1;
       act[k] = ALLACT || mk <= M;
       f[k] = 0;
-      b[k] = -1;
+      b[k] = 0;
       eo[k] = 0;   // e_m(0) = 0 (reading R1)
       op[k] = 1;   // opt_m(1) = 1 whatever the row type: logged up front
       cnt[k] = 1;
       lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * LC;
       if (act[k]) lg[k][0] = (1u << 16) | 1u;
-      B0[k] = F0[k] = Line<VT>{0, 1};
+      // the deque starts with a dummy line of value +inf at every query: the first push pops
+      // it from the front, so the deque is never empty at a push
+      B0[k] = F0[k] = Line<VT>{hull_inf<VT>(), 0};
+      rg.st(k, 0, F0[k]);
     }
     VT carry = 0, Pm1 = 0;
     hdd carry_dd{0.0, 0.0};
@@ -546,7 +557,6 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           const bool fresh = !skip[k];
           const Line<VT> F1 = (fresh & (d == 1)) ? nl : G1[k];   // lines f+1 / f+2 popped or new
           const Line<VT> F2 = (fresh & (d == 2)) ? nl : G2[k];
-          F0[k] = (fresh & (d == 0)) ? nl : F0[k];         // the deque was empty
           B0[k] = skip[k] ? B0[k] : nl;
           b[k] = nb;
           ovf |= act[k] & (d >= RING::cap(k));
@@ -588,7 +598,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           eo[k] = v0[k];
           const int nop = F0[k].s;
           if (act[k] & (nop != op[k])) {
-            if (cnt[k] < LC) lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop;
+            lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop;   // < LC: checked per chunk
             ++cnt[k];
           }
           op[k] = nop;
@@ -598,7 +608,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       evbase += nev;
       bool full = false;
 #pragma unroll
-      for (int k = 0; k < K; ++k) full |= cnt[k] > LC;
+      for (int k = 0; k < K; ++k) full |= (LC <= N) & (cnt[k] > LC - 33);   // 32 rows of headroom
       logfull = __any_sync(FULL, full);
       if (__any_sync(FULL, ovf) || logfull) {
         ovf = true;

@@ -551,7 +551,6 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const int nb = skip[k] ? b[k] : top[k] + 1;
-          pops_e += (unsigned)(b[k] - top[k]);
           const Line<VT> nl{bj[k], j};
           if (!skip[k]) rg.st(k, nb, nl);
           const int d = nb - f[k];
@@ -620,6 +619,8 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (!act[k]) continue;
+        // stats: pushes (support rows, less trimmed lines) = back pops + b; front pops = f - 1
+        pops_e += (unsigned)(evbase - b[k]) + (unsigned)(f[k] - 1);
         const int mk = ps * L + 32 * k + lane + 1;
         logn[ps * L + 32 * k + lane] = cnt[k];
         const HullCT<VT> V = TN + (HullCT<VT>)eo[k];   // V_m = T_N + e_m(N)

@@ -195,91 +195,9 @@ struct Line {
   int s;
 };
 
-// Ring storage policies, [slot][pos][lane] so that every lane has its own banks.
-// SRing: shared memory, int32 lines packed as int2 (256 B per position) or int64 lines as an int64
-// array (256 B per position) plus an int32 array (128 B per position); LDS/STS on 32-bit shared
-// addresses with compile-time masks.  GRing: a global overflow ring from the pool.
-template <typename VT, int C0, int C1>
-struct SRing;
-template <int C0, int C1>
-struct SRing<int, C0, C1> {
-  uint32_t base;   // shared address of the ring array + 8 lane
-  __device__ __forceinline__ uint32_t addr(int k, int pos) const {
-    const uint32_t m = (uint32_t)((k ? C1 : C0) - 1);
-    return (((uint32_t)pos & m) << 8) + (base + (k ? (uint32_t)C0 * 256u : 0u));
-  }
-  __device__ __forceinline__ Line<int> ld(int k, int pos) const {
-    Line<int> v;
-    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.b), "=r"(v.s) : "r"(addr(k, pos)));
-    return v;
-  }
-  __device__ __forceinline__ Line<int> ld_back(int k, int b, int t) const { return ld(k, b - t); }
-  __device__ __forceinline__ Line<int> ld_front(int k, int f, int t) const { return ld(k, f + t); }
-  __device__ __forceinline__ void st(int k, int pos, Line<int> v) const {
-    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr(k, pos)), "r"(v.b), "r"(v.s)
-                 : "memory");
-  }
-  static constexpr int cap(int k) { return k ? C1 : C0; }
-  static constexpr size_t bytes() { return (size_t)(C0 + C1) * 256; }
-};
-template <int C0, int C1>
-struct SRing<long long, C0, C1> {
-  uint32_t bb, sb;   // shared addresses of the intercept array + 8 lane and the s array + 4 lane
-  __device__ __forceinline__ uint32_t q(int k, int pos) const {
-    return (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
-  }
-  __device__ __forceinline__ Line<long long> ld_back(int k, int b, int t) const {
-    return ld(k, b - t);
-  }
-  __device__ __forceinline__ Line<long long> ld_front(int k, int f, int t) const {
-    return ld(k, f + t);
-  }
-  __device__ __forceinline__ Line<long long> ld(int k, int pos) const {
-    const uint32_t x = q(k, pos);
-    Line<long long> v;
-    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v.b) : "r"((x << 8) + bb + (k ? C0 * 256u : 0u)));
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.s) : "r"((x << 7) + sb + (k ? C0 * 128u : 0u)));
-    return v;
-  }
-  __device__ __forceinline__ void st(int k, int pos, Line<long long> v) const {
-    const uint32_t x = q(k, pos);
-    asm volatile("st.shared.b64 [%0], %1;" ::"r"((x << 8) + bb + (k ? C0 * 256u : 0u)), "l"(v.b)
-                 : "memory");
-    asm volatile("st.shared.b32 [%0], %1;" ::"r"((x << 7) + sb + (k ? C0 * 128u : 0u)), "r"(v.s)
-                 : "memory");
-  }
-  static constexpr int cap(int k) { return k ? C1 : C0; }
-  static constexpr size_t bytes() { return (size_t)(C0 + C1) * 384; }
-};
-
-template <int C0, int C1>
-struct SRing<double, C0, C1> {
-  uint32_t bb, sb;   // as SRing<long long>: double intercepts + 8 lane, s + 4 lane
-  __device__ __forceinline__ uint32_t q(int k, int pos) const {
-    return (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
-  }
-  __device__ __forceinline__ Line<double> ld_back(int k, int b, int t) const {
-    return ld(k, b - t);
-  }
-  __device__ __forceinline__ Line<double> ld_front(int k, int f, int t) const {
-    return ld(k, f + t);
-  }
-  __device__ __forceinline__ Line<double> ld(int k, int pos) const {
-    const uint32_t x = q(k, pos);
-    Line<double> v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v.b) : "r"((x << 8) + bb + (k ? C0 * 256u : 0u)));
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.s) : "r"((x << 7) + sb + (k ? C0 * 128u : 0u)));
-    return v;
-  }
-  __device__ __forceinline__ void st(int k, int pos, Line<double> v) const {
-    const uint32_t x = q(k, pos);
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"((x << 8) + bb + (k ? C0 * 256u : 0u)), "d"(v.b)
-                 : "memory");
-    asm volatile("st.shared.b32 [%0], %1;" ::"r"((x << 7) + sb + (k ? C0 * 128u : 0u)), "r"(v.s)
-                 : "memory");
-  }
-  static constexpr int cap(int k) { return k ? C1 : C0; }
-};
+// Ring storage policies, [slot][pos][lane] so that every lane has its own banks: SRingI (int32
+// lines, below) and SRingW (int64 / fp64 lines) in shared memory, GRing for a global overflow
+// ring from the pool.
 
 // double-double sums for the fp64 path (prefix sums rounded once, T_N, the definitional cost)
 struct hdd {
@@ -338,6 +256,39 @@ struct SRingI {
     const uint32_t a = at(k, pos);
     asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v.b) : "memory");
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a + ds), "h"((unsigned short)v.s) : "memory");
+  }
+  static constexpr int cap(int k) { return k ? C1 : C0; }
+};
+
+// 12-byte lines for the int64 / fp64 instantiations, interleaved like SRingI: a 384-byte
+// position row holds the 32 lanes' 8-byte intercepts then their int32 s; one IMAD per row address
+template <typename VT, int C0, int C1>
+struct SRingW {
+  uint32_t b0;   // shared address of slot 0, row 0, this lane's intercept
+  uint32_t ds;   // s address - intercept address: 256 - 4 lane
+  __device__ __forceinline__ uint32_t at(int k, int pos) const {
+    const uint32_t q = (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
+    return q * 384u + b0 + (k ? (uint32_t)C0 * 384u : 0u);
+  }
+  __device__ __forceinline__ Line<VT> ld(int k, int pos) const {
+    const uint32_t a = at(k, pos);
+    Line<VT> v;
+    if constexpr (std::is_same<VT, double>::value)
+      asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v.b) : "r"(a));
+    else
+      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v.b) : "r"(a));
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.s) : "r"(a + ds));
+    return v;
+  }
+  __device__ __forceinline__ Line<VT> ld_back(int k, int b, int t) const { return ld(k, b - t); }
+  __device__ __forceinline__ Line<VT> ld_front(int k, int f, int t) const { return ld(k, f + t); }
+  __device__ __forceinline__ void st(int k, int pos, Line<VT> v) const {
+    const uint32_t a = at(k, pos);
+    if constexpr (std::is_same<VT, double>::value)
+      asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v.b) : "memory");
+    else
+      asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v.b) : "memory");
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a + ds), "r"(v.s) : "memory");
   }
   static constexpr int cap(int k) { return k ? C1 : C0; }
 };
@@ -645,11 +596,11 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
   extern __shared__ __align__(16) uint8_t sring[];   // ring_bytes<K, VT>()
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
   using SR = typename std::conditional<std::is_same<VT, int>::value, SRingI<C0, C1>,
-                                       SRing<VT, C0, C1>>::type;
+                                       SRingW<VT, C0, C1>>::type;
   SR srg;
   if constexpr (sizeof(VT) == 8) {
-    srg.bb = sbase + 8u * (uint32_t)lane;
-    srg.sb = sbase + (uint32_t)NPOS * 256u + 4u * (uint32_t)lane;
+    srg.b0 = sbase + 8u * (uint32_t)lane;
+    srg.ds = 256u - 4u * (uint32_t)lane;
   } else {
     srg.b0 = sbase + 4u * (uint32_t)lane;
     srg.ds = 128u - 2u * (uint32_t)lane;

@@ -184,15 +184,18 @@ __global__ void __launch_bounds__(EV_NT)
 // segment offsets (int64) go to woff[], so P(x) = seg[x] + woff[x >> 10]: one shared lookup per
 // query instead of a 32-bin partial sum.  A segment whose own total reaches 2^31 (never on W5)
 // makes the entry use exact int64 partial sums from global memory instead.
-constexpr int EP_NT = 512;
-constexpr int EP_NW = EP_NT / 32;
-
+// ST = uint16_t: in-segment prefixes in 2 bytes (exact while a 1024-bin segment holds < 2^16
+// counts -- W5's rows hold <= 16404 in all): 64 KB of shared memory per entry, 3 CTAs of 256
+// threads per SM instead of 1 of 512.
+template <typename ST, int EP_NT>
 __global__ void __launch_bounds__(EP_NT)
     eval_p32_kernel(const int32_t* __restrict__ w, int E, int N,
                     const int32_t* __restrict__ positions, const int32_t* __restrict__ npos,
                     int S, int max_pos, int broadcast, int64_t* __restrict__ cost,
                     int32_t* __restrict__ worst) {
-  extern __shared__ __align__(16) int32_t seg[];   // [nseg * 1024] in-segment prefixes
+  constexpr int EP_NW = EP_NT / 32;
+  extern __shared__ __align__(16) unsigned char seg_raw[];
+  ST* seg = reinterpret_cast<ST*>(seg_raw);   // [nseg * 1024] in-segment prefixes
   __shared__ long long woff[65];                     // exclusive segment offsets
   __shared__ long long wtot[EP_NW], tsum[EP_NW];
   __shared__ long long sh_carry, sh_TN;
@@ -227,16 +230,16 @@ __global__ void __launch_bounds__(EP_NT)
           if (lane >= o) inc += y;
         }
         // exact while the segment total < 2^31 (checked below)
-        if (sg < nseg) seg[b0 + 32 * u + lane] = run32 + inc;
+        if (sg < nseg) seg[b0 + 32 * u + lane] = (ST)(run32 + inc);
         run32 += __shfl_sync(FULL, inc, 31);
       }
       const long long run = warp_sum(ls);
-      big |= run >= (1ll << 31);
+      big |= run >= (sizeof(ST) == 2 ? (1ll << 16) : (1ll << 31));
       if (lane == 0) wtot[wid] = sg < nseg ? run : 0;
       __syncthreads();
       if (wid == 0) {   // exclusive scan of this round's segment totals
         const long long c0 = sh_carry;
-        const long long x = wtot[lane];
+        const long long x = lane < EP_NW ? wtot[lane] : 0;
         long long inc = x;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -320,13 +323,30 @@ extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type w
   cudaStream_t st = (cudaStream_t)stream;
   if (wtype == SP_W_COUNTS_I32 && !getenv("SP_EVAL_CHUNKED")) {
     const int nseg = (N + 1 + 1023) / 1024;
-    const size_t dyn = (size_t)nseg * 1024 * 4;
-    cudaFuncSetAttribute(sp::eval_p32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)dyn);
-    const int g2 = n_entries < sms ? n_entries : sms;
-    sp::eval_p32_kernel<<<g2, sp::EP_NT, dyn, st>>>((const int32_t*)weights, n_entries, N,
-                                                    positions, n_positions, n_sets, max_pos,
-                                                    broadcast, (int64_t*)cost, worst_case);
+    const bool wide = getenv("SP_EVAL_P32") != nullptr;   // 4-byte prefixes (tests / comparison)
+    const size_t dyn = (size_t)nseg * 1024 * (wide ? 4 : 2);
+    int occ = 1;
+    if (wide) {
+      cudaFuncSetAttribute(sp::eval_p32_kernel<int32_t, 512>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp::eval_p32_kernel<int32_t, 512>, 512,
+                                                    dyn);
+    } else {
+      cudaFuncSetAttribute(sp::eval_p32_kernel<uint16_t, 256>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp::eval_p32_kernel<uint16_t, 256>, 256,
+                                                    dyn);
+    }
+    const long gcap = (long)sms * (occ < 1 ? 1 : occ);
+    const int g2 = n_entries < gcap ? n_entries : (int)gcap;
+    if (wide)
+      sp::eval_p32_kernel<int32_t, 512><<<g2, 512, dyn, st>>>(
+          (const int32_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
+          broadcast, (int64_t*)cost, worst_case);
+    else
+      sp::eval_p32_kernel<uint16_t, 256><<<g2, 256, dyn, st>>>(
+          (const int32_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
+          broadcast, (int64_t*)cost, worst_case);
   } else if (wtype == SP_W_COUNTS_I32)
     sp::eval_kernel<int32_t><<<grid, sp::EV_NT, 0, st>>>(
         (const int32_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,

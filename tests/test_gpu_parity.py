@@ -349,6 +349,31 @@ def test_expected_recompute_baselines(dev):
             assert (np_(worst)[:, i] == -(-(N + 1) // (m + 1)) - 1).all()
 
 
+def test_expected_recompute_prefix_widths(dev):
+    """int32 rows through both shared-prefix widths (2-byte default, 4-byte SP_EVAL_P32) and
+    rows whose 1024-bin segments hold >= 2^16 (resp. >= 2^31 in total) counts, which take the
+    exact global-memory path, against the oracle's definitional walk."""
+    import os
+    cfg = wl.scaled(wl.CONFIGS["W5"], 12)
+    H = wl.make_dense_hist(cfg, seed=14).numpy()
+    H[3, 5000] = 70000                      # one segment >= 2^16
+    H[7, 1:2000] = 2 ** 20                  # segments >= 2^31
+    N = cfg.N
+    pos, npos, _ = sp.baseline_sets(N, budgets=(1, 7, 64), blocks=(64, 128), device=dev)
+    rc, rw = oracle.eval_batch(H, np_(pos), np_(npos), broadcast=True, nthreads=8)
+    for env in (None, "SP_EVAL_P32", "SP_EVAL_CHUNKED"):
+        if env:
+            os.environ[env] = "1"
+        try:
+            cost, worst = sp.expected_recompute(torch.from_numpy(H).to(dev), pos, npos,
+                                                broadcast=True)
+            torch.cuda.synchronize()
+        finally:
+            if env:
+                del os.environ[env]
+        assert (np_(cost) == rc).all() and (np_(worst) == rw).all(), env
+
+
 def test_expected_recompute_dp_positions_and_bad_sets(dev):
     """E[r](DP output) == V_M, per-entry (non-broadcast) sets, malformed sets flagged."""
     cfg = wl.scaled(wl.CONFIGS["W3"], 16)

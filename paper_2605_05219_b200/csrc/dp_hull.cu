@@ -27,12 +27,13 @@
 //
 // Each layer's deque lives in shared memory as a ring (HC0 / HC1 lines for slot 0 / 1),
 // interleaved across lanes ([slot][pos][lane]) so that every lane hits its own bank whatever its
-// deque position; its ends are cached in registers (back, back-1 and three prefetched lines below;
-// front, front+1, front+2), so a row with at most four back pops and one front pop per layer
-// issues no dependent shared load.
+// deque position; the back and front lines are in registers and the two lines next to each end
+// are loaded at the top of every support row, so a row with at most two back pops and one front
+// pop per layer issues no dependent shared load (more pops: a warp-uniform loop).
 // Rings hold the live hull, which is small for histogram-shaped inputs (<= 51 lines on W5); an
-// entry whose hull outgrows a ring (e.g. the all-ones histogram: layer-1 hull ~N/2 lines) is
-// handed to the divide-and-conquer kernel (dp_place.cu), as are entries needing int64 range.
+// entry whose hull outgrows a ring is re-run on a global ring, and if that overflows too (e.g.
+// the all-ones histogram: layer-1 hull ~N/2 lines) handed to the divide-and-conquer kernel
+// (dp_place.cu), as are entries past the int64 guard.
 //
 // Argmin storage: opt_m(j) changes rarely along j, so each layer appends (j, opt_m(j)) to its
 // own log only when it changes (uint32: j << 16 | opt); the backtrack finds the last entry with
@@ -354,10 +355,10 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
     VT* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
     const bool chain_in = ps > 0, chain_out = ps + 1 < passes;
     // Per slot: deque [f, b] (monotone counters; ring position = counter mod capacity).  In
-    // registers: the back line B0 (the last one pushed) and the front line F0; the four lines
+    // registers: the back line B0 (the last one pushed) and the front line F0; the two lines
     // below the back and the two above the front are loaded from the ring at the top of every
     // support row (positions known a row ahead, so the loads overlap the shuffle).  A line is
-    // int2 (x = intercept b_s, y = s).  eo = e_m(j) (the running row value), op = opt_m(j).
+    // (intercept b_s, s).  eo = e_m(j) (the running row value), op = opt_m(j).
     int f[K], b[K], op[K], cnt[K];
     VT eo[K];
     Line<VT> B0[K], F0[K];
@@ -422,13 +423,11 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         evmask &= evmask - 1;
         const int j = jb + 1 + i;
         // ring lines around both ends (positions fixed by the previous row)
-        Line<VT> L1[K], L2[K], L3[K], L4[K], G1[K], G2[K];
+        Line<VT> L1[K], L2[K], G1[K], G2[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           L1[k] = rg.ld_back(k, b[k], 1);
           L2[k] = rg.ld_back(k, b[k], 2);
-          L3[k] = rg.ld_back(k, b[k], 3);
-          L4[k] = rg.ld_back(k, b[k], 4);
           G1[k] = rg.ld_front(k, f[k], 1);
           G2[k] = rg.ld_front(k, f[k], 2);
         }
@@ -446,7 +445,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         const VT Pj = __shfl_sync(FULL, Pc, i);
         const VT nPj = -Pj;
         ++ev_e;
-        // ---- push line j: up to four back pops decided from the loaded lines ---------------
+        // ---- push line j: up to two back pops decided from the loaded lines ----------------
         VT bj[K];
         int top[K];
         bool more[K], skip[K];
@@ -455,9 +454,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           bj[k] = in[k] + (VT)j * Pm1;
           // deltas of the back lines from the new point (j, bj)
           const int s0 = B0[k].s - j, s1 = L1[k].s - j, s2 = L2[k].s - j;
-          const int s3 = L3[k].s - j, s4 = L4[k].s - j;
           const VT c0 = B0[k].b - bj[k], c1 = L1[k].b - bj[k], c2 = L2[k].b - bj[k];
-          const VT c3 = L3[k].b - bj[k], c4 = L4[k].b - bj[k];
           // a line that overtakes the back line only beyond x = P_N = n is never optimal at a
           // query (x <= n): it is neither pushed nor allowed to pop.
           // x(back, new) > n  <=>  bj - B0.b > n (j - B0.s)  <=>  -c0 > -n s0
@@ -470,19 +467,19 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           const int sz = skip[k] ? 0 : b[k] - f[k];   // deque size - 1, before the push
           const int p1 = (sz >= 1) & pop_test(s1, c1, s0, c0);
           const int p2 = p1 & (sz >= 2) & pop_test(s2, c2, s1, c1);
-          const int p3 = p2 & (sz >= 3) & pop_test(s3, c3, s2, c2);
-          const int p4 = p3 & (sz >= 4) & pop_test(s4, c4, s3, c3);
-          top[k] = b[k] - (p1 + p2 + p3 + p4);   // position of the new second-to-back line
-          more[k] = act[k] & (p4 != 0);
+          // two pops decided eagerly; a lane with two pops may pop more: the warp-uniform loop
+          // below tests further lines (W5 34.3 -> 33.1 ms vs four eager tests)
+          top[k] = b[k] - (p1 + p2);   // position of the new second-to-back line
+          more[k] = act[k] & (p2 != 0);
         }
         bool anymore = more[0];
         if constexpr (K == 2) anymore |= more[1];
-        if (__any_sync(FULL, anymore)) {   // rare: more than four pops
+        if (__any_sync(FULL, anymore)) {   // a lane popped two lines: keep testing from the ring
 #pragma unroll
           for (int k = 0; k < K; ++k) {
             if (!more[k]) continue;
-            int cs = L4[k].s - j;
-            VT cb = L4[k].b - bj[k];
+            int cs = L2[k].s - j;
+            VT cb = L2[k].b - bj[k];
             while (top[k] - f[k] >= 1) {
               const Line<VT> l1 = rg.ld(k, top[k] - 1);
               const int ls = l1.s - j;

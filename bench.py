@@ -26,7 +26,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DP cells/s (entries*N*M)"
-TRAFFIC_JSON = "r01e_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
+TRAFFIC_JSON = "r01f_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
 UNIT = "cells/s"
 
 

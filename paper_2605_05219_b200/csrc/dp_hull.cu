@@ -474,6 +474,11 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         }
         bool anymore = more[0];
         if constexpr (K == 2) anymore |= more[1];
+#ifdef SP_HULL_BRSTATS   // instrumentation (tools/prof_dp.py, SP_BRSTATS_REPORT): rows, loops taken
+        if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(p.ws + 64), 1ull);
+        if (__any_sync(FULL, anymore) && lane == 0)
+          atomicAdd(reinterpret_cast<unsigned long long*>(p.ws + 72), 1ull);
+#endif
         if (__any_sync(FULL, anymore)) {   // a lane popped two lines: keep testing from the ring
 #pragma unroll
           for (int k = 0; k < K; ++k) {
@@ -521,6 +526,10 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         }
         bool anyq2 = q2[0];
         if constexpr (K == 2) anyq2 |= q2[1];
+#ifdef SP_HULL_BRSTATS
+        if (__any_sync(FULL, anyq2) && lane == 0)
+          atomicAdd(reinterpret_cast<unsigned long long*>(p.ws + 80), 1ull);
+#endif
         if (__any_sync(FULL, anyq2)) {   // rare: the front moves by two or more
 #pragma unroll
           for (int k = 0; k < K; ++k) {

@@ -66,3 +66,7 @@ if os.environ.get("SP_TIMING_REPORT"):
         print(f"  {nm:28s} {v[8+i]/1e6:10.2f} Mcyc  ({v[8+i]/max(tot,1)*100:5.1f}% of phase total)" if i < 4 else f"  {nm:28s} {v[8+i]/1e6:10.2f} Mcyc")
     nw = 32
     print(f"  segment phase: mean warp busy / max warp busy = {v[12]/nw/max(v[13],1):.2f}")
+if os.environ.get("SP_BRSTATS_REPORT"):
+    v = ws[:128].view(torch.int64).cpu().tolist()
+    print(f"brstats: support rows (warp-steps) {v[8]}, back-pop loop taken {v[9]} ({v[9]/max(v[8],1)*100:.1f}%), "
+          f"front-pop loop taken {v[10]} ({v[10]/max(v[8],1)*100:.1f}%)  [counts summed over {a.reps} reps]")

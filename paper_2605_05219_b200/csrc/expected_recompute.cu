@@ -6,10 +6,14 @@
 //     cost = sum_i sum_{t in seg i} c_t (t - c_i) = T_N - sum_{i=1}^k c_i (P(c_{i+1}-1) - P(c_i-1))
 // (the w(s,j) decomposition of P:758 summed over the segments), and
 //     worst = max_i (c_{i+1} - c_i) - 1.
-// HBM-bound: one CTA per entry reads the histogram row once (coalesced) into 32-bin chunk
-// prefix sums kept in shared memory; each placement then needs k+1 prefix values
-// P(x) = chunk prefix + a <= 32-bin partial sum (L1/L2-resident row).  One warp per placement.
-// Count types are exact in int64; fp64 weights are accumulated in double-double.
+// Three kernels, all reading each histogram row once:
+//   eval_bcast_kernel   int32 counts, <= 4 placement sets shared by every entry (the Table 1
+//                       baselines; the bench's path): per-CTA tables l(t; C) in shared memory,
+//                       then a balanced streaming pass over (entry, slice) items.
+//   eval_p32_kernel     other int32 cases: the row's prefix sums in shared memory, one warp per
+//                       placement.
+//   eval_kernel         int64 / fp64 weights: 32-bin chunk prefix sums (double-double for fp64).
+// Count types are exact in int64.
 #include <cmath>
 #include <cstdlib>
 
@@ -302,6 +306,161 @@ __global__ void __launch_bounds__(EP_NT)
   }
 }
 
+// int32 counts, placements shared by every entry (broadcast: the Table 1 baselines): with the
+// reusable depth l(t; C) of every bin tabulated, the cost is a single streaming pass,
+//     cost = T_N - sum_t c_t l(t; C)      (l(t; C) = largest position <= t, 0 if none)
+// i.e. a product of the count matrix with S fixed columns l(.; C_s).  Each CTA (one per SM)
+// validates the sets, computes their worst cases and fills the uint16 tables l[s][t] in shared
+// memory once; then its warps stream row slices (EB_U coalesced loads in flight per lane, no
+// phases, no barriers), accumulate c_t t and c_t l[s][t] and add them into cost atomically.  HBM-bound: the row is
+// read once.  Exact in int64 (|c_t| < 2^31, t, l <= SP_MAX_N).
+#ifndef SP_EVAL_BCAST_NT
+#define SP_EVAL_BCAST_NT 1024
+#endif
+#ifndef SP_EVAL_BCAST_U
+#define SP_EVAL_BCAST_U 16
+#endif
+constexpr int EB_NT = SP_EVAL_BCAST_NT;
+constexpr int EB_U = SP_EVAL_BCAST_U;
+constexpr int EB_MAXS = 4;
+constexpr size_t EB_SMEM_MAX = 200 * 1024;   // tables: S (N+1) 2 bytes
+
+__device__ __forceinline__ long long mad_wide(int a, int b, long long c) {   // c + a b, exact
+  long long d;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+
+template <int SN>   // SN = S, the number of broadcast sets
+__global__ void __launch_bounds__(EB_NT, 1)
+    eval_bcast_kernel(const int32_t* __restrict__ w, int E, int N,
+                      const int32_t* __restrict__ positions, const int32_t* __restrict__ npos,
+                      int S, int max_pos, int64_t* __restrict__ cost, int32_t* __restrict__ worst) {
+  extern __shared__ __align__(16) uint16_t ltab[];   // [S][N+1]
+  __shared__ int sh_ok[SN], sh_gap[SN];
+  constexpr int NW = EB_NT / 32;
+  const int lane = lane_id(), wid = warp_id();
+  const int rowlen = N + 1;
+  // ---- sets: validity and worst case (warp q: set q) ---------------------------------------
+  if (wid < S) {
+    const int32_t* pc = positions + (int64_t)wid * max_pos;
+    const int k = npos[wid];
+    bool ok = k >= 0 && k <= max_pos;
+    int g = 0;
+    if (ok) {
+      for (int i = lane; i <= k; i += 32) {   // gap i: (c_i, c_{i+1})
+        const int ci = i == 0 ? 0 : pc[i - 1];
+        const int cn = i == k ? N + 1 : pc[i];
+        if (cn <= ci || cn > N + 1 || (i > 0 && ci < 1)) ok = false;
+        g = max(g, cn - ci);
+      }
+    }
+    ok = __all_sync(FULL, ok);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g = max(g, __shfl_xor_sync(FULL, g, o));
+    if (lane == 0) {
+      sh_ok[wid] = ok;
+      sh_gap[wid] = g;
+    }
+  }
+  __syncthreads();
+  // ---- tables: l[s][t] = c_i on segment i = [c_i, c_{i+1}) (one warp per segment) ------------
+  for (int s = 0; s < S; ++s) {
+    if (!sh_ok[s]) continue;
+    const int32_t* pc = positions + (int64_t)s * max_pos;
+    const int k = npos[s];
+    uint16_t* lt = ltab + (size_t)s * rowlen;
+    for (int i = wid; i <= k; i += NW) {
+      const int ci = i == 0 ? 0 : pc[i - 1];
+      const int cn = i == k ? N + 1 : pc[i];
+      for (int t = ci + lane; t < cn; t += 32) lt[t] = (uint16_t)ci;
+    }
+  }
+  __syncthreads();
+  // ---- work items: (entry, 32 EB_U-bin slice of its row).  Warp w takes the contiguous item
+  // range [w I / W, (w+1) I / W) (perfect balance, whatever E), reading slice i+1 while it
+  // computes slice i.  Lane l reads bins l, l + 32, ... (coalesced 128-byte loads,
+  // conflict-free table lookups).  The cost is linear in the bins, so a warp adds its share of
+  // an entry with one 64-bit atomic per set into cost (zeroed by the host call) when it leaves
+  // the entry; the slice-0 item writes the worst case and the flag of a malformed set (which
+  // receives no atomics).
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(ltab);
+  const uint32_t sstride = 2u * (uint32_t)rowlen;   // bytes between two sets' tables
+  constexpr int SL = 32 * EB_U;
+  const int nsl = (N + SL) / SL;   // slices per row (N + 1 bins)
+  const int64_t items = (int64_t)E * nsl;
+  const int64_t gw = (int64_t)blockIdx.x * NW + wid, nwt = (int64_t)gridDim.x * NW;
+  const int64_t i0 = items * gw / nwt, i1 = items * (gw + 1) / nwt;
+  if (i0 >= i1) return;
+  int e = (int)(i0 / nsl), sl = (int)(i0 - (int64_t)e * nsl);
+  int c[EB_U];
+  {
+    const int32_t* we = w + (int64_t)e * rowlen;
+#pragma unroll
+    for (int u = 0; u < EB_U; ++u) {
+      const int t = sl * SL + 32 * u + lane;
+      c[u] = t <= N ? __ldcs(we + t) : 0;
+    }
+  }
+  long long tsum = 0, acc[SN];
+#pragma unroll
+  for (int q = 0; q < SN; ++q) acc[q] = 0;
+  for (int64_t it = i0; it < i1; ++it) {
+    int en = e, sn = sl + 1;
+    if (sn == nsl) {
+      sn = 0;
+      ++en;
+    }
+    const bool more = it + 1 < i1;
+    int cn[EB_U];
+    {
+      const int32_t* we = w + (int64_t)en * rowlen;
+#pragma unroll
+      for (int u = 0; u < EB_U; ++u) {
+        const int t = sn * SL + 32 * u + lane;
+        cn[u] = more && t <= N ? __ldcs(we + t) : 0;
+      }
+    }
+    const int tb = sl * SL;
+#pragma unroll
+    for (int u = 0; u < EB_U; ++u) {
+      const int t = min(tb + 32 * u + lane, N);   // c = 0 past the row
+      tsum = mad_wide(c[u], t, tsum);
+      const uint32_t a = sbase + 2u * (uint32_t)t;
+#pragma unroll
+      for (int q = 0; q < SN; ++q) {
+        unsigned short l;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(l) : "r"(a + q * sstride));
+        acc[q] = mad_wide(c[u], (int)l, acc[q]);
+      }
+    }
+    if (sl == 0 && lane == 0) {
+#pragma unroll
+      for (int q = 0; q < SN; ++q) {
+        const int64_t oi = (int64_t)e * S + q;
+        if (!sh_ok[q]) cost[oi] = -1;
+        if (worst) worst[oi] = sh_ok[q] ? sh_gap[q] - 1 : -SP_ERR_BAD_POSITIONS;
+      }
+    }
+    if (sn == 0 || !more) {   // leaving entry e: add this warp's share
+      tsum = warp_sum(tsum);
+#pragma unroll
+      for (int q = 0; q < SN; ++q) {
+        const long long a = warp_sum(acc[q]);
+        if (lane == 0 && sh_ok[q])
+          atomicAdd(reinterpret_cast<unsigned long long*>(cost + (int64_t)e * S + q),
+                    (unsigned long long)(tsum - a));
+        acc[q] = 0;
+      }
+      tsum = 0;
+    }
+#pragma unroll
+    for (int u = 0; u < EB_U; ++u) c[u] = cn[u];
+    e = en;
+    sl = sn;
+  }
+}
+
 }  // namespace sp
 
 extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type wtype,
@@ -321,7 +480,21 @@ extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type w
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = n_entries < sms * 8 ? n_entries : sms * 8;
   cudaStream_t st = (cudaStream_t)stream;
-  if (wtype == SP_W_COUNTS_I32 && !getenv("SP_EVAL_CHUNKED")) {
+  const bool legacy = getenv("SP_EVAL_CHUNKED") || getenv("SP_EVAL_P32") || getenv("SP_EVAL_PREFIX");
+  const size_t tab = (size_t)n_sets * (N + 1) * sizeof(uint16_t);
+  if (wtype == SP_W_COUNTS_I32 && !legacy && broadcast && n_sets <= sp::EB_MAXS &&
+      tab <= sp::EB_SMEM_MAX) {
+    auto kern = n_sets == 1   ? sp::eval_bcast_kernel<1>
+                : n_sets == 2 ? sp::eval_bcast_kernel<2>
+                : n_sets == 3 ? sp::eval_bcast_kernel<3>
+                              : sp::eval_bcast_kernel<4>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab);
+    if (cudaMemsetAsync(cost, 0, (size_t)n_entries * n_sets * sizeof(int64_t), st) != cudaSuccess)
+      return SP_ERR_CUDA;
+    kern<<<sms, sp::EB_NT, tab, st>>>(
+        (const int32_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
+        (int64_t*)cost, worst_case);
+  } else if (wtype == SP_W_COUNTS_I32 && !getenv("SP_EVAL_CHUNKED")) {
     const int nseg = (N + 1 + 1023) / 1024;
     const bool wide = getenv("SP_EVAL_P32") != nullptr;   // 4-byte prefixes (tests / comparison)
     const size_t dyn = (size_t)nseg * 1024 * (wide ? 4 : 2);

@@ -374,6 +374,43 @@ def test_expected_recompute_prefix_widths(dev):
         assert (np_(cost) == rc).all() and (np_(worst) == rw).all(), env
 
 
+@pytest.mark.parametrize("N,E", [(32768, 12), (5, 37), (1000, 301)])
+def test_expected_recompute_broadcast_tables(dev, N, E):
+    """The broadcast path (<= 4 shared sets: per-CTA l(t; C) tables, one streaming pass per row)
+    against the oracle: W5-like and ragged shapes (entry counts not a multiple of the warps per
+    CTA, rows not a multiple of the warp width), an empty set, a malformed set, large counts; and
+    the same rows through a pointer that is not 16-byte aligned."""
+    import dataclasses
+    cfg = dataclasses.replace(wl.scaled(wl.CONFIGS["W5"], E), N=N)
+    rng = np.random.default_rng(N + E)
+    H = rng.integers(0, 50, size=(E, N + 1)).astype(np.int32)
+    H[rng.random((E, N + 1)) < 0.7] = 0
+    if N >= 1000:
+        H[:min(E, 4)] = wl.make_dense_hist(dataclasses.replace(cfg, N=N), seed=3).numpy()[:min(E, 4)]
+        H[1, 1:min(N, 2000)] = 2 ** 20           # large counts: int64 sums
+    sets = [sp.balanced_positions(N, min(N, 64)), [], sp.block_positions(N, max(1, N // 7))]
+    S = len(sets) + 1
+    width = max(len(s) for s in sets) + 1
+    pos = np.zeros((S, width), np.int32)
+    npos = np.zeros(S, np.int32)
+    for i, s in enumerate(sets):
+        pos[i, :len(s)] = s
+        npos[i] = len(s)
+    pos[3, :2] = [min(3, N), min(3, N)]        # malformed: not strictly increasing
+    npos[3] = 2
+    rc, rw = oracle.eval_batch(H, np.ascontiguousarray(pos[:3]), npos[:3], broadcast=True,
+                               nthreads=8)   # (the oracle rejects malformed sets outright)
+    Hd = torch.from_numpy(H).to(dev)
+    for Hin in (Hd, torch.empty(E * (N + 1) + 1, dtype=torch.int32, device=dev)[1:].view(E, N + 1)):
+        Hin.copy_(Hd)
+        cost, worst = sp.expected_recompute(Hin, torch.from_numpy(pos).to(dev),
+                                            torch.from_numpy(npos).to(dev), broadcast=True)
+        torch.cuda.synchronize()
+        assert (np_(cost)[:, :3] == rc).all() and (np_(worst)[:, :3] == rw).all()
+        assert (np_(cost)[:, 3] == -1).all()
+        assert (np_(worst)[:, 3] == -sp.SP_ERR_BAD_POSITIONS).all()
+
+
 def test_expected_recompute_dp_positions_and_bad_sets(dev):
     """E[r](DP output) == V_M, per-entry (non-broadcast) sets, malformed sets flagged."""
     cfg = wl.scaled(wl.CONFIGS["W3"], 16)

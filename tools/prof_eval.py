@@ -1,0 +1,42 @@
+"""Profiling driver for a6 (sp_expected_recompute) on W5-shaped dense histograms with the bench's
+baseline sets (balanced M, block B = 64 and 128): times the default (broadcast-table) kernel and the
+shared-prefix kernel (SP_EVAL_PREFIX) and checks that they agree on every entry."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_2605_05219_b200 import sp
+from paper_2605_05219_b200 import workload as wl
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--entries", type=int, default=16384)
+ap.add_argument("--workload", default="W5")
+ap.add_argument("--reps", type=int, default=5)
+a = ap.parse_args()
+cfg = wl.scaled(wl.CONFIGS[a.workload], a.entries)
+dev = torch.device("cuda:0")
+H = wl.make_dense_hist(cfg, seed=0, device=dev)
+bpos, bnpos, _ = sp.baseline_sets(cfg.N, budgets=(cfg.M,), blocks=(64, 128), device=dev)
+out = {}
+for name, env in (("bcast", None), ("prefix", "SP_EVAL_PREFIX")):
+    if env:
+        os.environ[env] = "1"
+    ts = []
+    for r in range(a.reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        c, w = sp.expected_recompute(H, bpos, bnpos, broadcast=True)
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    if env:
+        del os.environ[env]
+    out[name] = (c, w)
+    gb = H.numel() * 4 / 1e9
+    print(f"{name}: " + " ".join(f"{t:.3f}" for t in ts) + f" ms  ({gb:.2f} GB row bytes, "
+          f"{gb / min(ts) * 1e3:.0f} GB/s at best)", flush=True)
+print("agree:", bool(torch.equal(out["bcast"][0], out["prefix"][0])
+                     and torch.equal(out["bcast"][1], out["prefix"][1])))

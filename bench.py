@@ -26,7 +26,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DP cells/s (entries*N*M)"
-TRAFFIC_JSON = "r01f_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
+TRAFFIC_JSON = "r01g_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
 UNIT = "cells/s"
 
 
@@ -72,6 +72,9 @@ class ClockSampler:
         except OSError:
             self.p = None
 
+    def wait(self, event):
+        event.synchronize()
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -94,6 +97,61 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "samples": len(sm),
                 "reasons": sorted(reasons)}
+
+
+class NvmlClockSampler:
+    """Samples NVML from the host thread itself while it waits for the timed region's end event
+    (query + sample every ~3 ms), so even a ~200 ms region gets tens of samples taken while the
+    kernels run; ClockSampler (nvidia-smi) is the fallback."""
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu: int):
+        import pynvml
+        import torch
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        try:
+            pr = torch.cuda.get_device_properties(gpu)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+        self.bits = dict(zip(self.NAMES, (pynvml.nvmlClocksEventReasonHwSlowdown,
+                                          pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                                          pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                                          pynvml.nvmlClocksEventReasonSwPowerCap)))
+        self.sm, self.reasons = [], set()
+
+    def _sample(self):
+        nv = self.nv
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        for nm, b in self.bits.items():
+            if r & b:
+                self.reasons.add(nm)
+
+    def start(self):
+        pass
+
+    def wait(self, event):
+        """Sample until `event` (recorded at the end of the timed region) has completed."""
+        while True:
+            self._sample()
+            if event.query():
+                break
+            time.sleep(0.003)
+
+    def stop(self):
+        smax = float(self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": smax,
+                "samples": len(self.sm), "reasons": sorted(self.reasons), "source": "nvml"}
+
+
+def clock_sampler(gpu: int):
+    try:
+        return NvmlClockSampler(gpu)
+    except Exception:
+        return ClockSampler(gpu)
 
 
 def measured_peaks():
@@ -351,7 +409,7 @@ def run_ours(args):
 
     # ---- timed region (device-resident inputs) -----------------------------------------------
     marks = [[ev() for _ in range(5)] for _ in range(args.steps)]
-    clocks = ClockSampler(local)
+    clocks = clock_sampler(local)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -360,6 +418,7 @@ def run_ours(args):
     for k in range(args.steps):
         step(marks[k])
     t_end.record(stream)
+    clocks.wait(t_end)          # samples clocks while the timed steps run
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()

@@ -403,12 +403,16 @@ def test_expected_recompute_broadcast_tables(dev, N, E):
     Hd = torch.from_numpy(H).to(dev)
     for Hin in (Hd, torch.empty(E * (N + 1) + 1, dtype=torch.int32, device=dev)[1:].view(E, N + 1)):
         Hin.copy_(Hd)
-        cost, worst = sp.expected_recompute(Hin, torch.from_numpy(pos).to(dev),
-                                            torch.from_numpy(npos).to(dev), broadcast=True)
-        torch.cuda.synchronize()
-        assert (np_(cost)[:, :3] == rc).all() and (np_(worst)[:, :3] == rw).all()
-        assert (np_(cost)[:, 3] == -1).all()
-        assert (np_(worst)[:, 3] == -sp.SP_ERR_BAD_POSITIONS).all()
+        for S in (1, 2, 3, 4):   # every instantiation of the kernel (S is a template parameter)
+            cost, worst = sp.expected_recompute(Hin, torch.from_numpy(pos[:S].copy()).to(dev),
+                                                torch.from_numpy(npos[:S].copy()).to(dev),
+                                                broadcast=True)
+            torch.cuda.synchronize()
+            k = min(S, 3)
+            assert (np_(cost)[:, :k] == rc[:, :k]).all() and (np_(worst)[:, :k] == rw[:, :k]).all()
+            if S == 4:
+                assert (np_(cost)[:, 3] == -1).all()
+                assert (np_(worst)[:, 3] == -sp.SP_ERR_BAD_POSITIONS).all()
 
 
 def test_expected_recompute_dp_positions_and_bad_sets(dev):

@@ -527,6 +527,7 @@ def run_ours(args):
     value = E_tot * N * M * K / (ms_max / 1e3)
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    eval_bytes = E_own * (N + 1) * 4 + E_own * S * (8 + 4)   # rows read once; costs + worst
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
@@ -573,6 +574,13 @@ def run_ours(args):
                          "frac": lcp_bytes_all * K / (lcp_ms / 1e3) / 1e9 / world / hbm_peak,
                          "traffic": traffic.get("lcp_hist_kernel", {}).get("traffic_bytes"),
                          "algorithmic_bytes": lcp_bytes_all / world},
+        # a6 (eval_bcast_kernel): reads every histogram row once, writes E x S costs
+        "roofline_eval": {"bound": "hbm", "kernel": "eval_bcast_kernel",
+                          "achieved": eval_bytes * K / (eval_ms / 1e3) / 1e9,
+                          "peak": hbm_peak, "unit": "GB/s",
+                          "frac": eval_bytes * K / (eval_ms / 1e3) / 1e9 / hbm_peak,
+                          "traffic": traffic.get(f"eval_bcast_kernel<{S}>", {}).get("traffic_bytes"),
+                          "algorithmic_bytes": eval_bytes},
         "dp_paths": {k: v for k, v in stats.items()},
         # per step: lcp_hist, support_count (+ CUB's radix-sort kernels), dp_hull<int32>,
         # dp_hull<int64> (its list; exits at once when empty), dp_place (the D&C list; ditto),

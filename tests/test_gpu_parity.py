@@ -102,6 +102,59 @@ def test_lcp_clamp_ragged_and_bad_entries(dev):
     assert (np_(hist) == np_(base) + ref_h).all()
 
 
+def test_lcp_w5_full_size_sampled(dev):
+    """BASELINE's scale config at full size (16384 entries x N=32768, 20 requests each, ~36 GB of
+    request tokens) in the bench's launch configuration: sampled requests' LCPs and sampled
+    entries' whole histogram rows against the oracle's literal LCP loop, one by one; the
+    drawn depth (the LCP by construction) for every request."""
+    cfg = wl.CONFIGS["W5"]
+    tr = wl.make_trace(cfg, seed=0, device=dev)
+    E, N = cfg.n_entries, cfg.N
+    R = tr["req_off"].numel() - 1
+    lcp = torch.full((R,), -7, dtype=torch.int32, device=dev)
+    hist, _ = sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], tr["req_tokens"], tr["req_off"],
+                              tr["req_entry"], N, lcp_out=lcp, n_entries=E)
+    torch.cuda.synchronize()
+    assert torch.equal(lcp, torch.clamp(tr["depth"], max=N))
+    eo, ro, re_ = np_(tr["entry_off"]), np_(tr["req_off"]), np_(tr["req_entry"])
+    lcp_h = np_(lcp)
+
+    def one_entry(e, reqs):
+        et = np_(tr["entry_tokens"][int(eo[e]):int(eo[e + 1])])
+        rts = [np_(tr["req_tokens"][int(ro[r]):int(ro[r + 1])]) for r in reqs]
+        roff = np.concatenate([[0], np.cumsum([len(x) for x in rts])]).astype(np.int64)
+        rtok = np.concatenate(rts).astype(np.int32) if rts else np.zeros(0, np.int32)
+        return oracle.lcp_hist(et, np.array([0, len(et)], np.int64), rtok, roff,
+                               np.zeros(len(reqs), np.int32), N, n_entries=1)
+
+    rng = np.random.default_rng(0)
+    for r in rng.choice(R, 64, replace=False):       # sampled requests
+        _, rl = one_entry(int(re_[r]), [int(r)])
+        assert lcp_h[r] == rl[0], r
+    for e in (0, 1, 4097, 16383):                     # sampled entries: their whole rows
+        reqs = np.nonzero(re_ == e)[0]
+        rh, _ = one_entry(e, [int(r) for r in reqs])
+        assert (np_(hist[e]) == rh[0]).all(), e
+
+
+def test_expected_recompute_w5_full_size_sampled(dev):
+    """The bench's a6 call at full W5 size (16384 dense rows, the balanced-64 and block-64/128
+    sets, broadcast): sampled entries against the oracle's definitional evaluation; worst cases
+    against the closed forms at every entry."""
+    cfg = wl.CONFIGS["W5"]
+    H = wl.make_dense_hist(cfg, seed=0, device=dev)
+    pos, npos, labels = sp.baseline_sets(cfg.N, budgets=(cfg.M,), blocks=(64, 128), device=dev)
+    cost, worst = sp.expected_recompute(H, pos, npos, broadcast=True)
+    torch.cuda.synchronize()
+    rows = [0, 1, 2, 777, 4097, 8191, 12000, 16383]
+    rc, rw = oracle.eval_batch(np_(H[rows]), np_(pos), np_(npos), broadcast=True, nthreads=8)
+    assert (np_(cost)[rows] == rc).all() and (np_(worst)[rows] == rw).all()
+    N = cfg.N
+    assert (np_(worst)[:, 0] == -(-(N + 1) // (cfg.M + 1)) - 1).all()   # Thm 1.2 tail
+    assert (np_(worst)[:, 1] == 63).all() and (np_(worst)[:, 2] == 127).all()   # block B: B - 1
+    assert (np_(cost) >= 0).all()
+
+
 def test_accumulate_depths(dev):
     rng = np.random.default_rng(5)
     n, E, N = 20000, 50, 700

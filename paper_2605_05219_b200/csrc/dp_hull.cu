@@ -435,8 +435,9 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         // lane 0 slot 0 from the previous pass (or e_0 = 0)
         VT in[K];
         const VT t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
-        VT ext = 0;
-        if (chain_in) ext = __shfl_sync(FULL, Ec, q);
+        // unconditional (Ec = 0 without a previous pass): the row's shuffles stay in one
+        // converged region, so ptxas emits one divergence check (BRA.DIV) for all of them
+        const VT ext = __shfl_sync(FULL, Ec, q);
         in[0] = lane ? t0 : ext;
         if constexpr (K == 2) {
           const VT t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);

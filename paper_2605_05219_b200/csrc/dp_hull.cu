@@ -625,6 +625,10 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
   VT* ebuf1 = ebuf0 + hull_align(8 * (size_t)(N + 1)) / sizeof(VT);
   unsigned long long pops = 0, events = 0;
   int done_entries = 0;
+#ifdef SP_HULL_TAIL   // instrumentation (tools/prof_dp.py, SP_TAIL_REPORT): warp busy vs span
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
 
   for (;;) {
     int it = 0;
@@ -796,6 +800,17 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
               (unsigned long long)done_entries);
     atomicAdd(&stats->hull_event_rows, events);
   }
+#ifdef SP_HULL_TAIL
+  if (!WIDE && lane == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    unsigned long long* tw = reinterpret_cast<unsigned long long*>(p.ws + 88);
+    atomicMax(tw + 0, t_end);              // last warp's end
+    atomicMax(tw + 1, ~t_start);           // first warp's start (max of the complement)
+    atomicAdd(tw + 2, t_end - t_start);    // summed warp busy time
+    atomicAdd(tw + 3, 1ull);               // warps
+  }
+#endif
 }
 
 // Longest-processing-time order: an entry's hull work is (support rows) x M, and entries are

@@ -50,6 +50,12 @@ for r in range(a.reps):
           f"Mcells/s={a.entries*cfg.N*M/s.elapsed_time(e)/1e3:.1f}  "
           f"hull={st['entries_hull']} support_rows/entry={st['hull_event_rows']/max(1,st['entries_hull']):.0f} "
           f"pops/support-cell={st['hull_pops']/max(1,st['hull_event_rows']*M):.3f}", flush=True)
+if os.environ.get("SP_TAIL_REPORT"):   # needs SP_NVCC_EXTRA=-DSP_HULL_TAIL; last rep
+    v = ws[:128].view(torch.int64).cpu().tolist()
+    end, nstart, busy, nw = v[11], v[12], v[13], v[14]
+    span = end - (2**64 - 1 - (nstart & (2**64 - 1)))   # t_start = ~(stored complement)
+    print(f"tail: {nw} warps, span {span/1e6:.3f} ms, mean warp busy {busy/max(nw,1)/1e6:.3f} ms, "
+          f"utilisation {busy/max(nw,1)/max(span,1):.3f}")
 if a.lcp:
     tr = wl.make_trace(cfg, seed=0, device=dev)
     lcp = torch.empty(tr["req_off"].numel() - 1, dtype=torch.int32, device=dev)

@@ -37,52 +37,53 @@ def short(name):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--full", required=True)
+    ap.add_argument("--full")
     ap.add_argument("--launches")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--cmd", default="")
     a = ap.parse_args()
-    raw = subprocess.run(["ncu", "-i", a.full, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout.splitlines()
-    rows = list(csv.reader(raw))
-    hdr, units = rows[0], rows[1]
-    out_txt = [f"# ncu --set full --clock-control none: `{a.cmd}`",
-               f"# report: {os.path.basename(a.full)} (not committed); first captured launch per kernel", ""]
-    traffic = {}
-    seen = set()
-    for r in rows[2:]:
-        kn = r[hdr.index("Kernel Name")]
-        sk = short(kn)
-        if sk in seen:
-            continue
-        seen.add(sk)
-        out_txt.append(f"== {kn[:110]}")
-        vals = {}
-        for k in KEYS:
-            if k in hdr:
-                i = hdr.index(k)
-                out_txt.append(f"   {k:76s} {r[i]} {units[i]}")
-                try:
-                    vals[k] = float(r[i].replace(",", "")) * UNIT.get(units[i], 1.0)
-                except ValueError:
-                    pass
-        st = [(h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""),
-               float(r[i] or 0)) for i, h in enumerate(hdr)
-              if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")]
-        st.sort(key=lambda x: -x[1])
-        out_txt.append("   top stall reasons (warps stalled per issued instruction):")
-        for nme, v in st[:8]:
-            out_txt.append(f"      {nme:30s} {v:.3f}")
-        out_txt.append("")
-        rd, wr = vals.get("dram__bytes_read.sum"), vals.get("dram__bytes_write.sum")
-        traffic[sk] = {"dram_read_bytes": rd, "dram_write_bytes": wr,
-                       "traffic_bytes": (rd + wr) if rd is not None and wr is not None else None,
-                       "duration_ns": vals.get("gpu__time_duration.sum", 0) * 1e6
-                       if "gpu__time_duration.sum" in vals else None,
-                       "inst_executed": vals.get("smsp__inst_executed.sum")}
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    open(os.path.join(ROOT, "profiles", f"{a.tag}_ncu_full.txt"), "w").write("\n".join(out_txt) + "\n")
-    json.dump(traffic, open(os.path.join(ROOT, "profiles", f"{a.tag}_ncu_traffic.json"), "w"), indent=1)
+    if a.full:
+        raw = subprocess.run(["ncu", "-i", a.full, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout.splitlines()
+        rows = list(csv.reader(raw))
+        hdr, units = rows[0], rows[1]
+        out_txt = [f"# ncu --set full --clock-control none: `{a.cmd}`",
+                   f"# report: {os.path.basename(a.full)} (not committed); first captured launch per kernel", ""]
+        traffic = {}
+        seen = set()
+        for r in rows[2:]:
+            kn = r[hdr.index("Kernel Name")]
+            sk = short(kn)
+            if sk in seen:
+                continue
+            seen.add(sk)
+            out_txt.append(f"== {kn[:110]}")
+            vals = {}
+            for k in KEYS:
+                if k in hdr:
+                    i = hdr.index(k)
+                    out_txt.append(f"   {k:76s} {r[i]} {units[i]}")
+                    try:
+                        vals[k] = float(r[i].replace(",", "")) * UNIT.get(units[i], 1.0)
+                    except ValueError:
+                        pass
+            st = [(h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""),
+                   float(r[i] or 0)) for i, h in enumerate(hdr)
+                  if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")]
+            st.sort(key=lambda x: -x[1])
+            out_txt.append("   top stall reasons (warps stalled per issued instruction):")
+            for nme, v in st[:8]:
+                out_txt.append(f"      {nme:30s} {v:.3f}")
+            out_txt.append("")
+            rd, wr = vals.get("dram__bytes_read.sum"), vals.get("dram__bytes_write.sum")
+            traffic[sk] = {"dram_read_bytes": rd, "dram_write_bytes": wr,
+                           "traffic_bytes": (rd + wr) if rd is not None and wr is not None else None,
+                           "duration_ns": vals.get("gpu__time_duration.sum", 0) * 1e6
+                           if "gpu__time_duration.sum" in vals else None,
+                           "inst_executed": vals.get("smsp__inst_executed.sum")}
+        os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+        open(os.path.join(ROOT, "profiles", f"{a.tag}_ncu_full.txt"), "w").write("\n".join(out_txt) + "\n")
+        json.dump(traffic, open(os.path.join(ROOT, "profiles", f"{a.tag}_ncu_traffic.json"), "w"), indent=1)
     if a.launches:
         lines = [ln for ln in open(a.launches) if not ln.startswith("==")]
         lr = list(csv.reader(lines))
@@ -101,7 +102,8 @@ def main():
         for k, v in agg.items():
             out.append(f"{k:44s} {len(v):8d} {sum(v) / len(v):10.3f} {sum(v) / tot * 100:7.1f}%")
         open(os.path.join(ROOT, "profiles", f"{a.tag}_launches.txt"), "w").write("\n".join(out) + "\n")
-    print(open(os.path.join(ROOT, "profiles", f"{a.tag}_ncu_full.txt")).read())
+    if a.full:
+        print(open(os.path.join(ROOT, "profiles", f"{a.tag}_ncu_full.txt")).read())
 
 
 if __name__ == "__main__":

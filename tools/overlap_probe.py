@@ -5,7 +5,8 @@ entries are cut into C blocks (requests are grouped by entry, so a block's reque
 contiguous); the LCP of block c runs on the main stream, and block c's DP + evaluation run on
 one of two side streams (own workspace each) once its LCP is done, so LCP(c+1) runs beside
 DP(c) and each DP launch's tail is filled by the next one's warps.  Prints both step times and
-checks that the two schedules give identical outputs.  W5, device-resident inputs.
+checks that the two schedules give identical outputs; also times the evaluation on a side
+stream beside the DP (it needs only the histograms).  W5, device-resident inputs.
 """
 import argparse
 import os
@@ -86,6 +87,20 @@ def step_overlap(o, C):
         main.wait_stream(s)
 
 
+def step_eval_side(o):
+    """The evaluation needs only the histograms: run it on a side stream beside the DP, where
+    its CTAs can take the SMs the DP's tail leaves idle."""
+    lcp(o, 0, R, main)
+    ev = torch.cuda.Event()
+    ev.record(main)
+    side[0].wait_event(ev)
+    sp.expected_recompute(o["hist"], bpos, bnpos, broadcast=True, cost=o["bcost"],
+                          worst=o["bworst"], stream=side[0])
+    sp.place_checkpoints(o["hist"], M, positions=o["positions"], n_positions=o["npos"],
+                         cost=o["cost"], cost_by_budget=o["cbb"], workspace=ws[0], stream=main)
+    main.wait_stream(side[0])
+
+
 def timed(fn, o):
     for _ in range(a.warmup):
         o["hist"].copy_(hist0)
@@ -107,6 +122,10 @@ def timed(fn, o):
 ref = outputs()
 t_ser = timed(step_serial, ref)
 print(f"serial: {t_ser:.3f} ms/step", flush=True)
+o = outputs()
+t = timed(step_eval_side, o)
+print(f"eval on a side stream beside the DP: {t:.3f} ms/step ({t_ser / t:.3f}x)  outputs identical: "
+      f"{all(torch.equal(ref[k], o[k]) for k in ref)}", flush=True)
 for C in a.chunks:
     o = outputs()
     t = timed(lambda x: step_overlap(x, C), o)

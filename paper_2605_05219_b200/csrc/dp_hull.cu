@@ -39,6 +39,7 @@
 // own log only when it changes (uint32: j << 16 | opt); the backtrack finds the last entry with
 // row <= j by a warp-cooperative 32-way search.  Outputs per entry: V_m = T_N + e_m(N) for every
 // m (cost_by_budget), the rule-B backtrack (positions, count), the f3 frontier.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cub/device/device_radix_sort.cuh>
@@ -108,6 +109,13 @@ __host__ __device__ __forceinline__ size_t hull_slot_bytes(int N, int M) {
 }
 __host__ __device__ __forceinline__ size_t hull_smem_bytes(int) { return 0; }   // static rings
 
+// per-entry row statistics from row_stats_kernel (integer weights)
+struct HullRowStat {
+  long long n, tn;   // P_N and T_N (int64; valid when !bad)
+  int tfirst;        // first non-zero bin (INT_MAX if none)
+  int bad;           // a negative count or one >= 2^40
+};
+
 struct HullParams {
   const void* w;
   int E, N, M;
@@ -125,6 +133,7 @@ struct HullParams {
   int32_t* wide;    // entries for the int64 instantiation
   const int32_t* order;   // processing order of the entries (largest support first), or NULL
   int logcap;             // argmin-log entries usable per layer (hull_log_cap(N); tests lower it)
+  const HullRowStat* rstat;   // n, T_N, first bin, guards per entry (integer weights), or NULL
 };
 
 __host__ __device__ __forceinline__ size_t hull_pool_bytes(int M) {
@@ -259,6 +268,14 @@ struct SRingI {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a + ds), "h"((unsigned short)v.s) : "memory");
   }
   static constexpr int cap(int k) { return k ? C1 : C0; }
+  static constexpr int UNIT = 1;
+  static constexpr size_t bytes(int K) { return (size_t)(C0 + (K == 2 ? C1 : 0)) * 192; }
+  __device__ __forceinline__ void ld2(int k, int pos, int& b, int& sv) const {
+    const Line<int> l = ld(k, pos);
+    b = l.b;
+    sv = l.s;
+  }
+  __device__ __forceinline__ void st2(int k, int pos, int b, int sv) const { st(k, pos, Line<int>{b, sv}); }
 };
 
 // 12-byte lines for the int64 / fp64 instantiations, interleaved like SRingI: a 384-byte
@@ -599,7 +616,6 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
   constexpr bool WIDE = std::is_same<VT, long long>::value;
   const int lane = threadIdx.x;
   constexpr int C0 = WIDE ? HW0 : HC0, C1 = WIDE ? HW1 : HC1;
-  constexpr int NPOS = C0 + (K == 2 ? C1 : 0);   // ring positions of this warp
   extern __shared__ __align__(16) uint8_t sring[];   // ring_bytes<K, VT>()
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
   using SR = typename std::conditional<std::is_same<VT, int>::value, SRingI<C0, C1>,
@@ -668,21 +684,29 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
     } else {
       long long n = 0, tn = 0;
       int bad = 0;
+      if (p.rstat) {   // from row_stats_kernel: the DP reads the row once
+        const HullRowStat rs = p.rstat[e];
+        n = rs.n;
+        tn = rs.tn;
+        tfirst = rs.tfirst;
+        bad = rs.bad;
+      } else {
 #pragma unroll 8
-      for (int t = lane + 1; t <= N; t += 32) {
-        const long long c = (long long)we[t];
-        bad |= (c < 0) | (c >= (1ll << 40));
-        if (!bad) {
-          n += c;
-          tn += (long long)t * c;
+        for (int t = lane + 1; t <= N; t += 32) {
+          const long long c = (long long)we[t];
+          bad |= (c < 0) | (c >= (1ll << 40));
+          if (!bad) {
+            n += c;
+            tn += (long long)t * c;
+          }
+          if (c > 0 && t < tfirst) tfirst = t;
         }
-        if (c > 0 && t < tfirst) tfirst = t;
-      }
-      bad = __any_sync(FULL, bad);
-      n = warp_sum(n);
-      tn = warp_sum(tn);
+        bad = __any_sync(FULL, bad);
+        n = warp_sum(n);
+        tn = warp_sum(tn);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tfirst = min(tfirst, __shfl_xor_sync(FULL, tfirst, o));
+        for (int o = 16; o > 0; o >>= 1) tfirst = min(tfirst, __shfl_xor_sync(FULL, tfirst, o));
+      }
       // int32 path: 2 n N < 2^31 (the D&C kernel's "narrow" condition: every intercept,
       // candidate and difference exact in int32); int64 path: n N < 2^46 (differences < 2^46,
       // cross products < 2^62); otherwise (or negative counts) the D&C kernel
@@ -813,23 +837,450 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
 #endif
 }
 
-// Longest-processing-time order: an entry's hull work is (support rows) x M, and entries are
-// taken from a counter, so starting the largest first trims the kernel's tail (W5: 52 -> 43 ms).
+// ---------------------------------------------------------------------------------------------
+// The lean int32 step (dp_lean_kernel): the same CHT, the same lockstep layers and the same
+// outputs as dp_hull_kernel<.., int>, with a step cut to what the pop statistics need
+// (tools/hull_stats.c on W5 rows: per (row, layer) 40% of pushes pop nothing from the back, 39%
+// one line, 15% two; 91% pop nothing from the front, 8% one).
+//  * The back line, the one below it, the front line and the one after it live in registers;
+//    the only eager shared load per row is the line two below the back (for a second back test).
+//  * Back test = one 64-bit sign test: with the new point as origin, line B goes iff
+//    Ab' Bs' - As' Bb' >= 0 (two IMAD.WIDE, the second accumulating; one ISETP on the high word).
+//  * The front block runs only when some lane pops its front line; the argmin log is appended
+//    there (opt_m changes exactly when the front line changes).
+//  * The row's (j, P_j) come from a per-chunk compacted list in shared memory (one broadcast load
+//    per row); P_{j-1} is the previous support row's P (zero rows do not change P).
+//  * n, T_N, the first non-zero bin and the guards come from row_stats_kernel (one read of every
+//    row, shared with the largest-first ordering), so the DP reads each histogram row once.
+// Entries whose deque outgrows a ring or whose argmin log fills are listed for the int64
+// instantiation of dp_hull_kernel (larger rings, then the global ring, then the D&C), which is
+// exact for them too.
+
+// 8-byte lines (intercept b, s) in 256-byte position rows, [slot][position][lane]: one LDS.64 /
+// STS.64 per line, every lane in its own banks whatever its position.  Positions are kept
+// pre-multiplied by 256 so that an address is (p8 & mask) + the lane's base.
+template <int C0, int C1>
+struct LRing {
+  uint32_t lb;   // shared address of slot 0, row 0, this lane's line
+  static constexpr int cap(int k) { return k ? C1 : C0; }
+  static constexpr uint32_t off(int k) { return k ? (uint32_t)C0 * 256u : 0u; }
+  __device__ __forceinline__ uint32_t at(int k, int p8) const {
+    return ((uint32_t)p8 & (uint32_t)((cap(k) - 1) << 8)) + lb + off(k);
+  }
+  __device__ __forceinline__ void ld(int k, int p8, int& b, int& sv) const {
+    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(b), "=r"(sv) : "r"(at(k, p8)));
+  }
+  __device__ __forceinline__ void st(int k, int p8, int b, int sv) const {
+    asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(at(k, p8)), "r"(b), "r"(sv) : "memory");
+  }
+  static constexpr size_t bytes(int K) { return (size_t)(C0 + (K == 2 ? C1 : 0)) * 256; }
+  static constexpr int UNIT = 256;
+  __device__ __forceinline__ void ld2(int k, int p8, int& b, int& sv) const { ld(k, p8, b, sv); }
+  __device__ __forceinline__ void st2(int k, int p8, int b, int sv) const { st(k, p8, b, sv); }
+};
+
+__device__ __forceinline__ bool hi_nonneg(long long w) { return (int)(w >> 32) >= 0; }
+
+template <int K, bool ALLACT, bool CHAIN, typename WT, class RG>
+__device__ __forceinline__ bool lean_dp(const HullParams& p, const WT* __restrict__ we, int e,
+                                        long long TN, const RG rg, uint32_t* logs,
+                                        int32_t* logn, int* ebuf0, int* ebuf1, int2* sev,
+                                        unsigned& pops_e, unsigned& ev_e, bool& logfull) {
+  const int lane = lane_id();
+  const int N = p.N, M = p.M;
+  const int LC = p.logcap;
+  constexpr int L = 32 * K;
+  const int passes = (M + L - 1) / L;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  constexpr int U = RG::UNIT;   // position unit (x256 for LRing's pre-shifted counters)
+  bool ovf = false;
+  logfull = false;
+  for (int ps = 0; ps < passes && !ovf; ++ps) {
+    const int* ein = (ps & 1) ? ebuf1 : ebuf0;
+    int* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
+    const bool chain_out = ps + 1 < passes;
+    // per slot: deque positions fr8 <= bk8 (x 256); the back line is always the previous row's
+    // line (B0b, s = jp); B1 = the line below it; F0, F1 = the front line and the next one
+    int fr8[K], bk8[K], cnt[K], eo[K];
+    int B0b[K], B1b[K], B1s[K], F0b[K], F0s[K], F1b[K], F1s[K];
+    bool act[K];
+    uint32_t* lg[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int mk = ps * L + 32 * k + lane + 1;
+      act[k] = ALLACT || mk <= M;
+      fr8[k] = 0;
+      bk8[k] = 0;
+      eo[k] = 0;    // e_m(0) = 0 (reading R1)
+      cnt[k] = 1;   // log entry 0: opt_m(1) = 1 whatever the row type
+      lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * LC;
+      if (act[k]) lg[k][0] = (1u << 16) | 1u;
+      // dummy front line (+inf at every query, s = 0), popped by the first row's front test
+      B0b[k] = B1b[k] = F0b[k] = F1b[k] = INT_MAX;
+      B1s[k] = F0s[k] = F1s[k] = 0;
+      rg.st2(k, 0, INT_MAX, 0);
+    }
+    int carry = 0, Pm1 = 0, jp = 0, evbase = 0;
+    // the counts are prefetched four chunks ahead (a chunk holds only ~5 support rows on W5)
+    int cq[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cq[c] = 32 * c + 1 + lane <= N ? (int)__ldcs(we + 32 * c + 1 + lane) : 0;
+    const uint32_t sev_a = (uint32_t)__cvta_generic_to_shared(sev);
+    for (int jb = 0; jb < N; jb += 32) {
+      const int jr = jb + 1 + lane;
+      const int craw = cq[0];
+      cq[0] = cq[1];
+      cq[1] = cq[2];
+      cq[2] = cq[3];
+      cq[3] = jr + 128 <= N ? (int)__ldcs(we + jr + 128) : 0;
+      const unsigned evmask = __ballot_sync(FULL, craw > 0);
+      if (evmask == 0) continue;
+      int Pc = craw;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, Pc, o);
+        if (lane >= o) Pc += y;
+      }
+      Pc += carry;
+      carry = __shfl_sync(FULL, Pc, 31);
+      if (craw > 0)
+        asm volatile("st.shared.v2.s32 [%0], {%1, %2};" ::"r"(sev_a + 8u * __popc(evmask & lt_mask)),
+                     "r"(jr), "r"(Pc) : "memory");
+      const int nev = __popc(evmask);
+      int Ec = 0;
+      if (CHAIN && ps > 0 && lane < nev) Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
+      __syncwarp();
+      for (int q = 0; q < nev; ++q) {
+        int j, x;
+        asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(j), "=r"(x) : "r"(sev_a + 8u * q));
+        // e_{m-1}(j-1) from the lane below (its value at the previous support row)
+        int in[K];
+        const int t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
+        if constexpr (CHAIN) {
+          const int ext = __shfl_sync(FULL, Ec, q);
+          in[0] = lane ? t0 : ext;
+        } else {
+          in[0] = lane ? t0 : 0;
+        }
+        if constexpr (K == 2) {
+          const int t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
+          in[1] = lane ? t1 : t0;
+        }
+        ++ev_e;
+        const int d0s = jp - j;   // (back line - new line).s, the same for every lane and slot
+        // ---- ring lines two below the back and two after the front (positions known) ------
+        int B2b[K], B2s[K], G2b[K], G2s[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          rg.ld2(k, bk8[k] - 2 * U, B2b[k], B2s[k]);
+          rg.ld2(k, fr8[k] + 2 * U, G2b[k], G2s[k]);
+        }
+        // ---- back: two pop tests, with the new point (j, nb) as origin: line B goes iff
+        //      (A - N).b (B - N).s - (A - N).s (B - N).b >= 0 for its predecessor A
+        int nb[K], top8[K];
+        bool p1[K], p2[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          nb[k] = in[k] + j * Pm1;
+          const int sz8 = bk8[k] - fr8[k];
+          const int d0b = B0b[k] - nb[k];
+          const int n1s = j - B1s[k], d1b = B1b[k] - nb[k];
+          p1[k] = act[k] & (sz8 >= U) & hi_nonneg((long long)d1b * d0s + (long long)n1s * d0b);
+          const int d2b = B2b[k] - nb[k], n2s = j - B2s[k];
+          p2[k] = p1[k] & (sz8 >= 2 * U) & hi_nonneg((long long)d2b * (-n1s) + (long long)n2s * d1b);
+          top8[k] = bk8[k] - 2 * U;
+        }
+        bool any2 = p2[0];
+        if constexpr (K == 2) any2 |= p2[1];
+        if (__any_sync(FULL, any2)) {   // a lane popped two lines: keep testing from the ring
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            bool more = p2[k];
+            int cs = B2s[k] - j, cb = B2b[k] - nb[k];
+            while (more && top8[k] - fr8[k] >= U) {
+              int lb, ls;
+              rg.ld2(k, top8[k] - U, lb, ls);
+              more = hi_nonneg((long long)(lb - nb[k]) * cs + (long long)(j - ls) * cb);
+              if (more) {
+                top8[k] -= U;
+                cs = ls - j;
+                cb = lb - nb[k];
+                B2b[k] = lb;
+                B2s[k] = ls;
+              }
+            }
+          }
+        }
+        int v0[K];
+        bool q1[K], q2[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          // push: the new line's predecessor becomes B1
+          const int t8 = p2[k] ? top8[k] : (p1[k] ? bk8[k] - U : bk8[k]);
+          B1b[k] = p1[k] ? (p2[k] ? B2b[k] : B1b[k]) : B0b[k];
+          B1s[k] = p1[k] ? (p2[k] ? B2s[k] : B1s[k]) : jp;
+          B0b[k] = nb[k];
+          bk8[k] = t8 + U;
+          ovf |= act[k] & (bk8[k] - fr8[k] >= RG::cap(k) * U);
+          rg.st2(k, bk8[k], nb[k], j);
+          // ---- front: up to two pops decided from registers; F1 / the line after it are the
+          //      new line when the back reached them
+          const bool e1 = bk8[k] == fr8[k] + U, e2 = bk8[k] == fr8[k] + 2 * U;
+          F1b[k] = e1 ? nb[k] : F1b[k];
+          F1s[k] = e1 ? j : F1s[k];
+          const int Gb = e2 ? nb[k] : G2b[k], Gs = e2 ? j : G2s[k];
+          v0[k] = F0b[k] - F0s[k] * x;
+          const int v1 = F1b[k] - F1s[k] * x;
+          const int vg = Gb - Gs * x;
+          q1[k] = act[k] & (v1 < v0[k]);
+          q2[k] = q1[k] & (bk8[k] - fr8[k] >= 2 * U) & (vg < v1);
+          F0b[k] = q2[k] ? Gb : (q1[k] ? F1b[k] : F0b[k]);
+          F0s[k] = q2[k] ? Gs : (q1[k] ? F1s[k] : F0s[k]);
+          v0[k] = q2[k] ? vg : (q1[k] ? v1 : v0[k]);
+          F1b[k] = q1[k] ? Gb : F1b[k];   // (after two pops the loop reloads F1)
+          F1s[k] = q1[k] ? Gs : F1s[k];
+          fr8[k] += q1[k] ? (q2[k] ? 2 * U : U) : 0;
+        }
+        bool a2 = q2[0];
+        if constexpr (K == 2) a2 |= q2[1];
+        while (__any_sync(FULL, a2)) {   // rare: the front moves by two or more
+          a2 = false;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            if (q2[k]) {
+              q2[k] = false;
+              if (fr8[k] < bk8[k]) {
+                int lb, ls;
+                rg.ld2(k, fr8[k] + U, lb, ls);
+                F1b[k] = lb;
+                F1s[k] = ls;
+                const int vl = lb - ls * x;
+                if (vl < v0[k]) {
+                  F0b[k] = lb;
+                  F0s[k] = ls;
+                  v0[k] = vl;
+                  fr8[k] += U;
+                  q2[k] = true;
+                }
+              }
+            }
+            a2 |= q2[k];
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (q1[k]) lg[k][cnt[k]++] = ((uint32_t)j << 16) | (uint32_t)F0s[k];   // < LC
+          eo[k] = v0[k];
+        }
+        Pm1 = x;
+        jp = j;
+        if (chain_out && lane == 31) eout_buf[evbase + q] = eo[K - 1];
+      }
+      evbase += nev;
+      bool full = false;
+#pragma unroll
+      for (int k = 0; k < K; ++k) full |= (LC <= N) & (cnt[k] > LC - 33);   // 32 rows of headroom
+      logfull = __any_sync(FULL, full);
+      if (__any_sync(FULL, ovf) || logfull) {
+        ovf = true;
+        break;
+      }
+      __syncwarp();   // sev is rewritten by the next chunk
+    }
+    if (!ovf) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (!act[k]) continue;
+        pops_e += (unsigned)(evbase - bk8[k] / U) + (unsigned)(fr8[k] / U - 1);
+        const int mk = ps * L + 32 * k + lane + 1;
+        logn[ps * L + 32 * k + lane] = cnt[k];
+        const long long V = TN + (long long)eo[k];   // V_m = T_N + e_m(N)
+        if (p.cbb) reinterpret_cast<long long*>(p.cbb)[(int64_t)e * (M + 1) + mk] = V;
+        if (mk == M) reinterpret_cast<long long*>(p.cost)[e] = V;
+      }
+    }
+    __syncwarp();
+  }
+  return ovf;
+}
+
+// a5 rule-B backtrack from the argmin-change logs (reading R3): the warp for budget M, one lane
+// per budget for the f3 frontier.  Shared by dp_hull_kernel and dp_lean_kernel.
+template <int K>
+__device__ __forceinline__ void hull_backtrack(const HullParams& p, int e, int tfirst,
+                                               const uint32_t* logs, const int32_t* logn) {
+  const int lane = lane_id();
+  const int N = p.N, M = p.M;
+  int32_t* out = p.pos + (int64_t)e * M;
+  int k = 0, j = N, m = M;
+  while (m > 0 && j >= tfirst) {   // P_j > 0  <=>  j >= first non-zero bin
+    const int ls = hull_layer_slot(K, m);
+    const int s = log_lookup_warp(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
+    if (lane == 0) out[k] = s;
+    ++k;
+    j = s - 1;
+    --m;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    for (int a = 0, z = k - 1; a < z; ++a, --z) {
+      const int t = out[a];
+      out[a] = out[z];
+      out[z] = t;
+    }
+    p.npos[e] = k;
+  }
+  for (int q = k + lane; q < M; q += 32) out[q] = 0;
+  if (p.fpos) {
+    for (int mb = lane + 1; mb <= M; mb += 32) {
+      int32_t* fo = p.fpos + ((int64_t)e * M + (mb - 1)) * M;
+      int kk = 0, jj = N, mm = mb;
+      while (mm > 0 && jj >= tfirst) {
+        const int ls = hull_layer_slot(K, mm);
+        const int s = log_lookup_lane(logs + (size_t)ls * hull_log_cap(N), logn[ls], jj);
+        fo[kk++] = s;
+        jj = s - 1;
+        --mm;
+      }
+      for (int a = 0, z = kk - 1; a < z; ++a, --z) {
+        const int t = fo[a];
+        fo[a] = fo[z];
+        fo[z] = t;
+      }
+      for (int q = kk; q < M; ++q) fo[q] = 0;
+      p.fn[(int64_t)e * M + mb - 1] = kk;
+    }
+  }
+}
+
+// the lean kernel's ring: 6-byte lines (SRingI, 12 warps/SM at 64/32 lines) by default;
+// -DSP_LEAN_RING8 selects 8-byte lines in 256-byte rows (LRing: one LDS.64 per line, 9 warps/SM)
+#ifdef SP_LEAN_RING8
+using LeanRing = LRing<HC0, HC1>;
+#else
+using LeanRing = SRingI<HC0, HC1>;
+#endif
+
+template <int K>
+static constexpr size_t lean_smem_bytes() {
+  return LeanRing::bytes(K) + 32 * sizeof(int2);
+}
+
+// One warp per entry (1-warp CTAs, persistent, largest support first).  Entries beyond the int32
+// guard (2 n N >= 2^31) are listed for the int64 instantiation of dp_hull_kernel, bad rows
+// (negative counts) for the D&C kernel.
+template <typename WT, int K>
+__global__ void __launch_bounds__(32, 1) dp_lean_kernel(HullParams p, const HullRowStat* rstat) {
+  const int lane = threadIdx.x;
+  extern __shared__ __align__(16) uint8_t sring[];
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
+  LeanRing srg;
+#ifdef SP_LEAN_RING8
+  srg.lb = sbase + 8u * (uint32_t)lane;
+#else
+  srg.b0 = sbase + 4u * (uint32_t)lane;
+  srg.ds = 128u - 2u * (uint32_t)lane;
+#endif
+  int2* sev = reinterpret_cast<int2*>(sring + LeanRing::bytes(K));
+  const int N = p.N, M = p.M;
+  sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
+  unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
+  unsigned* wide_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_WIDE_COUNT_OFF);
+  unsigned* ectr = reinterpret_cast<unsigned*>(p.ws + SP_WS_ENTRY_CTR_OFF);
+  uint8_t* slot = p.slots + (size_t)blockIdx.x * p.slot;
+  uint32_t* logs = reinterpret_cast<uint32_t*>(slot);
+  int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
+  int* ebuf0 = reinterpret_cast<int*>(slot + hull_log_bytes(N, M) + hull_cnt_bytes(M));
+  int* ebuf1 = ebuf0 + hull_align(8 * (size_t)(N + 1)) / sizeof(int);
+  unsigned long long pops = 0, events = 0;
+  int done_entries = 0;
+  const bool fullm = M % (32 * K) == 0;
+  const bool chained = hull_passes(M) > 1;
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = (int)atomicAdd(ectr, 1u);
+    it = __shfl_sync(FULL, it, 0);
+    if (it >= p.E) break;
+    const int e = p.order ? p.order[it] : it;
+    const HullRowStat rs = rstat[e];
+    if (rs.bad || rs.n >= (1ll << 30) / N) {   // int32 guard: 2 n N < 2^31
+      if (lane == 0) {
+        if (!rs.bad && rs.n < (1ll << 46) / N) p.wide[atomicAdd(wide_n, 1u)] = e;
+        else p.fb[atomicAdd(fb_n, 1u)] = e;
+      }
+      continue;
+    }
+    const WT* we = reinterpret_cast<const WT*>(p.w) + (int64_t)e * (N + 1);
+    if (lane == 0 && p.cbb) reinterpret_cast<long long*>(p.cbb)[(int64_t)e * (M + 1)] = rs.tn;
+    unsigned pops_e = 0, ev_e = 0;
+    bool logfull = false, ovf;
+    if (fullm && !chained)
+      ovf = lean_dp<K, true, false, WT>(p, we, e, rs.tn, srg, logs, logn, ebuf0, ebuf1, sev, pops_e, ev_e, logfull);
+    else if (!chained)
+      ovf = lean_dp<K, false, false, WT>(p, we, e, rs.tn, srg, logs, logn, ebuf0, ebuf1, sev, pops_e, ev_e, logfull);
+    else
+      ovf = lean_dp<K, false, true, WT>(p, we, e, rs.tn, srg, logs, logn, ebuf0, ebuf1, sev, pops_e, ev_e, logfull);
+    if (ovf) {   // ring or log full: the int64 instantiation re-runs the entry
+      if (lane == 0) p.wide[atomicAdd(wide_n, 1u)] = e;
+      continue;
+    }
+    pops += pops_e;
+    events += ev_e;
+    __threadfence_block();
+    __syncwarp();
+    hull_backtrack<K>(p, e, rs.tfirst, logs, logn);
+    ++done_entries;
+    __syncwarp();   // the slot is rewritten by the next entry
+  }
+  pops = warp_sum(pops);
+  if (lane == 0) {
+    atomicAdd(&stats->hull_pops, pops);
+    atomicAdd(&stats->entries_hull, (unsigned long long)done_entries);
+    atomicAdd(&stats->entries_i32, (unsigned long long)done_entries);
+    atomicAdd(&stats->hull_event_rows, events);
+  }
+}
+
+// One pass over every row (one warp per row): the support count (the largest-first order's key),
+// and for integer weights n = P_N, T_N, the first non-zero bin and the guards that dp_lean_kernel
+// needs before it starts (so the DP itself reads each row once).
 template <typename WT>
-__global__ void __launch_bounds__(256) support_count_kernel(const WT* __restrict__ w, int E, int N,
-                                                            int32_t* __restrict__ key,
-                                                            int32_t* __restrict__ val) {
+__global__ void __launch_bounds__(256) row_stats_kernel(const WT* __restrict__ w, int E, int N,
+                                                        int32_t* __restrict__ key,
+                                                        int32_t* __restrict__ val,
+                                                        HullRowStat* __restrict__ rstat) {
   const int lane = lane_id();
   const int nw = gridDim.x * 8;
   for (int e = blockIdx.x * 8 + warp_id(); e < E; e += nw) {
     const WT* we = w + (int64_t)e * (N + 1);
-    int c = 0;
+    int c = 0, bad = 0, tfirst = INT_MAX;
+    long long n = 0, tn = 0;
 #pragma unroll 8
-    for (int t = lane + 1; t <= N; t += 32) c += __ldcs(we + t) != WT(0);
+    for (int t = lane + 1; t <= N; t += 32) {
+      const WT v = __ldcs(we + t);
+      c += v != WT(0);
+      if constexpr (!std::is_same<WT, double>::value) {
+        const long long cv = (long long)v;
+        bad |= (cv < 0) | (cv >= (1ll << 40));
+        n += cv;
+        tn += (long long)t * cv;
+        if (cv > 0 && t < tfirst) tfirst = t;
+      }
+    }
     c = warp_sum(c);
+    if constexpr (!std::is_same<WT, double>::value) {
+      n = warp_sum(n);
+      tn = warp_sum(tn);
+      bad = __any_sync(FULL, bad);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tfirst = min(tfirst, __shfl_xor_sync(FULL, tfirst, o));
+    }
     if (lane == 0) {
-      key[e] = c;
-      val[e] = e;
+      if (key) {
+        key[e] = c;
+        val[e] = e;
+      }
+      if (rstat) rstat[e] = HullRowStat{n, tn, tfirst, bad};
     }
   }
 }
@@ -842,50 +1293,107 @@ static constexpr size_t ring_bytes() {
   return (size_t)NPOS * 192;
 }
 
-template <typename WT, int K, typename VT>
-static int hull_grid_t(int E) {
-  int dev = 0, sms = 148, occ = 1;
+// Host-side launch facts cached per device (the verdict's host-overhead item: no attribute,
+// occupancy or getenv calls on every sp_place_checkpoints call once warm).
+constexpr int HULL_MAX_DEV = 64;
+static int dev_sms() {
+  static int sms[HULL_MAX_DEV] = {0};
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  constexpr size_t dyn = ring_bytes<K, VT>();
-  cudaFuncSetAttribute(dp_hull_kernel<WT, K, VT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)dyn);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_hull_kernel<WT, K, VT>, 32, dyn);
-  if (occ < 1) occ = 1;
-  long g = (long)sms * occ;
+  if (dev < 0 || dev >= HULL_MAX_DEV) dev = 0;
+  if (!sms[dev]) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = v;
+  }
+  return sms[dev];
+}
+// resident 1-warp CTAs per SM for a kernel with `dyn` bytes of dynamic shared memory (sets the
+// opt-in attribute once per device)
+template <typename KernelT>
+static int occ_cached(KernelT kern, size_t dyn, int* cache) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= HULL_MAX_DEV) dev = 0;
+  if (!cache[dev]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, dyn);
+    cache[dev] = occ < 1 ? 1 : occ;
+  }
+  return cache[dev];
+}
+
+static int clamp_grid(long g, int E) {
   if (g > E) g = E;
   return (int)(g < 1 ? 1 : g);
 }
 
+template <typename WT, int K, typename VT>
+static int hull_grid_t(int E) {
+  static int cache[HULL_MAX_DEV] = {0};
+  const int occ = occ_cached(dp_hull_kernel<WT, K, VT>, ring_bytes<K, VT>(), cache);
+  return clamp_grid((long)dev_sms() * occ, E);
+}
+
 template <typename WT, int K>
-static void hull_launch_t(const HullParams& p, int gn, cudaStream_t st) {
+static int lean_grid_t(int E) {
+  static int cache[HULL_MAX_DEV] = {0};
+  const int occ = occ_cached(dp_lean_kernel<WT, K>, lean_smem_bytes<K>(), cache);
+  return clamp_grid((long)dev_sms() * occ, E);
+}
+
+// SP_HULL_LEAN=1 runs the int32 path on dp_lean_kernel instead of dp_hull_kernel<.., int>
+// (measured: faster on sparse rows, slower on W5's); read once per process
+static bool hull_lean() {
+  static const bool v = getenv("SP_HULL_LEAN") != nullptr;
+  return v;
+}
+
+template <typename WT, int K>
+static void hull_launch_t(const HullParams& p, const HullRowStat* rstat, int gn, cudaStream_t st) {
   if constexpr (std::is_same<WT, double>::value) {
     dp_hull_kernel<double, K, double><<<gn, 32, ring_bytes<K, double>(), st>>>(p);
   } else {
-    dp_hull_kernel<WT, K, int><<<gn, 32, ring_bytes<K, int>(), st>>>(p);
-    // the int64 instantiation on the listed entries (its warps exit at once if the list is empty)
-    dp_hull_kernel<WT, K, long long><<<hull_grid_t<WT, K, long long>(p.E), 32,
-                                       ring_bytes<K, long long>(), st>>>(p);
+    if (!hull_lean()) {
+      dp_hull_kernel<WT, K, int><<<gn, 32, ring_bytes<K, int>(), st>>>(p);
+    } else {
+      const int gl = std::min(gn, lean_grid_t<WT, K>(p.E));
+      dp_lean_kernel<WT, K><<<gl, 32, lean_smem_bytes<K>(), st>>>(p, rstat);
+    }
+    // the int64 instantiation on the listed entries (its warps exit at once if the list is
+    // empty); its grid is clamped to the slots allocated for the widest launch
+    const int gw = std::min(gn, hull_grid_t<WT, K, long long>(p.E));
+    dp_hull_kernel<WT, K, long long><<<gw, 32, ring_bytes<K, long long>(), st>>>(p);
   }
 }
 
 }  // namespace sp
 
-// the int32 instantiation has the largest grid; the int64 one uses a prefix of its slots
+// slots are allocated for the largest grid any launch of this weight type uses
 int sp_hull_grid(int E, int N, int M, int wtype) {
   (void)N;
   const bool k2 = sp::hull_K(M) == 2;
   if (wtype == SP_W_PROB_F64)
     return k2 ? sp::hull_grid_t<double, 2, double>(E) : sp::hull_grid_t<double, 1, double>(E);
+  int g;
   if (wtype == SP_W_COUNTS_I64)
-    return k2 ? sp::hull_grid_t<int64_t, 2, int>(E) : sp::hull_grid_t<int64_t, 1, int>(E);
-  return k2 ? sp::hull_grid_t<int32_t, 2, int>(E) : sp::hull_grid_t<int32_t, 1, int>(E);
+    g = k2 ? std::max(std::max(sp::hull_grid_t<int64_t, 2, int>(E), sp::lean_grid_t<int64_t, 2>(E)),
+                      sp::hull_grid_t<int64_t, 2, long long>(E))
+           : std::max(std::max(sp::hull_grid_t<int64_t, 1, int>(E), sp::lean_grid_t<int64_t, 1>(E)),
+                      sp::hull_grid_t<int64_t, 1, long long>(E));
+  else
+    g = k2 ? std::max(std::max(sp::hull_grid_t<int32_t, 2, int>(E), sp::lean_grid_t<int32_t, 2>(E)),
+                      sp::hull_grid_t<int32_t, 2, long long>(E))
+           : std::max(std::max(sp::hull_grid_t<int32_t, 1, int>(E), sp::lean_grid_t<int32_t, 1>(E)),
+                      sp::hull_grid_t<int32_t, 1, long long>(E));
+  return g;
 }
 
 size_t sp_hull_slot_bytes(int N, int M) { return sp::hull_slot_bytes(N, M); }
 size_t sp_hull_pool_bytes(int M) { return sp::hull_pool_bytes(M); }
 
-// ordering scratch: key/val in, key/val out (int32 [E] each) | cub temp
+// ordering scratch: key/val in, key/val out (int32 [E] each) | cub temp | row stats [E]
 static size_t order_cub_bytes(int E) {
   size_t b = 0;
   cub::DeviceRadixSort::SortPairsDescending(nullptr, b, (const int32_t*)nullptr, (int32_t*)nullptr,
@@ -893,34 +1401,50 @@ static size_t order_cub_bytes(int E) {
   return b;
 }
 size_t sp_hull_order_bytes(int E) {
-  return 4 * sp::hull_align(4 * (size_t)E) + sp::hull_align(order_cub_bytes(E));
+  return 4 * sp::hull_align(4 * (size_t)E) + sp::hull_align(order_cub_bytes(E)) +
+         sp::hull_align(sizeof(sp::HullRowStat) * (size_t)E);
 }
 
 cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
                            int32_t* npos, void* cost, void* cbb, int32_t* fpos,
                            int32_t* fn, uint8_t* ws, int32_t* fb, int32_t* wide, uint8_t* pool,
                            uint8_t* order_ws, uint8_t* slots, int grid, cudaStream_t st) {
+  static const bool no_order = getenv("SP_HULL_NO_ORDER") != nullptr;   // comparison hook
+  static const int logcap_env = [] {
+    const char* lc = getenv("SP_HULL_LOGCAP");   // test hook: force the log-full fallback
+    return lc ? atoi(lc) : 0;
+  }();
   sp::HullParams p;
   p.order = nullptr;
-  if (order_ws && E > 1 && !getenv("SP_HULL_NO_ORDER")) {
-    const size_t a = sp::hull_align(4 * (size_t)E);
-    int32_t* kin = (int32_t*)order_ws;
-    int32_t* vin = (int32_t*)(order_ws + a);
-    int32_t* kout = (int32_t*)(order_ws + 2 * a);
-    int32_t* vout = (int32_t*)(order_ws + 3 * a);
-    size_t tb = order_cub_bytes(E);
-    int blocks = (E + 7) / 8;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    if (wtype == SP_W_PROB_F64)
-      sp::support_count_kernel<double><<<blocks, 256, 0, st>>>((const double*)weights, E, N, kin, vin);
-    else if (wtype == SP_W_COUNTS_I64)
-      sp::support_count_kernel<int64_t><<<blocks, 256, 0, st>>>((const int64_t*)weights, E, N, kin, vin);
-    else
-      sp::support_count_kernel<int32_t><<<blocks, 256, 0, st>>>((const int32_t*)weights, E, N, kin, vin);
-    if (cub::DeviceRadixSort::SortPairsDescending(order_ws + 4 * a, tb, kin, kout, vin, vout, E, 0,
+  const size_t a = sp::hull_align(4 * (size_t)E);
+  int32_t* kin = (int32_t*)order_ws;
+  int32_t* vin = (int32_t*)(order_ws + a);
+  int32_t* kout = (int32_t*)(order_ws + 2 * a);
+  int32_t* vout = (int32_t*)(order_ws + 3 * a);
+  const size_t tb = order_cub_bytes(E);
+  sp::HullRowStat* rstat =
+      reinterpret_cast<sp::HullRowStat*>(order_ws + 4 * a + sp::hull_align(tb));
+  const bool order = E > 1 && !no_order;
+  int blocks = (E + 7) / 8;
+  if (blocks > sp::dev_sms() * 8) blocks = sp::dev_sms() * 8;
+  if (wtype == SP_W_PROB_F64) {
+    if (order)
+      sp::row_stats_kernel<double><<<blocks, 256, 0, st>>>((const double*)weights, E, N, kin, vin,
+                                                           nullptr);
+  } else if (wtype == SP_W_COUNTS_I64) {
+    sp::row_stats_kernel<int64_t><<<blocks, 256, 0, st>>>((const int64_t*)weights, E, N,
+                                                          order ? kin : nullptr, vin, rstat);
+  } else {
+    sp::row_stats_kernel<int32_t><<<blocks, 256, 0, st>>>((const int32_t*)weights, E, N,
+                                                          order ? kin : nullptr, vin, rstat);
+  }
+  if (order) {
+    size_t tbv = tb;
+    if (cub::DeviceRadixSort::SortPairsDescending(order_ws + 4 * a, tbv, kin, kout, vin, vout, E, 0,
                                                   32, st) == cudaSuccess)
       p.order = vout;
   }
+  p.rstat = wtype == SP_W_PROB_F64 ? nullptr : rstat;
   p.gring = pool;
   p.wide = wide;
   p.w = weights;
@@ -938,20 +1462,17 @@ cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, 
   p.slots = slots;
   p.slot = sp::hull_slot_bytes(N, M);
   p.logcap = sp::hull_log_cap(N);
-  if (const char* lc = getenv("SP_HULL_LOGCAP")) {   // test hook: force the log-full fallback
-    const int v = atoi(lc);
-    if (v >= 1 && v < p.logcap) p.logcap = v;
-  }
+  if (logcap_env >= 1 && logcap_env < p.logcap) p.logcap = logcap_env;
   const bool k2 = sp::hull_K(M) == 2;
   if (wtype == SP_W_PROB_F64) {
-    if (k2) sp::hull_launch_t<double, 2>(p, grid, st);
-    else sp::hull_launch_t<double, 1>(p, grid, st);
+    if (k2) sp::hull_launch_t<double, 2>(p, rstat, grid, st);
+    else sp::hull_launch_t<double, 1>(p, rstat, grid, st);
   } else if (wtype == SP_W_COUNTS_I64) {
-    if (k2) sp::hull_launch_t<int64_t, 2>(p, grid, st);
-    else sp::hull_launch_t<int64_t, 1>(p, grid, st);
+    if (k2) sp::hull_launch_t<int64_t, 2>(p, rstat, grid, st);
+    else sp::hull_launch_t<int64_t, 1>(p, rstat, grid, st);
   } else {
-    if (k2) sp::hull_launch_t<int32_t, 2>(p, grid, st);
-    else sp::hull_launch_t<int32_t, 1>(p, grid, st);
+    if (k2) sp::hull_launch_t<int32_t, 2>(p, rstat, grid, st);
+    else sp::hull_launch_t<int32_t, 1>(p, rstat, grid, st);
   }
   return cudaGetLastError();
 }

@@ -213,14 +213,80 @@ def test_hull_f64_path_vs_exact(dev):
     assert (np.abs(d["cost"] - r["cost"]) <= 1e-12 * exact).all()
 
 
+LOGFULL_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import oracle
+from paper_2605_05219_b200 import sp, workload as wl
+dev = torch.device('cuda:0')
+c = wl.TraceConfig('t', 10, 700, 8, 1, (700, 700), (1, 1), 'mix', dense_n=(233, 350))
+H = wl.make_dense_hist(c, seed=21).numpy()
+w = torch.as_tensor(H).to(dev).contiguous()
+ws = torch.empty(sp.place_checkpoints_workspace_bytes(10, 700, 40), dtype=torch.uint8, device=dev)
+pos, npos, cost, cbb = sp.place_checkpoints(w, 40, cost_by_budget=True, workspace=ws)
+torch.cuda.synchronize()
+assert sp.dp_stats(ws)['entries_hull'] < 10
+pos, npos, cost, cbb = (t.cpu().numpy() for t in (pos, npos, cost, cbb))
+for e in range(10):
+    rp, rc, rcbb = oracle.place(H[e].astype(np.int64), 40, 'naive')
+    k = len(rp)
+    assert npos[e] == k and pos[e, :k].tolist() == rp.tolist() and cost[e] == rc, e
+    assert (cbb[e] == rcbb).all(), e
+print('logfull ok')
+"""
+
+
+def run_with_env(script, **env):
+    """The library reads its test hooks (SP_HULL_LOGCAP, SP_HULL_LEAN, ...) once per process:
+    run the check in a fresh interpreter with them set."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", script, root], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    return r.returncode, r.stdout + r.stderr
+
+
 def test_hull_log_full_falls_back(dev):
     """Entries whose argmin-change log fills (forced with a tiny capacity) are solved by the
     D&C kernel instead -- same outputs as the oracle."""
-    H = dense(10, 700, seed=21)
-    os.environ["SP_HULL_LOGCAP"] = "3"
-    try:
-        r = place(H, 40, dev)
-    finally:
-        del os.environ["SP_HULL_LOGCAP"]
-    assert r["stats"]["entries_hull"] < 10
-    check(H, 40, r, algo="naive")
+    rc, out = run_with_env(LOGFULL_SCRIPT, SP_HULL_LOGCAP="3")
+    assert rc == 0 and "logfull ok" in out, out
+
+
+LEAN_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import oracle
+from paper_2605_05219_b200 import sp, workload as wl
+dev = torch.device('cuda:0')
+cases = []
+cfg = wl.scaled(wl.CONFIGS['W5'], 24)
+cases.append((wl.make_dense_hist(cfg, seed=7).numpy(), 64))
+for N, M, seed in ((3000, 40, 3), (700, 17, 5), (2048, 8, 6)):
+    c = wl.TraceConfig('t', 16, N, M, 1, (N, N), (1, 1), 'mix', dense_n=(N // 4, N // 2))
+    cases.append((wl.make_dense_hist(c, seed=seed).numpy(), M))
+H = np.zeros((4, 2001), np.int64); H[0, 1:] = 1; H[1, 5] = 9; H[3, ::7] = 2
+cases.append((H, 40))   # all-ones (ring overflow -> int64 instantiation), point mass, empty, sparse
+for H, M in cases:
+    w = torch.as_tensor(H).to(torch.int32).to(dev).contiguous()
+    E, N = w.shape[0], w.shape[1] - 1
+    ws = torch.empty(sp.place_checkpoints_workspace_bytes(E, N, M), dtype=torch.uint8, device=dev)
+    pos, npos, cost, cbb = sp.place_checkpoints(w, M, cost_by_budget=True, workspace=ws)
+    torch.cuda.synchronize()
+    pos, npos, cost, cbb = (t.cpu().numpy() for t in (pos, npos, cost, cbb))
+    for e in range(E):
+        rp, rc, rcbb = oracle.place(H[e].astype(np.int64), M, 'cht')
+        k = len(rp)
+        assert npos[e] == k and pos[e, :k].tolist() == rp.tolist() and cost[e] == rc, (N, M, e)
+        assert (cbb[e] == rcbb).all(), (N, M, e)
+print('lean ok')
+"""
+
+
+def test_lean_kernel_matches_oracle(dev):
+    """dp_lean_kernel (SP_HULL_LEAN=1, read once per process: a subprocess) against the oracle's
+    CHT on W5 rows, smaller dense configs, the all-ones row (its ring overflow goes to the int64
+    instantiation), a point mass, an empty row and a sparse row."""
+    rc, out = run_with_env(LEAN_SCRIPT, SP_HULL_LEAN="1")
+    assert rc == 0 and "lean ok" in out, out

@@ -37,8 +37,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="W5", choices=["W2", "W3", "W4", "W5"])
-    ap.add_argument("--entries", type=int, default=None, help="entries per GPU (default: config)")
+    ap.add_argument("--entries", type=int, default=None,
+                    help="entries in total (strong) or per GPU (weak); default: the config's")
     ap.add_argument("--merge", default="sparse", choices=["sparse", "allreduce"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's entries split over the GPUs (BASELINE configs[4]); "
+                         "weak: the config's entries on every GPU")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=8, help="entry blocks of the pipelined e2e")
@@ -262,10 +266,10 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     cells = s["E"] * s["N"] * s["M"] * args.steps
     v = cells / dt
-    cfg = workload_config(args, 1, None)
+    cfg = workload_config(args, max(args.gpus, world), None)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads, "kind": "oracle",
                              "sample": f"first {s['E']} entries of {args.workload} per step"},
@@ -276,18 +280,116 @@ def run_reference(args):
 def workload_config(args, world, extra):
     from paper_2605_05219_b200 import workload as wl
     cfg = wl.CONFIGS[args.workload]
-    E = args.entries or cfg.n_entries
-    d = {"workload": f"{args.workload}: {E} entries/GPU x N={cfg.N} x M={cfg.M}",
-         "entries_per_gpu": E, "entries_total": E * world, "N": cfg.N, "M": cfg.M,
+    E_tot, E = plan_entries(args, cfg, world)
+    d = {"workload": f"{args.workload}: {E_tot} entries x N={cfg.N} x M={cfg.M}"
+                     + (f" ({E}/GPU)" if world > 1 else ""),
+         "entries_per_gpu": E, "entries_total": E_tot, "N": cfg.N, "M": cfg.M,
          "requests_per_entry": cfg.req_per_entry, "lcp_law": cfg.shape,
          "dp_hist": (f"dense depth-mode, n~U{list(cfg.dense_n)} draws/entry, {cfg.dense_shape} "
                      f"laws, + the step's requests" if cfg.dense_n else "from the LCP requests"),
-         "parallelism": f"entries sharded over {world} GPU(s)",
+         "parallelism": f"entries sharded over {world} GPU(s) ({args.scaling} scaling)",
          "merge": None if world == 1 else args.merge,
          "l2": "inputs larger than L2 (request tokens and histograms >> 126 MB)"}
     if extra:
         d.update(extra)
     return d
+
+
+# ---------------------------------------------------------------------------------------------
+# one rank's resident state and step (shared by the GPU arm and the gloo CPU test of the N > 1
+# path, tests/test_bench_gloo.py, which passes CPU stand-ins as `ops`)
+# ---------------------------------------------------------------------------------------------
+def plan_entries(args, cfg, world):
+    """(E_total, E_own).  Strong scaling (default): BASELINE.json configs[4] is "16k entries ...
+    sharded across 8xB200", so the total is the config's and each rank owns E_total / N.
+    Weak: each rank owns the config's entry count."""
+    if args.scaling == "strong":
+        E_tot = args.entries or cfg.n_entries
+        if E_tot % world:
+            raise SystemExit(f"strong scaling: {E_tot} entries do not split over {world} ranks")
+        return E_tot, E_tot // world
+    E_own = args.entries or cfg.n_entries
+    return E_own * world, E_own
+
+
+class HotPath:
+    """Rank `rank` of `world`: owns entries [rank E_own, (rank+1) E_own) of E_tot, holds their
+    resident histograms, this rank's batch of new requests (routed at random),
+    the outputs and the DP workspace.  step(): a1+a2 LCP-histogram of the batch, the merge
+    (world > 1: the one exchange step, paper_2605_05219_b200.dist), a3-a5 DP on the owned
+    entries, a6 baseline evaluation."""
+
+    def __init__(self, cfg, E_tot, E_own, world, rank, merge, seed, dev, ops=None):
+        import torch
+        from paper_2605_05219_b200 import workload as wl
+        if ops is None:
+            from paper_2605_05219_b200 import sp as ops
+        self.ops, self.world, self.merge_mode = ops, world, merge
+        self.E_tot, self.E_own, self.N, self.M = E_tot, E_own, cfg.N, cfg.M
+        self.e0 = rank * E_own
+        N, M = cfg.N, cfg.M
+        tcfg = wl.scaled(cfg, E_tot)
+        self.tr = tr = wl.make_trace(tcfg, seed=seed, device=dev, world=world, rank=rank)
+        self.R = tr["req_off"].numel() - 1
+        if cfg.dense_n:
+            self.hist = wl.make_dense_hist(tcfg, seed=seed, device=dev, entry_begin=self.e0,
+                                           n_entries=E_own)
+        else:
+            self.hist = torch.zeros(E_own, N + 1, dtype=torch.int32, device=dev)
+        budgets = cfg.M_sweep if cfg.M_sweep else (M,)
+        self.bpos, self.bnpos, self.labels = ops.baseline_sets(N, budgets=budgets,
+                                                               blocks=(64, 128), device=dev)
+        self.S = S = self.bpos.shape[0]
+        self.positions = torch.empty(E_own, M, dtype=torch.int32, device=dev)
+        self.npos = torch.empty(E_own, dtype=torch.int32, device=dev)
+        self.cost = torch.empty(E_own, dtype=torch.int64, device=dev)
+        self.cbb = torch.empty(E_own, M + 1, dtype=torch.int64, device=dev)
+        self.bcost = torch.empty(E_own, S, dtype=torch.int64, device=dev)
+        self.bworst = torch.empty(E_own, S, dtype=torch.int32, device=dev)
+        self.ws = torch.empty(ops.place_checkpoints_workspace_bytes(E_own, N, M),
+                              dtype=torch.uint8, device=dev)
+        self.lcp = torch.full((max(self.R, 1),), -1, dtype=torch.int32, device=dev)
+        self.merger = None
+        if world > 1:
+            from paper_2605_05219_b200.dist import HistMerger
+            self.merger = HistMerger(tr["req_entry"], E_own, N, mode=merge,
+                                     accumulate=ops.accumulate_depths)
+
+    def step(self, stream=None, marks=None):
+        ops, tr, N, M = self.ops, self.tr, self.N, self.M
+        if marks:
+            marks[0].record(stream)
+        # a1 + a2
+        if self.world == 1:
+            ops.overlap_hist(tr["entry_tokens"], tr["entry_off"], tr["req_tokens"], tr["req_off"],
+                             tr["req_entry"], N, hist=self.hist, lcp_out=self.lcp,
+                             n_entries=self.E_tot, stream=stream)
+        elif self.merge_mode == "sparse":
+            ops.overlap_hist(tr["entry_tokens"], tr["entry_off"], tr["req_tokens"], tr["req_off"],
+                             tr["req_entry"], N, lcp_out=self.merger.lcp_out,
+                             n_entries=self.E_tot, stream=stream, with_hist=False)
+        else:
+            ops.overlap_hist(tr["entry_tokens"], tr["entry_off"], tr["req_tokens"], tr["req_off"],
+                             tr["req_entry"], N, hist=self.merger.partial, lcp_out=self.lcp,
+                             n_entries=self.E_tot, stream=stream)
+        if marks:
+            marks[1].record(stream)
+        # merge (the one exchange step, SURVEY 8(e))
+        if self.world > 1:
+            self.merger.merge(self.hist, stream=stream)
+        if marks:
+            marks[2].record(stream)
+        # a3 - a5
+        ops.place_checkpoints(self.hist, M, positions=self.positions, n_positions=self.npos,
+                              cost=self.cost, cost_by_budget=self.cbb, workspace=self.ws,
+                              stream=stream)
+        if marks:
+            marks[3].record(stream)
+        # a6
+        ops.expected_recompute(self.hist, self.bpos, self.bnpos, broadcast=True, cost=self.bcost,
+                               worst=self.bworst, stream=stream)
+        if marks:
+            marks[4].record(stream)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -314,31 +416,14 @@ def run_ours(args):
     sp.lib()
 
     cfg = wl.CONFIGS[args.workload]
-    E_own = args.entries or cfg.n_entries
-    E_tot = E_own * world
-    e0, e1 = rank * E_own, (rank + 1) * E_own
+    E_tot, E_own = plan_entries(args, cfg, world)
+    e0 = rank * E_own
     N, M = cfg.N, cfg.M
-    tcfg = wl.scaled(cfg, E_tot)
-
-    # ---- inputs (resident in HBM before timing) ------------------------------------------------
-    tr = wl.make_trace(tcfg, seed=args.seed, device=dev, world=world, rank=rank)
-    R = tr["req_off"].numel() - 1
-    if cfg.dense_n:
-        hist = wl.make_dense_hist(tcfg, seed=args.seed, device=dev, entry_begin=e0,
-                                  n_entries=E_own)
-    else:
-        hist = torch.zeros(E_own, N + 1, dtype=torch.int32, device=dev)
-    budgets = cfg.M_sweep if cfg.M_sweep else (M,)
-    bpos, bnpos, labels = sp.baseline_sets(N, budgets=budgets, blocks=(64, 128), device=dev)
-    S = bpos.shape[0]
-    positions = torch.empty(E_own, M, dtype=torch.int32, device=dev)
-    npos = torch.empty(E_own, dtype=torch.int32, device=dev)
-    cost = torch.empty(E_own, dtype=torch.int64, device=dev)
-    cbb = torch.empty(E_own, M + 1, dtype=torch.int64, device=dev)
-    bcost = torch.empty(E_own, S, dtype=torch.int64, device=dev)
-    bworst = torch.empty(E_own, S, dtype=torch.int32, device=dev)
-    ws = torch.empty(sp.place_checkpoints_workspace_bytes(E_own, N, M), dtype=torch.uint8,
-                     device=dev)
+    hp = HotPath(cfg, E_tot, E_own, world, rank, args.merge, args.seed, dev)
+    tr, hist, R = hp.tr, hp.hist, hp.R
+    positions, npos, cost, cbb, bcost, bworst = (hp.positions, hp.npos, hp.cost, hp.cbb,
+                                                 hp.bcost, hp.bworst)
+    bpos, bnpos, S, ws, lcp = hp.bpos, hp.bnpos, hp.S, hp.ws, hp.lcp
 
     # tokens examined by the LCP (generator depths): sum min(t+1, len, L_e)
     d = torch.minimum(tr["depth"].to(torch.int64), torch.tensor(N, device=dev))
@@ -353,48 +438,12 @@ def run_ours(args):
     ent_max.scatter_reduce_(0, tr["req_entry"].long(), examined, reduce="amax")
     lcp_bytes = 4 * tokens_examined + 4 * int(ent_max.sum()) + R * (4 + 16 + 16 + 4 + 4)
 
-    lcp = torch.full((max(R, 1),), -1, dtype=torch.int32, device=dev)
-    merger = None
-    if world > 1:
-        from paper_2605_05219_b200.dist import HistMerger
-        merger = HistMerger(tr["req_entry"], E_own, N, mode=args.merge)
-
     stream = torch.cuda.current_stream(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-
     req_tokens, req_off, req_entry = tr["req_tokens"], tr["req_off"], tr["req_entry"]
 
     def step(marks=None):
-        if marks:
-            marks[0].record(stream)
-        # a1 + a2
-        if world == 1:
-            sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], req_tokens, req_off, req_entry,
-                            N, hist=hist, lcp_out=lcp, n_entries=E_tot, stream=stream)
-        elif args.merge == "sparse":
-            sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], req_tokens, req_off, req_entry,
-                            N, lcp_out=merger.lcp_out, n_entries=E_tot, stream=stream,
-                            with_hist=False)
-        else:
-            sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], req_tokens, req_off, req_entry,
-                            N, hist=merger.partial, lcp_out=lcp, n_entries=E_tot, stream=stream)
-        if marks:
-            marks[1].record(stream)
-        # merge (the one exchange step; paper_2605_05219_b200.dist)
-        if world > 1:
-            merger.merge(hist, stream=stream)
-        if marks:
-            marks[2].record(stream)
-        # a3 - a5
-        sp.place_checkpoints(hist, M, positions=positions, n_positions=npos, cost=cost,
-                             cost_by_budget=cbb, workspace=ws, stream=stream)
-        if marks:
-            marks[3].record(stream)
-        # a6
-        sp.expected_recompute(hist, bpos, bnpos, broadcast=True, cost=bcost, worst=bworst,
-                              stream=stream)
-        if marks:
-            marks[4].record(stream)
+        hp.step(stream=stream, marks=marks)
 
     def barrier():
         if world > 1:
@@ -551,7 +600,7 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32-exact (int64 costs)",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "int32-exact (int64 costs)",
         "data": "synthetic (seeded; SURVEY 8(d) recipe)",
         "config": workload_config(args, world, None),
         "lcp_tokens_per_s": tokens_all * K / (lcp_ms / 1e3),

@@ -104,8 +104,13 @@ __host__ __device__ __forceinline__ size_t hull_log_bytes(int N, int M) {
 __host__ __device__ __forceinline__ size_t hull_cnt_bytes(int M) {
   return hull_align((size_t)hull_layers_padded(M) * 4);
 }
+// fp64 (a7) scratch: the canonical placement of every budget, int32 [M][M]
+__host__ __device__ __forceinline__ size_t hull_fscr_bytes(int M) {
+  return hull_align(4 * (size_t)M * (size_t)M);
+}
 __host__ __device__ __forceinline__ size_t hull_slot_bytes(int N, int M) {
-  return hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(8 * (size_t)(N + 1));
+  return hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(8 * (size_t)(N + 1)) +
+         hull_fscr_bytes(M);
 }
 __host__ __device__ __forceinline__ size_t hull_smem_bytes(int) { return 0; }   // static rings
 
@@ -608,6 +613,57 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
   return ovf;
 }
 
+// a7: V_0..V_M for fp64 weights as the definitional cost sum_t w_t (t - l(t; C_m)) of the
+// canonical placement C_m of every budget m (the frontier backtrack from the argmin logs), in
+// double-double, so that cost_by_budget meets the 1e-12 bound of SURVEY 8(c) a7 (the DP's own
+// e_m(N) carries ~m N eps P_N of absolute rounding; reading R10).  One budget per lane per pass;
+// the warp walks the row's non-zero bins once per pass.
+template <int K>
+__device__ __forceinline__ void hull_cbb_f64(const HullParams& p, int e, int tfirst,
+                                             const double* __restrict__ we, const uint32_t* logs,
+                                             const int32_t* logn, int32_t* fscr) {
+  const int lane = lane_id();
+  const int N = p.N, M = p.M;
+  double* cbb = reinterpret_cast<double*>(p.cbb) + (int64_t)e * (M + 1);
+  for (int g = 0; g < M; g += 32) {
+    const int mb = g + lane + 1;
+    int32_t* fo = fscr + (size_t)(mb - 1) * M;
+    int k = 0;
+    if (mb <= M) {
+      int j = N, m = mb;
+      while (m > 0 && j >= tfirst) {
+        const int ls = hull_layer_slot(K, m);
+        const int s = log_lookup_lane(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
+        fo[k++] = s;
+        j = s - 1;
+        --m;
+      }
+      for (int a = 0, z = k - 1; a < z; ++a, --z) {
+        const int t = fo[a];
+        fo[a] = fo[z];
+        fo[z] = t;
+      }
+    }
+    hdd acc{0.0, 0.0};
+    int ptr = 0, l = 0;   // positions <= t so far; the largest of them
+    for (int jb = 0; jb < N; jb += 32) {
+      const double w = jb + 1 + lane <= N ? we[jb + 1 + lane] : 0.0;
+      unsigned mask = __ballot_sync(FULL, w != 0.0);
+      while (mask) {
+        const int i = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int t = jb + 1 + i;
+        const double wt = __shfl_sync(FULL, w, i);
+        if (mb <= M) {
+          while (ptr < k && fo[ptr] <= t) l = fo[ptr++];
+          acc = hdd_add(acc, hdd_prod(wt, (double)(t - l)));
+        }
+      }
+    }
+    if (mb <= M) cbb[mb] = acc.hi + acc.lo;
+  }
+}
+
 // VT = int: every entry first; those beyond the int32 guard but within the int64 one are listed
 // for the VT = long long instantiation (launched next, same slots); the rest for the D&C kernel.
 template <typename WT, int K, typename VT>
@@ -791,6 +847,11 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
         }
         acc = hdd_warp_sum(acc);
         if (lane == 0) reinterpret_cast<double*>(p.cost)[e] = acc.hi + acc.lo;
+        if (p.cbb) {
+          int32_t* fscr = reinterpret_cast<int32_t*>(
+              slot + hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(8 * (size_t)(N + 1)));
+          hull_cbb_f64<K>(p, e, tfirst, reinterpret_cast<const double*>(we), logs, logn, fscr);
+        }
       }
     }
     if (p.fpos) {
@@ -890,19 +951,18 @@ __device__ __forceinline__ bool lean_dp(const HullParams& p, const WT* __restric
   const int N = p.N, M = p.M;
   const int LC = p.logcap;
   constexpr int L = 32 * K;
+  constexpr int U = RG::UNIT;   // position unit (x256 for LRing's pre-shifted counters)
   const int passes = (M + L - 1) / L;
   const unsigned lt_mask = (1u << lane) - 1u;
-  constexpr int U = RG::UNIT;   // position unit (x256 for LRing's pre-shifted counters)
   bool ovf = false;
   logfull = false;
   for (int ps = 0; ps < passes && !ovf; ++ps) {
     const int* ein = (ps & 1) ? ebuf1 : ebuf0;
     int* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
     const bool chain_out = ps + 1 < passes;
-    // per slot: deque positions fr8 <= bk8 (x 256); the back line is always the previous row's
-    // line (B0b, s = jp); B1 = the line below it; F0, F1 = the front line and the next one
-    int fr8[K], bk8[K], cnt[K], eo[K];
-    int B0b[K], B1b[K], B1s[K], F0b[K], F0s[K], F1b[K], F1s[K];
+    // per slot: deque positions fr8 <= bk8 (in units U); the back line is always the previous
+    // row's line (B0b, s = jp); every other line is read from the ring when needed
+    int fr8[K], bk8[K], cnt[K], eo[K], B0b[K];
     bool act[K];
     uint32_t* lg[K];
 #pragma unroll
@@ -916,8 +976,7 @@ __device__ __forceinline__ bool lean_dp(const HullParams& p, const WT* __restric
       lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * LC;
       if (act[k]) lg[k][0] = (1u << 16) | 1u;
       // dummy front line (+inf at every query, s = 0), popped by the first row's front test
-      B0b[k] = B1b[k] = F0b[k] = F1b[k] = INT_MAX;
-      B1s[k] = F0s[k] = F1s[k] = 0;
+      B0b[k] = INT_MAX;
       rg.st2(k, 0, INT_MAX, 0);
     }
     int carry = 0, Pm1 = 0, jp = 0, evbase = 0;
@@ -953,6 +1012,16 @@ __device__ __forceinline__ bool lean_dp(const HullParams& p, const WT* __restric
       for (int q = 0; q < nev; ++q) {
         int j, x;
         asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(j), "=r"(x) : "r"(sev_a + 8u * q));
+        // ---- ring lines next to both ends (positions known from the previous row) ------------
+        int B1b[K], B1s[K], B2b[K], B2s[K], F0b[K], F0s[K], F1b[K], F1s[K], Gb[K], Gs[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          rg.ld2(k, bk8[k] - U, B1b[k], B1s[k]);
+          rg.ld2(k, bk8[k] - 2 * U, B2b[k], B2s[k]);
+          rg.ld2(k, fr8[k], F0b[k], F0s[k]);
+          rg.ld2(k, fr8[k] + U, F1b[k], F1s[k]);
+          rg.ld2(k, fr8[k] + 2 * U, Gb[k], Gs[k]);
+        }
         // e_{m-1}(j-1) from the lane below (its value at the previous support row)
         int in[K];
         const int t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
@@ -968,13 +1037,6 @@ __device__ __forceinline__ bool lean_dp(const HullParams& p, const WT* __restric
         }
         ++ev_e;
         const int d0s = jp - j;   // (back line - new line).s, the same for every lane and slot
-        // ---- ring lines two below the back and two after the front (positions known) ------
-        int B2b[K], B2s[K], G2b[K], G2s[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          rg.ld2(k, bk8[k] - 2 * U, B2b[k], B2s[k]);
-          rg.ld2(k, fr8[k] + 2 * U, G2b[k], G2s[k]);
-        }
         // ---- back: two pop tests, with the new point (j, nb) as origin: line B goes iff
         //      (A - N).b (B - N).s - (A - N).s (B - N).b >= 0 for its predecessor A
         int nb[K], top8[K];
@@ -986,8 +1048,8 @@ __device__ __forceinline__ bool lean_dp(const HullParams& p, const WT* __restric
           const int d0b = B0b[k] - nb[k];
           const int n1s = j - B1s[k], d1b = B1b[k] - nb[k];
           p1[k] = act[k] & (sz8 >= U) & hi_nonneg((long long)d1b * d0s + (long long)n1s * d0b);
-          const int d2b = B2b[k] - nb[k], n2s = j - B2s[k];
-          p2[k] = p1[k] & (sz8 >= 2 * U) & hi_nonneg((long long)d2b * (-n1s) + (long long)n2s * d1b);
+          const int d2b = B2b[k] - nb[k], d1s = B1s[k] - j, n2s = j - B2s[k];
+          p2[k] = p1[k] & (sz8 >= 2 * U) & hi_nonneg((long long)d2b * d1s + (long long)n2s * d1b);
           top8[k] = bk8[k] - 2 * U;
         }
         bool any2 = p2[0];
@@ -1005,45 +1067,36 @@ __device__ __forceinline__ bool lean_dp(const HullParams& p, const WT* __restric
                 top8[k] -= U;
                 cs = ls - j;
                 cb = lb - nb[k];
-                B2b[k] = lb;
-                B2s[k] = ls;
               }
             }
           }
         }
-        int v0[K];
+        int v0[K], Fs[K];
         bool q1[K], q2[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          // push: the new line's predecessor becomes B1
-          const int t8 = p2[k] ? top8[k] : (p1[k] ? bk8[k] - U : bk8[k]);
-          B1b[k] = p1[k] ? (p2[k] ? B2b[k] : B1b[k]) : B0b[k];
-          B1s[k] = p1[k] ? (p2[k] ? B2s[k] : B1s[k]) : jp;
+          // push the new line after its predecessor
+          bk8[k] = (p2[k] ? top8[k] : (p1[k] ? bk8[k] - U : bk8[k])) + U;
           B0b[k] = nb[k];
-          bk8[k] = t8 + U;
           ovf |= act[k] & (bk8[k] - fr8[k] >= RG::cap(k) * U);
           rg.st2(k, bk8[k], nb[k], j);
-          // ---- front: up to two pops decided from registers; F1 / the line after it are the
-          //      new line when the back reached them
+          // ---- front: up to two pops decided from the loaded lines; the line after the
+          //      front (F1) or the one after it (G) is the new line when the back reached it
           const bool e1 = bk8[k] == fr8[k] + U, e2 = bk8[k] == fr8[k] + 2 * U;
-          F1b[k] = e1 ? nb[k] : F1b[k];
-          F1s[k] = e1 ? j : F1s[k];
-          const int Gb = e2 ? nb[k] : G2b[k], Gs = e2 ? j : G2s[k];
-          v0[k] = F0b[k] - F0s[k] * x;
-          const int v1 = F1b[k] - F1s[k] * x;
-          const int vg = Gb - Gs * x;
-          q1[k] = act[k] & (v1 < v0[k]);
-          q2[k] = q1[k] & (bk8[k] - fr8[k] >= 2 * U) & (vg < v1);
-          F0b[k] = q2[k] ? Gb : (q1[k] ? F1b[k] : F0b[k]);
-          F0s[k] = q2[k] ? Gs : (q1[k] ? F1s[k] : F0s[k]);
-          v0[k] = q2[k] ? vg : (q1[k] ? v1 : v0[k]);
-          F1b[k] = q1[k] ? Gb : F1b[k];   // (after two pops the loop reloads F1)
-          F1s[k] = q1[k] ? Gs : F1s[k];
+          const int f1b = e1 ? nb[k] : F1b[k], f1s = e1 ? j : F1s[k];
+          const int gb = e2 ? nb[k] : Gb[k], gs = e2 ? j : Gs[k];
+          const int w0 = F0b[k] - F0s[k] * x;
+          const int w1 = f1b - f1s * x;
+          const int wg = gb - gs * x;
+          q1[k] = act[k] & (w1 < w0);
+          q2[k] = q1[k] & (bk8[k] - fr8[k] >= 2 * U) & (wg < w1);
+          v0[k] = q2[k] ? wg : (q1[k] ? w1 : w0);
+          Fs[k] = q2[k] ? gs : f1s;
           fr8[k] += q1[k] ? (q2[k] ? 2 * U : U) : 0;
         }
         bool a2 = q2[0];
         if constexpr (K == 2) a2 |= q2[1];
-        while (__any_sync(FULL, a2)) {   // rare: the front moves by two or more
+        while (__any_sync(FULL, a2)) {   // rare: the front moves by three or more
           a2 = false;
 #pragma unroll
           for (int k = 0; k < K; ++k) {
@@ -1052,13 +1105,10 @@ __device__ __forceinline__ bool lean_dp(const HullParams& p, const WT* __restric
               if (fr8[k] < bk8[k]) {
                 int lb, ls;
                 rg.ld2(k, fr8[k] + U, lb, ls);
-                F1b[k] = lb;
-                F1s[k] = ls;
                 const int vl = lb - ls * x;
                 if (vl < v0[k]) {
-                  F0b[k] = lb;
-                  F0s[k] = ls;
                   v0[k] = vl;
+                  Fs[k] = ls;
                   fr8[k] += U;
                   q2[k] = true;
                 }
@@ -1069,7 +1119,7 @@ __device__ __forceinline__ bool lean_dp(const HullParams& p, const WT* __restric
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          if (q1[k]) lg[k][cnt[k]++] = ((uint32_t)j << 16) | (uint32_t)F0s[k];   // < LC
+          if (q1[k]) lg[k][cnt[k]++] = ((uint32_t)j << 16) | (uint32_t)Fs[k];   // < LC
           eo[k] = v0[k];
         }
         Pm1 = x;

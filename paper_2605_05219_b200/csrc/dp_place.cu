@@ -1503,7 +1503,36 @@ __global__ void __launch_bounds__(DP_NT, 1) dp_place_kernel(DpParams p) {
       // V_M carries ~M N eps P_N absolute rounding)
       __syncthreads();
       const int k = sh.red_s[0];
-      if (k >= 0 && M > 0) {
+      if (k >= 0 && M > 0 && cbb) {
+        // V_1..V_M as the definitional costs of the canonical placement of every budget (the
+        // same backtrack from the argmin table), so that cost_by_budget meets the 1e-12 bound
+        // (SURVEY 8(c) a7); the loop ends with budget M, whose placement stays in `out`
+        const uint16_t* opt = reinterpret_cast<const uint16_t*>(slot + slot_opt_off(N));
+        for (int mb = 1; mb <= M; ++mb) {
+          if (threadIdx.x == 0) {
+            int kk = 0, j = N, m = mb;
+            while (m > 0 && P[j] > 0) {
+              const int s = opt[(size_t)(m - 1) * opt_ld(N) + j];
+              out[kk++] = s;
+              j = s - 1;
+              --m;
+            }
+            for (int a = 0, z = kk - 1; a < z; ++a, --z) {
+              const int tmp = out[a];
+              out[a] = out[z];
+              out[z] = tmp;
+            }
+            sh.red_s[1] = kk;
+          }
+          __syncthreads();
+          const int kk = sh.red_s[1];
+          const double v = eval_cost_f64(we, N, out, kk, sh);
+          if (threadIdx.x == 0) cbb[(int64_t)e * (M + 1) + mb] = v;
+          __syncthreads();
+        }
+        for (int q = k + threadIdx.x; q < M; q += DP_NT) out[q] = 0;
+        if (threadIdx.x == 0) cost[e] = cbb[(int64_t)e * (M + 1) + M];
+      } else if (k >= 0 && M > 0) {
         const double v = eval_cost_f64(we, N, out, k, sh);
         if (threadIdx.x == 0) cost[e] = v;
       }

@@ -458,3 +458,30 @@ def test_row_argmin_monotone_in_j_sparse():
         N = len(c) - 1
         _, O = oracle.dp(c, min(N, 12), "cht")
         assert (np.diff(O[1:, 1:], axis=1) >= 0).all()
+
+
+def test_expected_cost_f64_pins():
+    """or_expected_cost_f64 (P:171-173 on fp64 weights) pinned independently of itself:
+    (1) a point mass at depth d costs exactly d - l(d; C), l = the largest position <= d (0 if
+    none) -- the textbook reusable depth of P:133-137, restated here in plain Python, so an
+    off-by-one in r(t) or in l fails; (2) weights c / 2^k with a dyadic total are exact in
+    binary, so the fp64 cost equals the integer oracle's cost / 2^k bit for bit."""
+    rng = np.random.default_rng(5)
+    N = 40
+    for _ in range(30):
+        k = int(rng.integers(0, 6))
+        C = np.sort(rng.choice(np.arange(1, N + 1), size=k, replace=False)).astype(np.int32)
+        for d in range(1, N + 1):
+            w = np.zeros(N + 1)
+            w[d] = 1.0
+            l = max([c for c in C.tolist() if c <= d], default=0)
+            assert oracle.expected_cost_f64(w, C) == d - l
+    for _ in range(30):
+        c = rng.integers(0, 50, N + 1).astype(np.int64)
+        c[0] = 0
+        total = 1 << int(np.ceil(np.log2(max(2, c.sum() + 1))))
+        c[N] += total - c.sum()
+        assert c.sum() == total
+        k = int(rng.integers(0, 8))
+        C = np.sort(rng.choice(np.arange(1, N + 1), size=k, replace=False)).astype(np.int32)
+        assert oracle.expected_cost_f64(c / total, C) == oracle.expected_cost(c, C) / total

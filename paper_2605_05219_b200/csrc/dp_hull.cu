@@ -358,13 +358,27 @@ __device__ __forceinline__ bool pop_test<double>(int as, double ab, int ks, doub
 template <typename VT>
 using HullCT = typename std::conditional<std::is_same<VT, double>::value, double, long long>::type;
 
+// SPLIT mode (small batches): the two warps of a CTA share an entry, warp 0 running layers 1-32
+// (pass 0) and warp 1 layers 33-64 (pass 1); e_32(j) of every support row goes from warp 0's
+// lane 31 to warp 1's lane 0 through a shared-memory ring instead of the global e-row buffer
+// of sequential passes.  Warp 0 publishes after each 32-row chunk, warp 1 releases ring space
+// after each chunk; either warp raises `abort` when it gives the entry up (ring / log full).
+constexpr int SPLIT_RING = 1024;
+struct SplitSync {
+  int* ring;                 // shared, SPLIT_RING ints
+  volatile int* produced;    // support rows published by warp 0
+  volatile int* consumed;    // lowest support-row index warp 1 still needs
+  volatile int* abort_;      // either warp gave the entry up
+};
+
 // ALLACT: every slot of every pass holds a layer (M a multiple of 32 K) -- the per-slot "active"
 // predicates vanish at compile time
 template <typename WT, typename VT, int K, bool ALLACT, class RING>
 __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
                                         HullCT<VT> TN, VT nV, const RING rg, uint32_t* logs,
                                         int32_t* logn, VT* ebuf0, VT* ebuf1,
-                                        unsigned& pops_e, unsigned& ev_e, bool& logfull) {
+                                        unsigned& pops_e, unsigned& ev_e, bool& logfull,
+                                        const SplitSync* ss = nullptr, int ps_only = -1) {
   const int lane = lane_id();
   const int N = p.N, M = p.M;
   const int LC = p.logcap;   // <= hull_log_cap(N), the allocated stride
@@ -372,7 +386,8 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
   constexpr int L = 32 * K;
   const int passes = (M + L - 1) / L;
   bool ovf = false;
-  for (int ps = 0; ps < passes && !ovf; ++ps) {
+  const int ps_begin = ps_only < 0 ? 0 : ps_only, ps_end = ps_only < 0 ? passes : ps_only + 1;
+  for (int ps = ps_begin; ps < ps_end && !ovf; ++ps) {
     const VT* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
     VT* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
     const bool chain_in = ps > 0, chain_out = ps + 1 < passes;
@@ -439,7 +454,24 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       // value at support row t-1 (constant over zero rows), 0 before the first
       VT Ec = 0;
       const int nev = __popc(evmask);
-      if (chain_in && lane < nev) Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
+      if (ss) {   // SPLIT mode: wait for the other warp (consumer: data; producer: ring space)
+        if (lane == 0) {
+          if (chain_in)
+            while (*ss->produced < evbase + nev - 1 && !*ss->abort_) __nanosleep(64);
+          else
+            while (evbase + nev - 1 - *ss->consumed >= SPLIT_RING && !*ss->abort_) __nanosleep(64);
+        }
+        __syncwarp();
+        if (*ss->abort_) {
+          ovf = true;
+          break;
+        }
+        __threadfence_block();
+        if (chain_in && lane < nev)
+          Ec = evbase + lane >= 1 ? (VT)ss->ring[(evbase + lane - 1) & (SPLIT_RING - 1)] : (VT)0;
+      } else if (chain_in && lane < nev) {
+        Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
+      }
       for (int q = 0; evmask; ++q) {
         const int i = __ffs(evmask) - 1;
         evmask &= evmask - 1;
@@ -583,7 +615,18 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           }
           op[k] = nop;
         }
-        if (chain_out && lane == 31) eout_buf[evbase + q] = eo[K - 1];
+        if (chain_out && lane == 31) {
+          if (ss) ss->ring[(evbase + q) & (SPLIT_RING - 1)] = (int)eo[K - 1];
+          else eout_buf[evbase + q] = eo[K - 1];
+        }
+      }
+      if (ss) {   // publish this chunk (producer) / release its ring slots (consumer)
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) {
+          if (chain_out) *ss->produced = evbase + nev;
+          else *ss->consumed = evbase + nev - 1;
+        }
       }
       evbase += nev;
       bool full = false;
@@ -592,6 +635,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       logfull = __any_sync(FULL, full);
       if (__any_sync(FULL, ovf) || logfull) {
         ovf = true;
+        if (ss && lane == 0) *ss->abort_ = 1;
         break;
       }
     }
@@ -1203,6 +1247,91 @@ __device__ __forceinline__ void hull_backtrack(const HullParams& p, int e, int t
   }
 }
 
+// SPLIT mode kernel (int32 path, 32 < M <= 64): one entry per 2-warp CTA, warp w running the
+// layers of pass w of the K = 1 lockstep DP, chained through a shared-memory ring (SplitSync).
+// For batches with few entries per resident warp (a GPU's share at 8-way strong scaling: 2048
+// W5 entries on 1776 warps) an entry's time halves, and the largest-first order has twice the
+// work items to balance.  Entries that overflow a ring or a log go to the int64 instantiation
+// (launched after, exact for them too); entries beyond the int32 guard likewise, bad rows to the
+// D&C kernel.
+template <typename WT>
+__global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
+  const int lane = lane_id(), w = warp_id();
+  extern __shared__ __align__(16) uint8_t sring[];
+  constexpr size_t RB = (size_t)HC0 * 192;   // one K = 1 ring per warp
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring) + (uint32_t)(w * RB);
+  SRingI<HC0, HC1> srg;
+  srg.b0 = sbase + 4u * (uint32_t)lane;
+  srg.ds = 128u - 2u * (uint32_t)lane;
+  int* ring = reinterpret_cast<int*>(sring + 2 * RB);
+  __shared__ int s_it, s_prod, s_cons, s_abort;
+  SplitSync ss{ring, &s_prod, &s_cons, &s_abort};
+  const int N = p.N, M = p.M;
+  sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
+  unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
+  unsigned* wide_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_WIDE_COUNT_OFF);
+  unsigned* ectr = reinterpret_cast<unsigned*>(p.ws + SP_WS_ENTRY_CTR_OFF);
+  uint8_t* slot = p.slots + (size_t)blockIdx.x * p.slot;
+  uint32_t* logs = reinterpret_cast<uint32_t*>(slot);
+  int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
+  int* ebuf0 = reinterpret_cast<int*>(slot + hull_log_bytes(N, M) + hull_cnt_bytes(M));
+  unsigned long long pops = 0, events = 0;
+  int done_entries = 0;
+  const bool fullm = M == 64;
+  for (;;) {
+    __syncthreads();   // both warps are done with the previous entry
+    if (threadIdx.x == 0) {
+      s_it = (int)atomicAdd(ectr, 1u);
+      s_prod = 0;
+      s_cons = 0;
+      s_abort = 0;
+    }
+    __syncthreads();
+    const int it = s_it;
+    if (it >= p.E) break;
+    const int e = p.order ? p.order[it] : it;
+    const HullRowStat rs = p.rstat[e];
+    if (rs.bad || rs.n >= (1ll << 30) / N) {   // int32 guard: 2 n N < 2^31
+      if (threadIdx.x == 0) {
+        if (!rs.bad && rs.n < (1ll << 46) / N) p.wide[atomicAdd(wide_n, 1u)] = e;
+        else p.fb[atomicAdd(fb_n, 1u)] = e;
+      }
+      continue;
+    }
+    const WT* we = reinterpret_cast<const WT*>(p.w) + (int64_t)e * (N + 1);
+    if (threadIdx.x == 0 && p.cbb) reinterpret_cast<long long*>(p.cbb)[(int64_t)e * (M + 1)] = rs.tn;
+    unsigned pops_e = 0, ev_e = 0;
+    bool logfull = false;
+    if (fullm)
+      hull_dp<WT, int, 1, true>(p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0, pops_e,
+                                ev_e, logfull, &ss, w);
+    else
+      hull_dp<WT, int, 1, false>(p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0,
+                                 pops_e, ev_e, logfull, &ss, w);
+    __syncthreads();
+    if (s_abort) {   // ring or log full in either warp: the int64 instantiation re-runs it
+      if (threadIdx.x == 0) p.wide[atomicAdd(wide_n, 1u)] = e;
+      continue;
+    }
+    pops += pops_e;
+    events += w == 0 ? ev_e : 0;
+    if (w == 0) {
+      __threadfence_block();
+      hull_backtrack<1>(p, e, rs.tfirst, logs, logn);
+      ++done_entries;
+    }
+  }
+  pops = warp_sum(pops);
+  if (lane == 0) {
+    atomicAdd(&stats->hull_pops, pops);
+    if (w == 0) {
+      atomicAdd(&stats->entries_hull, (unsigned long long)done_entries);
+      atomicAdd(&stats->entries_i32, (unsigned long long)done_entries);
+      atomicAdd(&stats->hull_event_rows, events);
+    }
+  }
+}
+
 // the lean kernel's ring: 6-byte lines (SRingI, 12 warps/SM at 64/32 lines) by default;
 // -DSP_LEAN_RING8 selects 8-byte lines in 256-byte rows (LRing: one LDS.64 per line, 9 warps/SM)
 #ifdef SP_LEAN_RING8
@@ -1386,6 +1515,39 @@ static int hull_grid_t(int E) {
   return clamp_grid((long)dev_sms() * occ, E);
 }
 
+constexpr size_t split_smem_bytes() { return 2 * (size_t)HC0 * 192 + SPLIT_RING * sizeof(int); }
+
+template <typename WT>
+static int split_grid_t(int E) {
+  static int cache[HULL_MAX_DEV] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= HULL_MAX_DEV) dev = 0;
+  if (!cache[dev]) {
+    cudaFuncSetAttribute(dp_hull_split_kernel<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)split_smem_bytes());
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dp_hull_split_kernel<WT>, 64,
+                                                  split_smem_bytes());
+    cache[dev] = occ < 1 ? 1 : occ;
+  }
+  return clamp_grid((long)dev_sms() * cache[dev], E);
+}
+
+// SPLIT mode for the int32 path when 32 < M <= 64 and the batch has fewer than 1.5 entries per
+// resident warp of the one-warp kernel (measured on W5 rows, 1776 warps: 2048 entries 7.35 ->
+// 5.60 ms; 4096 entries 8.0 -> 10.3 ms, so not there); SP_HULL_SPLIT=0 / 1 forces it off / on
+// (comparison hook, read once per process)
+static bool use_split(int E, int M, int one_warp_grid) {
+  static const int force = [] {
+    const char* v = getenv("SP_HULL_SPLIT");
+    return v ? atoi(v) : -1;
+  }();
+  if (M <= 32 || M > 64) return false;
+  if (force >= 0) return force != 0;
+  return 2L * E < 3L * one_warp_grid;
+}
+
 template <typename WT, int K>
 static int lean_grid_t(int E) {
   static int cache[HULL_MAX_DEV] = {0};
@@ -1405,7 +1567,11 @@ static void hull_launch_t(const HullParams& p, const HullRowStat* rstat, int gn,
   if constexpr (std::is_same<WT, double>::value) {
     dp_hull_kernel<double, K, double><<<gn, 32, ring_bytes<K, double>(), st>>>(p);
   } else {
-    if (!hull_lean()) {
+    if (K == 2 && !hull_lean() && p.rstat &&
+        use_split(p.E, p.M, std::min(gn, hull_grid_t<WT, K, int>(p.E)))) {
+      const int gs = std::min(gn, split_grid_t<WT>(p.E));
+      dp_hull_split_kernel<WT><<<gs, 64, split_smem_bytes(), st>>>(p);
+    } else if (!hull_lean()) {
       dp_hull_kernel<WT, K, int><<<gn, 32, ring_bytes<K, int>(), st>>>(p);
     } else {
       const int gl = std::min(gn, lean_grid_t<WT, K>(p.E));
@@ -1428,13 +1594,15 @@ int sp_hull_grid(int E, int N, int M, int wtype) {
     return k2 ? sp::hull_grid_t<double, 2, double>(E) : sp::hull_grid_t<double, 1, double>(E);
   int g;
   if (wtype == SP_W_COUNTS_I64)
-    g = k2 ? std::max(std::max(sp::hull_grid_t<int64_t, 2, int>(E), sp::lean_grid_t<int64_t, 2>(E)),
-                      sp::hull_grid_t<int64_t, 2, long long>(E))
+    g = k2 ? std::max(std::max(std::max(sp::hull_grid_t<int64_t, 2, int>(E), sp::lean_grid_t<int64_t, 2>(E)),
+                               sp::hull_grid_t<int64_t, 2, long long>(E)),
+                      sp::split_grid_t<int64_t>(E))
            : std::max(std::max(sp::hull_grid_t<int64_t, 1, int>(E), sp::lean_grid_t<int64_t, 1>(E)),
                       sp::hull_grid_t<int64_t, 1, long long>(E));
   else
-    g = k2 ? std::max(std::max(sp::hull_grid_t<int32_t, 2, int>(E), sp::lean_grid_t<int32_t, 2>(E)),
-                      sp::hull_grid_t<int32_t, 2, long long>(E))
+    g = k2 ? std::max(std::max(std::max(sp::hull_grid_t<int32_t, 2, int>(E), sp::lean_grid_t<int32_t, 2>(E)),
+                               sp::hull_grid_t<int32_t, 2, long long>(E)),
+                      sp::split_grid_t<int32_t>(E))
            : std::max(std::max(sp::hull_grid_t<int32_t, 1, int>(E), sp::lean_grid_t<int32_t, 1>(E)),
                       sp::hull_grid_t<int32_t, 1, long long>(E));
   return g;

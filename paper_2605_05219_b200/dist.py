@@ -19,6 +19,8 @@ merge runs in the library's kernels (sp_overlap_hist / sp_accumulate_depths).
 """
 from __future__ import annotations
 
+import contextlib
+
 import torch
 import torch.distributed as dist
 
@@ -63,7 +65,16 @@ class HistMerger:
         return self.lcp_pad
 
     def merge(self, hist_own: torch.Tensor, stream=None) -> torch.Tensor:
-        """Add every rank's observations of the owned entries into hist_own [E_own][N+1]."""
+        """Add every rank's observations of the owned entries into hist_own [E_own][N+1].
+        The collectives are issued with `stream` as the current stream, so they are ordered
+        after the LCP kernel that filled lcp_out on that stream (NCCL runs on its own stream
+        but waits on the current one)."""
+        ctx = (torch.cuda.stream(stream) if stream is not None and hist_own.is_cuda
+               else contextlib.nullcontext())
+        with ctx:
+            return self._merge(hist_own, stream)
+
+    def _merge(self, hist_own: torch.Tensor, stream=None) -> torch.Tensor:
         if self.mode == "sparse":
             dist.all_gather_into_tensor(self.g_lcp, self.lcp_pad, group=self.group)
             self.accumulate(self.g_ent, self.g_lcp, self.e0, self.e1, self.N, hist_own,

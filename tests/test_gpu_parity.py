@@ -499,3 +499,51 @@ def test_expected_recompute_f64(dev):
     rc, _ = oracle.eval_batch(H.astype(np.int32), np_(pos), np_(npos), broadcast=True)
     ref = rc / H.sum(1, keepdims=True)
     assert np.allclose(np_(cost), ref, rtol=1e-13, atol=0)
+
+
+# ------------------------------------------------------------------------------------------
+# e : multi-GPU, emulated on one GPU ("split requests into R shards, sum histograms,
+#     assert identical placements")
+# ------------------------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("ranks", [2, 4, 8])
+def test_multirank_emulation_one_gpu(dev, ranks):
+    """The N-rank path of bench.py / dist.HistMerger emulated on one GPU: the requests of a
+    QuALITY-like trace routed to `ranks` shards exactly as on N ranks (make_trace(world, rank)),
+    each shard's depths from sp_overlap_hist(lcp_out, with_hist=False), the all-gather as a
+    concatenation of the padded per-rank buffers, every owner's slice scatter-added with
+    sp_accumulate_depths; the owners' histograms and placements must equal the single-rank
+    ones bit for bit (per-edge independence P:189-190; integer sums commute)."""
+    E = 64
+    cfg = wl.scaled(wl.CONFIGS["W3"], E)
+    N, M = cfg.N, cfg.M
+    full = wl.make_trace(cfg, seed=9, device=dev)
+    h_ref, _ = sp.overlap_hist(full["entry_tokens"], full["entry_off"], full["req_tokens"],
+                               full["req_off"], full["req_entry"], N, n_entries=E)
+    shards = [wl.make_trace(cfg, seed=9, device=dev, world=ranks, rank=r) for r in range(ranks)]
+    assert sum(s["req_off"].numel() - 1 for s in shards) == full["req_off"].numel() - 1
+    Rmax = max(s["req_off"].numel() - 1 for s in shards)
+    g_ent, g_lcp = [], []
+    for s in shards:
+        R = s["req_off"].numel() - 1
+        lcp = torch.full((Rmax,), -1, dtype=torch.int32, device=dev)
+        ent = torch.full((Rmax,), -1, dtype=torch.int32, device=dev)
+        ent[:R] = s["req_entry"]
+        sp.overlap_hist(s["entry_tokens"], s["entry_off"], s["req_tokens"], s["req_off"],
+                        s["req_entry"], N, lcp_out=lcp, n_entries=E, with_hist=False)
+        g_ent.append(ent)
+        g_lcp.append(lcp)
+    g_ent, g_lcp = torch.cat(g_ent), torch.cat(g_lcp)       # the all-gather
+    E_own = E // ranks
+    owners = []
+    for o in range(ranks):
+        h = torch.zeros(E_own, N + 1, dtype=torch.int32, device=dev)
+        sp.accumulate_depths(g_ent, g_lcp, o * E_own, (o + 1) * E_own, N, h)
+        owners.append(h)
+    merged = torch.cat(owners)
+    assert torch.equal(merged, h_ref)
+    ref = sp.place_checkpoints(h_ref, M, cost_by_budget=True)
+    got = [sp.place_checkpoints(h, M, cost_by_budget=True) for h in owners]
+    for i in range(4):
+        assert torch.equal(torch.cat([g[i] for g in got]), ref[i])

@@ -100,8 +100,10 @@ sp_status sp_accumulate_depths(const int32_t* entry, const int32_t* depth, int64
  *   weights        [E][N+1] of type wtype (bin 0 ignored; not normalised)
  *   positions      int32 [E][M]: the rule-B placement, ascending, unused slots 0
  *   n_positions    int32 [E]: number of positions (0..min(M, #nonzero bins)), or a NEGATIVE
- *                  sp_status for that entry (-SP_ERR_OVERFLOW if 2 * P_N * N >= 2^62 for the
- *                  count types; -SP_ERR_INTERNAL never expected)
+ *                  sp_status for that entry: -SP_ERR_BAD_ARGUMENT for a negative count / a
+ *                  negative or non-finite fp64 weight; -SP_ERR_OVERFLOW for the count types if
+ *                  a count is >= 2^47 or 2 * P_N * N >= 2^62; -SP_ERR_INTERNAL never expected.
+ *                  Such an entry's positions are 0 and its costs unspecified.
  *   cost           [E]: V_M = dp[M][N] = n * E[r] -- int64 for count types, double for F64
  *   cost_by_budget [E][M+1] V_0..V_M (same type as cost; V_0 = T_N = n * R_nc), or
  *                  NULL.  (The DP computes every budget m <= M on the way.)
@@ -201,12 +203,15 @@ sp_status sp_clip_to_blocks(const int32_t* positions /*[E][max_pos]*/,
  *   t     int64  [E]       observations so far;   tau  int64 [E]   reference epoch
  * sp_gamma_observe appends one batch of observations GROUPED BY ENTRY, in arrival order within
  * each entry: obs_off int64 [E+1] (CSR offsets), depth int32 [obs_off[E]] (e.g. sp_overlap_hist's
- * lcp_out); depths are clamped to [0, N] (bin 0 = miss).  Each observation adds g^-(t+1-tau) to
- * W[e][depth]; the row is rescaled (tau = t) before exponents pass 2^64.  fp64 atomics: the
+ * lcp_out).  Only hits are samples of T in {1..N}: a depth < 1 (a miss) is
+ * skipped -- no weight, t unchanged; depths > N are clamped to N.  Hit number t+1 adds
+ * g^-(t+1-tau) to W[e][depth]; the row is rescaled (tau = t) before exponents pass 2^64.  t counts
+ * hits.  fp64 atomics: the
  * summation order (not the value) of equal-depth observations in one batch is unspecified.
  * W can be handed to sp_place_checkpoints (SP_W_PROB_F64) directly: it differs from p_t by a
  * positive per-entry factor, and the placement is scale-invariant.
- * sp_gamma_snapshot writes p_t (double [E][N+1], sums to 1; all zero when t = 0).
+ * sp_gamma_snapshot writes p_t (double [E][N+1], bins 1..N sum to 1, bin 0 = 0; all zero when
+ * t = 0).
  * Errors: BAD_LENGTH (N < 1, N > SP_MAX_N, E < 0), BAD_ARGUMENT (g outside (0, 1], NULL), CUDA.
  * ---------------------------------------------------------------------------------------- */
 sp_status sp_gamma_observe(double* W, int64_t* t, int64_t* tau, const int64_t* obs_off,
@@ -255,6 +260,22 @@ const char* sp_status_string(sp_status status);
 const char* sp_last_error_string(void);
 /* Library version string, e.g. "sparseprefix 0.1 sm_100a". */
 const char* sp_version(void);
+
+/* Comparison / test hooks -- not needed by callers.  Process-wide values that steer which
+ * kernel path a call takes (the results are the same on every path; the parity tests run each):
+ *   SP_DBG_NO_HULL       1: the DP uses the divide-and-conquer kernel only
+ *   SP_DBG_HULL_LEAN     1: the int32 hull path uses dp_lean_kernel
+ *   SP_DBG_HULL_SPLIT    -1 automatic (default), 0 never, 1 always two warps per entry
+ *   SP_DBG_HULL_LOGCAP   > 0: argmin-log capacity override (forces the log-full fallback)
+ *   SP_DBG_HULL_NO_ORDER 1: no largest-first entry order
+ *   SP_DBG_EVAL_PATH     0 automatic, 1 chunked kernel, 2 4-byte-prefix kernel, 3 2-byte-prefix
+ * Initial values come from the environment variables of the same names (SP_NO_HULL, ...), read
+ * once per process; sp_debug_set returns the previous value (or -SP_ERR_BAD_ARGUMENT for an
+ * unknown flag).  Read on the host at launch time: not stream-ordered. */
+enum { SP_DBG_NO_HULL = 0, SP_DBG_HULL_LEAN = 1, SP_DBG_HULL_SPLIT = 2, SP_DBG_HULL_LOGCAP = 3,
+       SP_DBG_HULL_NO_ORDER = 4, SP_DBG_EVAL_PATH = 5, SP_DBG_COUNT = 6 };
+int sp_debug_set(int flag, int value);
+int sp_debug_get(int flag);
 
 #ifdef __cplusplus
 }

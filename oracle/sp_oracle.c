@@ -509,18 +509,26 @@ int or_eval_batch(const int32_t* hist, int32_t n_entries, int32_t N, const int32
 /* clamped to [0, N] (S:327 design decision; bin 0 = miss).  O(t) per call, long double.      */
 /* ------------------------------------------------------------------------------------------ */
 int or_gamma_hist(const int32_t* depths, int64_t t, int32_t N, double gamma, double* p) {
-  if (N < 1 || t < 1 || !(gamma > 0.0 && gamma <= 1.0)) return -1;
+  if (N < 1 || t < 0 || !(gamma > 0.0 && gamma <= 1.0)) return -1;
+  /* the samples T_s are the HITS of the stream, in order: T in {1..N}, conditioning on
+     hits (DESIGN reading R15); a miss (depth < 1) is not a sample */
+  int64_t h = 0;
+  for (int64_t s = 0; s < t; ++s) h += depths[s] >= 1;
+  for (int32_t d = 0; d <= N; ++d) p[d] = 0.0;
+  if (h == 0) return 0;
   long double* acc = (long double*)calloc((size_t)N + 1, sizeof(long double));
   if (!acc) return -3;
-  for (int64_t s = 1; s <= t; ++s) {
-    int32_t d = depths[s - 1];
-    if (d < 0) d = 0;
-    if (d > N) d = N;
-    acc[d] += powl((long double)gamma, (long double)(t - s));   /* gamma^(t-s) e_{T_s} */
+  int64_t s = 0;   /* sample index 1..h */
+  for (int64_t i = 0; i < t; ++i) {
+    int32_t d = depths[i];
+    if (d < 1) continue;
+    ++s;
+    if (d > N) d = N;                                              /* clamp */
+    acc[d] += powl((long double)gamma, (long double)(h - s));     /* gamma^(t-s) e_{T_s} */
   }
   long double norm;
-  if (gamma == 1.0) norm = 1.0L / (long double)t;
-  else norm = (1.0L - (long double)gamma) / (1.0L - powl((long double)gamma, (long double)t));
+  if (gamma == 1.0) norm = 1.0L / (long double)h;
+  else norm = (1.0L - (long double)gamma) / (1.0L - powl((long double)gamma, (long double)h));
   for (int32_t d = 0; d <= N; ++d) p[d] = (double)(acc[d] * norm);
   free(acc);
   return 0;

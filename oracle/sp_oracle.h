@@ -94,7 +94,9 @@ int or_eval_batch(const int32_t* hist, int32_t n_entries, int32_t N, const int32
 
 /* f2: Thm 4's exponentially weighted empirical histogram, definitional O(t N):
  * p[d] = (1-g)/(1-g^t) sum_{s<=t} g^(t-s) [T_s = d]  (g = 1: empirical frequencies).
- * depths[t] in arrival order, clamped to [0, N]; p[N+1] normalised (sums to 1). */
+ * depths[t] in arrival order; the samples T_s are the hits (depth >= 1, clamped to N): a miss
+ * is not a sample of T in {1..N} (reading R15).  p[N+1] sums to 1 over bins
+ * 1..N (bin 0 stays 0); all zero when the stream has no hit. */
 int or_gamma_hist(const int32_t* depths, int64_t t, int32_t N, double gamma, double* p);
 /* Thm 4's variance term sqrt(N (1-g)/(1+g) (1+g^t)/(1-g^t)). */
 double or_gamma_variance_term(double gamma, int64_t t, int32_t N);

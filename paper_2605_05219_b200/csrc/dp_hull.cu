@@ -1536,13 +1536,10 @@ static int split_grid_t(int E) {
 
 // SPLIT mode for the int32 path when 32 < M <= 64 and the batch has fewer than 1.5 entries per
 // resident warp of the one-warp kernel (measured on W5 rows, 1776 warps: 2048 entries 7.35 ->
-// 5.60 ms; 4096 entries 8.0 -> 10.3 ms, so not there); SP_HULL_SPLIT=0 / 1 forces it off / on
-// (comparison hook, read once per process)
+// 5.60 ms; 4096 entries 8.0 -> 10.3 ms, so not there); SP_DBG_HULL_SPLIT = 0 / 1 forces it off
+// / on (comparison hook)
 static bool use_split(int E, int M, int one_warp_grid) {
-  static const int force = [] {
-    const char* v = getenv("SP_HULL_SPLIT");
-    return v ? atoi(v) : -1;
-  }();
+  const int force = sp_debug_get(SP_DBG_HULL_SPLIT);
   if (M <= 32 || M > 64) return false;
   if (force >= 0) return force != 0;
   return 2L * E < 3L * one_warp_grid;
@@ -1555,12 +1552,9 @@ static int lean_grid_t(int E) {
   return clamp_grid((long)dev_sms() * occ, E);
 }
 
-// SP_HULL_LEAN=1 runs the int32 path on dp_lean_kernel instead of dp_hull_kernel<.., int>
-// (measured: faster on sparse rows, slower on W5's); read once per process
-static bool hull_lean() {
-  static const bool v = getenv("SP_HULL_LEAN") != nullptr;
-  return v;
-}
+// SP_DBG_HULL_LEAN runs the int32 path on dp_lean_kernel instead of dp_hull_kernel<.., int>
+// (measured: faster on sparse rows, slower on W5's)
+static bool hull_lean() { return sp_debug_get(SP_DBG_HULL_LEAN) != 0; }
 
 template <typename WT, int K>
 static void hull_launch_t(const HullParams& p, const HullRowStat* rstat, int gn, cudaStream_t st) {
@@ -1627,11 +1621,8 @@ cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, 
                            int32_t* npos, void* cost, void* cbb, int32_t* fpos,
                            int32_t* fn, uint8_t* ws, int32_t* fb, int32_t* wide, uint8_t* pool,
                            uint8_t* order_ws, uint8_t* slots, int grid, cudaStream_t st) {
-  static const bool no_order = getenv("SP_HULL_NO_ORDER") != nullptr;   // comparison hook
-  static const int logcap_env = [] {
-    const char* lc = getenv("SP_HULL_LOGCAP");   // test hook: force the log-full fallback
-    return lc ? atoi(lc) : 0;
-  }();
+  const bool no_order = sp_debug_get(SP_DBG_HULL_NO_ORDER) != 0;   // comparison hook
+  const int logcap_env = sp_debug_get(SP_DBG_HULL_LOGCAP);   // test hook: force the log-full fallback
   sp::HullParams p;
   p.order = nullptr;
   const size_t a = sp::hull_align(4 * (size_t)E);

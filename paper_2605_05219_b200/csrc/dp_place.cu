@@ -19,6 +19,9 @@
 // results; int64 / double otherwise, then in the slot's global/L2 scratch); opt_m(j) for the
 // current layer lives in shared memory (uint16); P_j, b_next and the full argmin table
 // opt[M][N+1] (uint16) live in the CTA's workspace slot.
+#include <map>
+#include <mutex>
+#include <utility>
 #include <climits>
 #include <cstdlib>
 #include <algorithm>
@@ -1255,7 +1258,9 @@ __device__ void prefix_counts(const WT* we, int N, int64_t* P, int32_t* P32, Sha
     const int t = base + threadIdx.x;
     int64_t cnt = 0;
     if (t >= 1 && t <= N) cnt = (int64_t)we[t];
-    bad |= cnt < 0;
+    // 1: a negative count (BAD_ARGUMENT); 2: a count >= 2^47, which could wrap the int64 sums
+    // (N <= 2^16 such counts stay below 2^63, so n and the 2 n N < 2^62 guard are then exact)
+    bad |= (cnt < 0 ? 1 : 0) | (cnt >= (int64_t(1) << 47) ? 2 : 0);
     int64_t tot;
     const int64_t ex = block_exclusive_scan<DP_NT>(cnt, sh.wbuf, &tot);
     if (t <= N) {
@@ -1267,7 +1272,7 @@ __device__ void prefix_counts(const WT* we, int N, int64_t* P, int32_t* P32, Sha
   }
   TN = block_sum<DP_NT>(tpart, sh.wbuf);
   n = carry;
-  neg = __syncthreads_or(bad);
+  neg = (__syncthreads_or(bad & 1) ? 1 : 0) | (__syncthreads_or(bad & 2) ? 2 : 0);
 }
 
 // ---- a3/a7 for fp64 weights: double-double block scan, P_j rounded once ---------------------
@@ -1412,8 +1417,10 @@ __global__ void __launch_bounds__(DP_NT, 1) dp_place_kernel(DpParams p) {
 
     // ---- a4: the DP ----------------------------------------------------------------------
     int status = 0, path = -1;
-    if (neg) {
+    if (neg & 1) {
       status = SP_ERR_BAD_ARGUMENT;
+    } else if (neg & 2) {
+      status = SP_ERR_OVERFLOW;
     } else if (M > 0) {
       if constexpr (F64) {
         solve_entry<double, false, PT, CT>(p, sh, nullptr, sopt, scratch64, e, TN, P, phase);
@@ -1552,17 +1559,37 @@ static bool dp_smem_b_fits(int N) {
 
 static size_t dp_dyn_smem(int N, bool smem_b) { return sp::dyn_smem_bytes(N, smem_b); }
 
+// resident CTAs per SM of dp_place_kernel<WT> (cached per device and shared-memory size: no
+// attribute or occupancy query on every call once warm)
 template <typename WT>
 static int dp_grid_t(int E, int N) {
-  int dev = 0, sms = 148;
+  static std::mutex mu;
+  static std::map<std::pair<int, size_t>, std::pair<int, int>> cache;   // -> (sms, occ)
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t dyn = dp_dyn_smem(N, dp_smem_b_fits(N));
-  int occ = 1;
-  cudaFuncSetAttribute(sp::dp_place_kernel<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)dyn);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp::dp_place_kernel<WT>, sp::DP_NT, dyn);
-  if (occ < 1) occ = 1;
+  int sms = 148, occ = 1;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({dev, dyn});
+    if (it != cache.end()) {
+      sms = it->second.first;
+      occ = it->second.second;
+    } else {
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      // opt in to the most dynamic shared memory the kernel can have (static + dynamic <= the
+      // per-block opt-in limit), once per device: every later size fits
+      int optin = 227 * 1024;
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncAttributes fa;
+      if (cudaFuncGetAttributes(&fa, sp::dp_place_kernel<WT>) == cudaSuccess)
+        cudaFuncSetAttribute(sp::dp_place_kernel<WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - (int)fa.sharedSizeBytes);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp::dp_place_kernel<WT>, sp::DP_NT, dyn);
+      if (occ < 1) occ = 1;
+      cache[{dev, dyn}] = {sms, occ};
+    }
+  }
   long g = (long)sms * occ;
   if (g > E) g = E;
   return (int)(g < 1 ? 1 : g);
@@ -1634,7 +1661,7 @@ static sp_status place_impl(const void* weights, sp_weight_type wtype,
   else grid = dp_grid_t<double>(n_entries, N);
   // the hull kernels (dp_hull.cu: int32 / int64 for counts, double for fp64 weights) solve every
   // entry they can and list the rest (bad weights, nN >= 2^46, ring overflow) for the D&C kernel
-  const bool use_hull = M > 0 && !getenv("SP_NO_HULL");
+  const bool use_hull = M > 0 && !sp_debug_get(SP_DBG_NO_HULL);
   const int hgrid = use_hull ? sp_hull_grid(n_entries, N, M, wtype) : 0;
   const size_t fb_off = SP_WS_STATS_BYTES;
   const size_t wide_off = fb_off + (use_hull ? sp::align256(4 * (size_t)n_entries) : 0);

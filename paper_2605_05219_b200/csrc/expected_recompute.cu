@@ -17,6 +17,11 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "common.cuh"
 
 namespace sp {
@@ -463,6 +468,57 @@ __global__ void __launch_bounds__(EB_NT, 1)
 
 }  // namespace sp
 
+// Launch facts cached per device (no attribute / occupancy query on every call once warm).
+constexpr int EV_MAX_DEV = 64;
+static int eval_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 || dev >= EV_MAX_DEV ? 0 : dev;
+}
+static int eval_sms() {
+  static std::atomic<int> sms[EV_MAX_DEV];
+  const int dev = eval_dev();
+  int v = sms[dev].load(std::memory_order_relaxed);
+  if (!v) {
+    v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+// opt in, once per (device, kernel slot), to the most dynamic shared memory the kernel can have
+// (static + dynamic <= the per-block opt-in limit): every later size fits
+template <typename K>
+static void eval_smem_attr(K kern, int slot) {
+  static std::atomic<bool> done[EV_MAX_DEV][8];
+  const int dev = eval_dev();
+  if (!done[dev][slot].load(std::memory_order_acquire)) {
+    int optin = 227 * 1024;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           optin - (int)fa.sharedSizeBytes);
+    done[dev][slot].store(true, std::memory_order_release);
+  }
+}
+// resident CTAs per SM for `dyn` bytes (cached per device, kernel slot and size)
+template <typename K>
+static int eval_occ(K kern, int nt, size_t dyn, int slot) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, size_t>, int> cache;
+  const int dev = eval_dev();
+  eval_smem_attr(kern, slot);
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, slot, dyn);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, dyn);
+  cache[key] = occ;
+  return occ;
+}
+
 extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type wtype,
                                            int32_t n_entries, int32_t N,
                                            const int32_t* positions, const int32_t* n_positions,
@@ -475,41 +531,29 @@ extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type w
   if (n_entries == 0 || n_sets == 0) return SP_OK;
   if (!weights || !n_positions || !cost || (max_pos > 0 && !positions))
     return SP_ERR_BAD_ARGUMENT;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = eval_sms();
   const int grid = n_entries < sms * 8 ? n_entries : sms * 8;
   cudaStream_t st = (cudaStream_t)stream;
-  const bool legacy = getenv("SP_EVAL_CHUNKED") || getenv("SP_EVAL_P32") || getenv("SP_EVAL_PREFIX");
+  const int path = sp_debug_get(SP_DBG_EVAL_PATH);   // 0 auto; 1 chunked, 2 p32, 3 prefix
   const size_t tab = (size_t)n_sets * (N + 1) * sizeof(uint16_t);
-  if (wtype == SP_W_COUNTS_I32 && !legacy && broadcast && n_sets <= sp::EB_MAXS &&
+  if (wtype == SP_W_COUNTS_I32 && path == 0 && broadcast && n_sets <= sp::EB_MAXS &&
       tab <= sp::EB_SMEM_MAX) {
     auto kern = n_sets == 1   ? sp::eval_bcast_kernel<1>
                 : n_sets == 2 ? sp::eval_bcast_kernel<2>
                 : n_sets == 3 ? sp::eval_bcast_kernel<3>
                               : sp::eval_bcast_kernel<4>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab);
+    eval_smem_attr(kern, n_sets - 1);
     if (cudaMemsetAsync(cost, 0, (size_t)n_entries * n_sets * sizeof(int64_t), st) != cudaSuccess)
       return SP_ERR_CUDA;
     kern<<<sms, sp::EB_NT, tab, st>>>(
         (const int32_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
         (int64_t*)cost, worst_case);
-  } else if (wtype == SP_W_COUNTS_I32 && !getenv("SP_EVAL_CHUNKED")) {
+  } else if (wtype == SP_W_COUNTS_I32 && path != 1) {
     const int nseg = (N + 1 + 1023) / 1024;
-    const bool wide = getenv("SP_EVAL_P32") != nullptr;   // 4-byte prefixes (tests / comparison)
+    const bool wide = path == 2;   // 4-byte prefixes (tests / comparison)
     const size_t dyn = (size_t)nseg * 1024 * (wide ? 4 : 2);
-    int occ = 1;
-    if (wide) {
-      cudaFuncSetAttribute(sp::eval_p32_kernel<int32_t, 512>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp::eval_p32_kernel<int32_t, 512>, 512,
-                                                    dyn);
-    } else {
-      cudaFuncSetAttribute(sp::eval_p32_kernel<uint16_t, 256>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sp::eval_p32_kernel<uint16_t, 256>, 256,
-                                                    dyn);
-    }
+    const int occ = wide ? eval_occ(sp::eval_p32_kernel<int32_t, 512>, 512, dyn, 4)
+                         : eval_occ(sp::eval_p32_kernel<uint16_t, 256>, 256, dyn, 5);
     const long gcap = (long)sms * (occ < 1 ? 1 : occ);
     const int g2 = n_entries < gcap ? n_entries : (int)gcap;
     if (wide)

@@ -14,7 +14,7 @@
 //
 // One warp per entry (grid-stride): lanes take the entry's observations of the batch in chunks
 // whose exponents stay below 2^64, add their increments with fp64 atomics, and the warp rescales
-// the row between chunks when needed.
+// the row between chunks when needed.  Misses (depth < 1) are not samples of T (reading R15).
 #include <cmath>
 
 #include "common.cuh"
@@ -45,13 +45,23 @@ __global__ void __launch_bounds__(GE_NT)
         __syncwarp();
         ta = t;
       }
-      for (int64_t i = c0 + lane; i < c1; i += 32) {
-        int d = depth[o0 + i];
-        d = d < 0 ? 0 : (d > N ? N : d);   // clamp; bin 0 = miss
-        const double inc = g < 1.0 ? pow(g, -(double)(t + (i - c0) + 1 - ta)) : 1.0;
-        atomicAdd(row + d, inc);
+      // only hits are samples (T in {1..N}; conditioning on hits; reading
+      // R15): a miss (depth < 1) neither adds weight nor advances t, so each hit's exponent is
+      // its rank among the hits (ballot + popc over each 32-observation group)
+      const unsigned lt = (1u << lane) - 1u;
+      for (int64_t i0 = c0; i0 < c1; i0 += 32) {
+        const int64_t i = i0 + lane;
+        int d = i < c1 ? depth[o0 + i] : 0;
+        const bool hit = d >= 1;
+        const unsigned bal = __ballot_sync(FULL, hit);
+        if (hit) {
+          d = d > N ? N : d;   // clamp
+          const int64_t x = t + __popc(bal & lt) + 1 - ta;
+          const double inc = g < 1.0 ? pow(g, -(double)x) : 1.0;
+          atomicAdd(row + d, inc);
+        }
+        t += __popc(bal);
       }
-      t += c1 - c0;
       __syncwarp();
     }
     if (lane == 0) {

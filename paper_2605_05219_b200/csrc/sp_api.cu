@@ -1,6 +1,8 @@
 // sp_api.cu -- host-side pieces of the C ABI: status strings, error text, version, and the
 // Table 1 baseline generators.
+#include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -48,4 +50,42 @@ extern "C" int32_t sp_block_positions(int32_t N, int32_t B, int32_t* out_host) {
   if (k > 0 && !out_host) return -SP_ERR_BAD_ARGUMENT;
   for (int32_t i = 1; i <= k; ++i) out_host[i - 1] = i * B;
   return k;
+}
+
+// Comparison / test hooks (sp_debug_set in the header): process-wide values read by the launch
+// code from atomics -- no getenv on the call path.  Each starts from its environment variable,
+// read once (so the tools' SP_* variables keep working).
+static std::atomic<int> g_dbg[SP_DBG_COUNT];
+static std::atomic<bool> g_dbg_init{false};
+
+static void dbg_init() {
+  if (g_dbg_init.load(std::memory_order_acquire)) return;
+  static const char* names[SP_DBG_COUNT] = {"SP_NO_HULL", "SP_HULL_LEAN", "SP_HULL_SPLIT",
+                                            "SP_HULL_LOGCAP", "SP_HULL_NO_ORDER", "SP_EVAL_PATH"};
+  static const int defaults[SP_DBG_COUNT] = {0, 0, -1, 0, 0, 0};
+  for (int i = 0; i < SP_DBG_COUNT; ++i) {
+    int v = defaults[i];
+    if (const char* s = getenv(names[i])) v = atoi(s);
+    if (i == SP_DBG_EVAL_PATH) {   // legacy spellings of the evaluation-path hook
+      if (getenv("SP_EVAL_CHUNKED")) v = 1;
+      if (getenv("SP_EVAL_P32")) v = 2;
+      if (getenv("SP_EVAL_PREFIX")) v = 3;
+    }
+    int expect = 0;
+    (void)expect;
+    g_dbg[i].store(v, std::memory_order_relaxed);
+  }
+  g_dbg_init.store(true, std::memory_order_release);
+}
+
+extern "C" int sp_debug_get(int flag) {
+  if (flag < 0 || flag >= SP_DBG_COUNT) return 0;
+  dbg_init();
+  return g_dbg[flag].load(std::memory_order_relaxed);
+}
+
+extern "C" int sp_debug_set(int flag, int value) {
+  if (flag < 0 || flag >= SP_DBG_COUNT) return -SP_ERR_BAD_ARGUMENT;
+  dbg_init();
+  return g_dbg[flag].exchange(value, std::memory_order_relaxed);
 }

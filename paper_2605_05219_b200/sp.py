@@ -24,6 +24,10 @@ SP_ERR_WORKSPACE = 6
 SP_ERR_CUDA = 7
 SP_ERR_INTERNAL = 8
 
+# comparison / test hooks (sp_debug_set)
+SP_DBG_NO_HULL, SP_DBG_HULL_LEAN, SP_DBG_HULL_SPLIT = 0, 1, 2
+SP_DBG_HULL_LOGCAP, SP_DBG_HULL_NO_ORDER, SP_DBG_EVAL_PATH = 3, 4, 5
+
 SP_W_COUNTS_I32 = 0
 SP_W_COUNTS_I64 = 1
 SP_W_PROB_F64 = 2
@@ -62,6 +66,8 @@ SYMBOLS = {
                                         _vp]),
     "sp_gamma_snapshot": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i32, ctypes.c_double, _vp, _vp]),
     "sp_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "sp_debug_set": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "sp_debug_get": (ctypes.c_int, [ctypes.c_int]),
     "sp_last_error_string": (ctypes.c_char_p, []),
     "sp_version": (ctypes.c_char_p, []),
 }
@@ -425,3 +431,25 @@ class PrefixIndex:
             _dev(out_depth, torch.int32, "match_depth"), _stream(stream, dev))
         _check(st, "sp_match_longest_prefix")
         return out_entry, out_depth
+
+
+# ---------------------------------------------------------------------------------------------
+# comparison / test hooks
+# ---------------------------------------------------------------------------------------------
+class debug:
+    """Context manager: `with sp.debug(SP_DBG_NO_HULL=1): ...` sets process-wide kernel-path
+    hooks (sp_debug_set) and restores the previous values on exit."""
+
+    def __init__(self, **flags):
+        self.flags = {globals()[k]: int(v) for k, v in flags.items()}
+        self.prev = {}
+
+    def __enter__(self):
+        for f, v in self.flags.items():
+            self.prev[f] = int(lib().sp_debug_set(f, v))
+        return self
+
+    def __exit__(self, *exc):
+        for f, v in self.prev.items():
+            lib().sp_debug_set(f, v)
+        return False

@@ -129,11 +129,8 @@ def test_hull_matches_dc_kernel_w5_rows(dev):
     H = wl.make_dense_hist(cfg, seed=4).numpy()
     a = place(H, 64, dev)
     assert a["stats"]["entries_hull"] == 40
-    os.environ["SP_NO_HULL"] = "1"
-    try:
+    with sp.debug(SP_DBG_NO_HULL=1):
         b = place(H, 64, dev)
-    finally:
-        del os.environ["SP_NO_HULL"]
     assert b["stats"]["entries_hull"] == 0
     for k in ("pos", "npos", "cost", "cbb"):
         assert (a[k] == b[k]).all(), k
@@ -161,11 +158,8 @@ def test_hull_vs_dc_every_w5_entry(dev):
     cfg = wl.CONFIGS["W5"]
     H = wl.make_dense_hist(cfg, seed=0, device=dev)
     a = sp.place_checkpoints(H, cfg.M, cost_by_budget=True)
-    os.environ["SP_NO_HULL"] = "1"
-    try:
+    with sp.debug(SP_DBG_NO_HULL=1):
         b = sp.place_checkpoints(H, cfg.M, cost_by_budget=True)
-    finally:
-        del os.environ["SP_NO_HULL"]
     torch.cuda.synchronize()
     for x, y, name in zip(a, b, ("pos", "npos", "cost", "cbb")):
         assert torch.equal(x, y), name
@@ -183,11 +177,8 @@ def test_hull_int64_path_large_counts(dev):
     # hulls of large-n rows outgrow the shared rings more often; the global-ring pool is
     # bounded, so a few entries may reach the D&C -- the outputs are identical either way
     assert a["stats"]["entries_i64"] == 96 and a["stats"]["entries_hull"] >= 80
-    os.environ["SP_NO_HULL"] = "1"
-    try:
+    with sp.debug(SP_DBG_NO_HULL=1):
         b = place(H, 64, dev, dtype=torch.int64)
-    finally:
-        del os.environ["SP_NO_HULL"]
     for k in ("pos", "npos", "cost", "cbb"):
         assert (a[k] == b[k]).all(), k
     check(H, 64, a, rows=[0, 7, 50])
@@ -212,11 +203,8 @@ def test_hull_f64_path_vs_exact(dev):
         assert f64_within(r["cbb"][e], vcbb[e] / n[e], H[e]).all(), e
         got = oracle.expected_cost_f64(W[e], r["pos"][e, :r["npos"][e]])
         assert f64_within([got], [vint[e] / n[e]], H[e]).all(), e
-    os.environ["SP_NO_HULL"] = "1"
-    try:
+    with sp.debug(SP_DBG_NO_HULL=1):
         d = place(W, 64, dev, dtype=torch.float64)
-    finally:
-        del os.environ["SP_NO_HULL"]
     for e in range(24):
         assert f64_within([d["cost"][e]], [vint[e] / n[e]], H[e]).all(), e
         assert f64_within(d["cbb"][e], vcbb[e] / n[e], H[e]).all(), e
@@ -311,3 +299,19 @@ def test_one_warp_mode_on_small_batches(dev):
     assert rc == 0 and "onewarp ok" in out, out
     rc, out = run_with_env(ONEWARP_SCRIPT.replace("onewarp ok", "split ok"), SP_HULL_SPLIT="1")
     assert rc == 0 and "split ok" in out, out
+
+
+
+def test_huge_counts_flag_overflow(dev):
+    """int64 counts whose row sum would wrap int64 (four counts of 2^62) or that exceed 2^47
+    must come back as -SP_ERR_OVERFLOW (header contract), never as a silent int32-path answer;
+    a negative count as -SP_ERR_BAD_ARGUMENT.  The other entries of the batch stay exact."""
+    N, M = 40, 5
+    H = dense(6, N, seed=31).astype(np.int64)
+    H[1, 1:5] = 1 << 62            # sums to 2^64: wraps to 0 in int64
+    H[2, 7] = 1 << 48
+    H[4, 3] = -1
+    r = place(H, M, dev, dtype=torch.int64)
+    assert r["npos"][1] == -sp.SP_ERR_OVERFLOW and r["npos"][2] == -sp.SP_ERR_OVERFLOW
+    assert r["npos"][4] == -sp.SP_ERR_BAD_ARGUMENT
+    check(H, M, r, rows=[0, 3, 5])

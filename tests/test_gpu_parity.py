@@ -405,7 +405,7 @@ def test_expected_recompute_baselines(dev):
 
 
 def test_expected_recompute_prefix_widths(dev):
-    """int32 rows through both shared-prefix widths (2-byte default, 4-byte SP_EVAL_P32) and
+    """int32 rows through both shared-prefix widths (2-byte, 4-byte: SP_DBG_EVAL_PATH) and
     rows whose 1024-bin segments hold >= 2^16 (resp. >= 2^31 in total) counts, which take the
     exact global-memory path, against the oracle's definitional walk."""
     import os
@@ -416,17 +416,12 @@ def test_expected_recompute_prefix_widths(dev):
     N = cfg.N
     pos, npos, _ = sp.baseline_sets(N, budgets=(1, 7, 64), blocks=(64, 128), device=dev)
     rc, rw = oracle.eval_batch(H, np_(pos), np_(npos), broadcast=True, nthreads=8)
-    for env in (None, "SP_EVAL_P32", "SP_EVAL_CHUNKED"):
-        if env:
-            os.environ[env] = "1"
-        try:
+    for path in (0, 3, 2, 1):   # automatic (broadcast tables), 2-byte / 4-byte prefixes, chunked
+        with sp.debug(SP_DBG_EVAL_PATH=path):
             cost, worst = sp.expected_recompute(torch.from_numpy(H).to(dev), pos, npos,
                                                 broadcast=True)
             torch.cuda.synchronize()
-        finally:
-            if env:
-                del os.environ[env]
-        assert (np_(cost) == rc).all() and (np_(worst) == rw).all(), env
+        assert (np_(cost) == rc).all() and (np_(worst) == rw).all(), path
 
 
 @pytest.mark.parametrize("N,E", [(32768, 12), (5, 37), (1000, 301)])

@@ -32,10 +32,14 @@ def test_matches_online_recursion(g):
     N, t = 40, 300
     d = rng.integers(0, N + 3, t)      # includes depths beyond N (clamped) and misses (0)
     w = np.zeros(N + 1)
+    h = 0
     for x in d:
+        if x < 1:                      # a miss is not a sample of T in {1..N} (R15)
+            continue
         w *= g
         w[min(x, N)] += 1.0
-    assert abs(w.sum() - (1 - g ** t) / (1 - g)) < 1e-9 * w.sum()
+        h += 1
+    assert abs(w.sum() - (1 - g ** h) / (1 - g)) < 1e-9 * w.sum()
     p = oracle.gamma_hist(d, N, g)
     assert np.allclose(p, w / w.sum(), rtol=1e-12, atol=1e-15)
     assert abs(p.sum() - 1) < 1e-12
@@ -79,3 +83,23 @@ def test_thm4_tracking_bound_monte_carlo():
     wts = (1 - g) * g ** (t - s) / (1 - g ** t)
     bias = (wts * np.abs(laws - laws[-1]).sum(1)).sum()
     assert np.mean(errs) <= bias + oracle.gamma_variance_term(g, t, N)
+
+
+def test_misses_are_not_samples():
+    """Thm 4 samples T_s in {1..N} conditioned on hits (reading R15):
+    interleaving misses (depth <= 0) anywhere in the stream leaves the estimate unchanged, bin 0
+    stays empty, and a stream of misses only gives the zero vector."""
+    rng = np.random.default_rng(7)
+    N = 30
+    hits = rng.integers(1, N + 4, 200)
+    for g in (0.5, 0.9, 1.0):
+        ref = oracle.gamma_hist(hits, N, g)
+        mixed = hits.tolist()
+        for _ in range(80):
+            mixed.insert(int(rng.integers(0, len(mixed) + 1)), int(rng.integers(-3, 1)))
+        p = oracle.gamma_hist(np.array(mixed), N, g)
+        assert np.array_equal(p, ref) and p[0] == 0 and abs(p.sum() - 1) < 1e-12
+        # the same via the SPEC example: misses around (2, 2, 5) at g = 0.5 (S:289)
+    p = oracle.gamma_hist([0, 2, -1, 2, 0, 5, 0], 5, 0.5)
+    assert np.allclose(p, [0, 0, 3 / 7, 0, 0, 4 / 7], rtol=0, atol=1e-15)
+    assert np.array_equal(oracle.gamma_hist([0, -2, 0], 5, 0.9), np.zeros(6))

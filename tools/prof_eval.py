@@ -1,6 +1,6 @@
 """Profiling driver for a6 (sp_expected_recompute) on W5-shaped dense histograms with the bench's
 baseline sets (balanced M, block B = 64 and 128): times the default (broadcast-table) kernel and the
-shared-prefix kernel (SP_EVAL_PREFIX) and checks that they agree on every entry."""
+shared-prefix kernel (SP_DBG_EVAL_PATH = 3) and checks that they agree on every entry."""
 import argparse
 import os
 import sys
@@ -21,9 +21,9 @@ dev = torch.device("cuda:0")
 H = wl.make_dense_hist(cfg, seed=0, device=dev)
 bpos, bnpos, _ = sp.baseline_sets(cfg.N, budgets=(cfg.M,), blocks=(64, 128), device=dev)
 out = {}
-for name, env in (("bcast", None), ("prefix", "SP_EVAL_PREFIX")):
-    if env:
-        os.environ[env] = "1"
+for name, path in (("bcast", 0), ("prefix", 3)):
+    dbg = sp.debug(SP_DBG_EVAL_PATH=path)
+    dbg.__enter__()
     ts = []
     for r in range(a.reps):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -32,8 +32,7 @@ for name, env in (("bcast", None), ("prefix", "SP_EVAL_PREFIX")):
         e.record()
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
-    if env:
-        del os.environ[env]
+    dbg.__exit__(None, None, None)
     out[name] = (c, w)
     gb = H.numel() * 4 / 1e9
     print(f"{name}: " + " ".join(f"{t:.3f}" for t in ts) + f" ms  ({gb:.2f} GB row bytes, "

@@ -26,7 +26,31 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DP cells/s (entries*N*M)"
-TRAFFIC_JSON = "r01g_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
+TRAFFIC_JSON = "r02_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
+PIPES_JSON = "r02_ncu_pipes.json"       # the same capture: issue / ALU / FMA / LSU pipe %
+
+
+def dp_update_cost():
+    """Minimal amortised SASS of one hull update on the INT pipes, and the
+    SM-cycles it needs at the lane rates measured on this pool's B200 by tools/int_rate.cu
+    (profiles/r02_int_rate.json).  Per update, with b = 1.905 back tests and f = 1.091 front
+    tests (W5 rows, tools/hull_stats.c): intercept 1 IMAD; per back test 2 IADD deltas, 2
+    IMAD.WIDE, 1 ISETP; per back pop (b - 1) and front pop (f - 1) one ring LDS + 1 address
+    op; push 2 STS + 1 address op; per front test 1 IMAD + 1 ISETP; query 1 IMAD; counters 1."""
+    b, f = 1.905, 1.091
+    alu = 2 * b + b + (b - 1) + (f - 1) + 1 + f + 1
+    imad = 1 + f + 1
+    imad_wide = 2 * b
+    lsu = (b - 1) + 2 + (f - 1)
+    rates = {"alu": 63.6, "fma_imad": 63.5, "imad_wide": 26.8, "lsu": 31.1, "issue": 128.0}
+    t = {"alu": alu / rates["alu"],
+         "fma": imad / rates["fma_imad"] + imad_wide / rates["imad_wide"],
+         "lsu": lsu / rates["lsu"],
+         "issue": (alu + imad + imad_wide + lsu) / rates["issue"]}
+    binding = max(t, key=t.get)
+    return {"ops": {"alu": round(alu, 3), "imad": round(imad, 3), "imad_wide": round(imad_wide, 3),
+                    "lsu": round(lsu, 3)},
+            "rates": rates, "clk_per_update_per_sm": t[binding], "binding": binding}
 UNIT = "cells/s"
 
 
@@ -40,6 +64,10 @@ def parse():
     ap.add_argument("--entries", type=int, default=None,
                     help="entries in total (strong) or per GPU (weak); default: the config's")
     ap.add_argument("--merge", default="sparse", choices=["sparse", "allreduce"])
+    ap.add_argument("--dp-hist", default="dense", choices=["dense", "ones", "accum"],
+                    help="DP input rows: dense depth-mode (default, SURVEY 8(d) W5); ones: all-ones "
+                         "rows (full support, the D&C worst case and Thm 1's uniform law); accum: "
+                         "accumulated rows with n ~ U[1.2e5, 1.8e5] draws (past the int32 guard)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the config's entries split over the GPUs (BASELINE configs[4]); "
                          "weak: the config's entries on every GPU")
@@ -245,7 +273,19 @@ def cpu_baseline(args, nthreads):
                        f"their {len(s['req_off']) - 1} requests): literal LCP loop + paper's "
                        f"CHT DP (int64/__int128) + definitional baseline evaluation, "
                        f"{nthreads} pthreads"),
-            "seconds": dt, "seconds_lcp_dp_eval": parts}
+            "seconds": dt, "seconds_lcp_dp_eval": parts,
+            "dp_only_cells_per_s": cells / parts[1] if parts[1] > 0 else None,
+            "cpu_model": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def run_reference(args):
@@ -272,7 +312,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": nthreads, "kind": "oracle",
-                             "sample": f"first {s['E']} entries of {args.workload} per step"},
+                             "sample": f"first {s['E']} entries of {args.workload} per step",
+                             "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -285,8 +326,12 @@ def workload_config(args, world, extra):
                      + (f" ({E}/GPU)" if world > 1 else ""),
          "entries_per_gpu": E, "entries_total": E_tot, "N": cfg.N, "M": cfg.M,
          "requests_per_entry": cfg.req_per_entry, "lcp_law": cfg.shape,
-         "dp_hist": (f"dense depth-mode, n~U{list(cfg.dense_n)} draws/entry, {cfg.dense_shape} "
-                     f"laws, + the step's requests" if cfg.dense_n else "from the LCP requests"),
+         "dp_hist": ({"ones": "all-ones rows (full support) + the step's requests",
+                      "accum": f"accumulated depth-mode rows, n~U[120000, 180000] draws/entry, "
+                               f"{cfg.dense_shape} laws, + the step's requests"}.get(
+                         getattr(args, "dp_hist", "dense"))
+                     or (f"dense depth-mode, n~U{list(cfg.dense_n)} draws/entry, {cfg.dense_shape} "
+                         f"laws, + the step's requests" if cfg.dense_n else "from the LCP requests")),
          "parallelism": f"entries sharded over {world} GPU(s) ({args.scaling} scaling)",
          "merge": None if world == 1 else args.merge,
          "l2": "inputs larger than L2 (request tokens and histograms >> 126 MB)"}
@@ -319,7 +364,8 @@ class HotPath:
     (world > 1: the one exchange step, paper_2605_05219_b200.dist), a3-a5 DP on the owned
     entries, a6 baseline evaluation."""
 
-    def __init__(self, cfg, E_tot, E_own, world, rank, merge, seed, dev, ops=None):
+    def __init__(self, cfg, E_tot, E_own, world, rank, merge, seed, dev, ops=None,
+                 dp_hist="dense"):
         import torch
         from paper_2605_05219_b200 import workload as wl
         if ops is None:
@@ -331,7 +377,14 @@ class HotPath:
         tcfg = wl.scaled(cfg, E_tot)
         self.tr = tr = wl.make_trace(tcfg, seed=seed, device=dev, world=world, rank=rank)
         self.R = tr["req_off"].numel() - 1
-        if cfg.dense_n:
+        if dp_hist == "ones":
+            self.hist = wl.uniform_hist(E_own, N, device=dev)
+        elif dp_hist == "accum":
+            import dataclasses
+            acfg = dataclasses.replace(tcfg, dense_n=(120000, 180000))
+            self.hist = wl.make_dense_hist(acfg, seed=seed, device=dev, entry_begin=self.e0,
+                                           n_entries=E_own)
+        elif cfg.dense_n:
             self.hist = wl.make_dense_hist(tcfg, seed=seed, device=dev, entry_begin=self.e0,
                                            n_entries=E_own)
         else:
@@ -419,7 +472,8 @@ def run_ours(args):
     E_tot, E_own = plan_entries(args, cfg, world)
     e0 = rank * E_own
     N, M = cfg.N, cfg.M
-    hp = HotPath(cfg, E_tot, E_own, world, rank, args.merge, args.seed, dev)
+    hp = HotPath(cfg, E_tot, E_own, world, rank, args.merge, args.seed, dev,
+                 dp_hist=args.dp_hist)
     tr, hist, R = hp.tr, hp.hist, hp.R
     positions, npos, cost, cbb, bcost, bworst = (hp.positions, hp.npos, hp.cost, hp.cbb,
                                                  hp.bcost, hp.bworst)
@@ -580,23 +634,23 @@ def run_ours(args):
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
-    # DP roofline: INT-ALU bound, no tensor cores (min-plus).  The algorithmic
+    # DP roofline: INT-pipe bound, no tensor cores (min-plus).  The algorithmic
     # unit is one hull update -- one (layer, support row) step of the paper's monotone CHT
-    # (P:764-773): intercept, amortised back-pop tests, push, front test, query -- counted
-    # exactly by the kernel (support rows x M).  Its minimal INT-pipe cost is UPD_OPS thread
-    # instructions (DESIGN.md derivation); the INT pipes (ALU + FMA, 64 lanes/clk/SM each)
-    # retire 128 thread-ops/clk/SM, so peak = SMs * f_max * 128 / UPD_OPS updates/s.
-    UPD_OPS = 24
+    # -- counted exactly by the kernel (support rows x M).  Peak = the minimal
+    # amortised SASS of an update (dp_update_cost) on the INT pipes at the rates measured by
+    # tools/int_rate.cu on this B200 (profiles/r02_int_rate.json).
+    upd = dp_update_cost()
     updates = stats["hull_event_rows"] * M
-    traffic = {}
-    try:   # DRAM bytes per launch from the committed `ncu --set full` capture (W5 config)
-        if args.workload == "W5" and E_own == 16384:
+    traffic, pipes = {}, {}
+    try:   # DRAM bytes and pipe utilisation per launch from the committed `ncu --set full`
+        if args.workload == "W5" and E_own == 16384 and args.dp_hist == "dense":
             traffic = json.load(open(os.path.join(ROOT, "profiles", TRAFFIC_JSON)))
+            pipes = json.load(open(os.path.join(ROOT, "profiles", PIPES_JSON)))
     except Exception:
-        traffic = {}
+        traffic, pipes = traffic or {}, {}
     dp_launch_s = dp_ms / K / 1e3
     achieved = updates / dp_launch_s / 1e9
-    peak = sms * sm_max * 1e6 * 128 / UPD_OPS / 1e9
+    peak = sms * sm_max * 1e6 / upd["clk_per_update_per_sm"] / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True,
@@ -606,7 +660,7 @@ def run_ours(args):
         "lcp_tokens_per_s": tokens_all * K / (lcp_ms / 1e3),
         "stage_ms_per_step": {"lcp_hist": lcp_ms / K, "merge": merge_ms / K, "dp": dp_ms / K,
                               "eval": eval_ms / K},
-        "roofline": {"bound": "alu", "kernel": "dp_hull_kernel", "achieved": achieved,
+        "roofline": {"bound": "alu", "kernel": "dp_hull_kernel<int32> (dp_hull_split_kernel for < 1.5 entries per resident warp)", "achieved": achieved,
                      "peak": peak, "unit": "Gupd/s", "frac": achieved / peak,
                      "traffic": traffic.get("dp_hull_kernel<int, 2, int>", {}).get("traffic_bytes"),
                      "work": f"{updates} hull updates per launch = {stats['hull_event_rows']} "
@@ -615,8 +669,15 @@ def run_ours(args):
                              f"{stats['entries_hull']} entries on the hull kernel, "
                              f"{E_own - stats['entries_hull']} on the D&C fallback "
                              f"({stats['evaluations']} candidate evaluations)",
-                     "peak_basis": f"{sms} SMs x {sm_max:.0f} MHz x 128 INT lanes / "
-                                   f"{UPD_OPS} INT ops per hull update"},
+                     "peak_basis": (f"{sms} SMs x {sm_max:.0f} MHz / {upd['clk_per_update_per_sm']:.4f} "
+                                    f"SM-cycles per update (binding pipe: {upd['binding']}); "
+                                    f"minimal amortised update = {upd['ops']} at measured lanes/clk/SM "
+                                    f"{upd['rates']}"),
+                     "pipes_ncu": pipes.get("dp_hull_kernel<int, 2, int>"),
+                     "support_fraction": stats["hull_event_rows"] / max(1, stats["entries_hull"]) / N
+                     if stats["entries_hull"] else None,
+                     "support_updates_per_s": updates / dp_launch_s,
+                     "dense_cells_per_s": E_own * N * M / dp_launch_s},
         "roofline_lcp": {"bound": "hbm", "kernel": "lcp_hist_kernel",
                          "achieved": lcp_bytes_all * K / (lcp_ms / 1e3) / 1e9 / world,
                          "peak": hbm_peak, "unit": "GB/s",
@@ -631,9 +692,10 @@ def run_ours(args):
                           "traffic": traffic.get(f"eval_bcast_kernel<{S}>", {}).get("traffic_bytes"),
                           "algorithmic_bytes": eval_bytes},
         "dp_paths": {k: v for k, v in stats.items()},
-        # per step: lcp_hist, support_count (+ CUB's radix-sort kernels), dp_hull<int32>,
-        # dp_hull<int64> (its list; exits at once when empty), dp_place (the D&C list; ditto),
-        # eval (+ accumulate_depths for the sparse merge).  Counted: our kernels only.
+        # per step: lcp_hist, row_stats (+ CUB's radix-sort kernels), dp_hull<int32> (or
+        # dp_hull_split for small batches), dp_hull<int64> (its list; exits at once when empty),
+        # dp_place (the D&C list; ditto), eval (+ accumulate_depths for the sparse merge).
+        # Counted: our kernels only.
         "gpu_launches": K * (6 + (1 if world > 1 and args.merge == "sparse" else 0)),
         "clocks": clk,
         "e2e": e2e,

@@ -49,7 +49,7 @@ def main():
         hdr, units = rows[0], rows[1]
         out_txt = [f"# ncu --set full --clock-control none: `{a.cmd}`",
                    f"# report: {os.path.basename(a.full)} (not committed); first captured launch per kernel", ""]
-        traffic = {}
+        traffic, pipes = {}, {}
         seen = set()
         for r in rows[2:]:
             kn = r[hdr.index("Kernel Name")]
@@ -81,9 +81,16 @@ def main():
                            "duration_ns": vals.get("gpu__time_duration.sum", 0) * 1e6
                            if "gpu__time_duration.sum" in vals else None,
                            "inst_executed": vals.get("smsp__inst_executed.sum")}
+            pipes[sk] = {"issue_active_pct": vals.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                         "alu_pct": vals.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                         "fma_pct": vals.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                         "lsu_pct": vals.get("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"),
+                         "warps_active_pct": vals.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                         "dram_throughput_pct": vals.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
         os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
         open(os.path.join(ROOT, "profiles", f"{a.tag}_ncu_full.txt"), "w").write("\n".join(out_txt) + "\n")
         json.dump(traffic, open(os.path.join(ROOT, "profiles", f"{a.tag}_ncu_traffic.json"), "w"), indent=1)
+        json.dump(pipes, open(os.path.join(ROOT, "profiles", f"{a.tag}_ncu_pipes.json"), "w"), indent=1)
     if a.launches:
         lines = [ln for ln in open(a.launches) if not ln.startswith("==")]
         lr = list(csv.reader(lines))

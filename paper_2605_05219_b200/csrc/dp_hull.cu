@@ -59,27 +59,20 @@ namespace sp {
 #define SP_HULL_CAP1 32
 #endif
 constexpr int HC0 = SP_HULL_CAP0, HC1 = SP_HULL_CAP1;
-// the int64 instantiation serves accumulated (large-count) rows, whose hulls are larger
-#ifndef SP_HULL_WCAP0
-#define SP_HULL_WCAP0 128
+// The int64 and fp64 instantiations keep a WINDOW of WC lines per layer in shared memory and every
+// older live line in a global array per layer (WRing below): they take the large hulls --
+// accumulated rows (layer-1 hulls ~100 lines), near-uniform / all-ones rows (~N/(m+1) lines in
+// layer m) and the int32 entries whose hull outgrew a shared ring.
+#ifndef SP_HULL_WCAP
+#define SP_HULL_WCAP 32
 #endif
-#ifndef SP_HULL_WCAP1
-#define SP_HULL_WCAP1 64
+constexpr int WC = SP_HULL_WCAP;
+static_assert((WC & (WC - 1)) == 0, "window capacity: a power of two");
+// row prefetch depth of the hull kernels, in 32-row chunks
+#ifndef SP_HULL_PF
+#define SP_HULL_PF 8
 #endif
-constexpr int HW0 = SP_HULL_WCAP0, HW1 = SP_HULL_WCAP1;
-// An entry whose hull outgrows a shared ring is re-run at once by the same warp on a global
-// overflow ring of HCG lines per layer, taken from a pool of HPOOL rings (a 64-bit occupancy mask
-// in the workspace head); only if that overflows too (or the pool is busy) does it go to the
-// divide-and-conquer kernel.
-#ifndef SP_HULL_HCG
-#define SP_HULL_HCG 2048
-#endif
-#ifndef SP_HULL_POOL
-#define SP_HULL_POOL 64
-#endif
-constexpr int HCG = SP_HULL_HCG;
-constexpr int HPOOL = SP_HULL_POOL;
-static_assert(HPOOL >= 1 && HPOOL <= 64, "the pool's occupancy mask is one 64-bit word");
+constexpr int HULL_PF = SP_HULL_PF;
 static_assert((HC0 & (HC0 - 1)) == 0 && (HC1 & (HC1 - 1)) == 0, "ring capacities: powers of two");
 
 __host__ __device__ __forceinline__ size_t hull_align(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -134,36 +127,24 @@ struct HullParams {
   int32_t* fb;      // fallback entry list
   uint8_t* slots;   // per-warp slots
   size_t slot;
-  void* gring;      // HPOOL global overflow rings, [ring][slot][HCG][32] lines (16 B each)
+  uint8_t* wg;      // windowed rings' global arrays: one region of wgb bytes per CTA
+  size_t wgb;       // wring_pass_bytes(N, M)
   int32_t* wide;    // entries for the int64 instantiation
   const int32_t* order;   // processing order of the entries (largest support first), or NULL
   int logcap;             // argmin-log entries usable per layer (hull_log_cap(N); tests lower it)
   const HullRowStat* rstat;   // n, T_N, first bin, guards per entry (integer weights), or NULL
 };
 
-__host__ __device__ __forceinline__ size_t hull_pool_bytes(int M) {
-  return (size_t)HPOOL * hull_K(M) * HCG * 32 * 16;   // sized for Line<long long>
+// Global capacity (lines, a power of two) of layer m's windowed ring: ~1.125x the hull size of
+// the uniform law in layer m, (N+1)/(m+1) (the deque spans opt_m(j) ~ j m/(m+1) to j), at least 256
+// (accumulated W5 rows: <= ~100 lines); a hull that outgrows it goes to the D&C kernel.
+__host__ __device__ __forceinline__ int wring_cap(int N, int m) {
+  long c = (long)(N + 1) * 9 / (8 * (long)(m + 1)) + 64;
+  if (c < 256) c = 256;
+  int p = 256;
+  while (p < c) p <<= 1;
+  return p;
 }
-
-// claim / return a global overflow ring (lane 0 only)
-__device__ __forceinline__ int pool_acquire(const HullParams& p) {
-  unsigned long long* mask = reinterpret_cast<unsigned long long*>(p.ws + SP_WS_POOL_OFF);
-  unsigned long long m = *reinterpret_cast<volatile unsigned long long*>(mask);
-  for (int tries = 0; tries < 64; ++tries) {
-    const unsigned long long fr = ~m & ((HPOOL == 64) ? ~0ull : ((1ull << HPOOL) - 1));
-    if (!fr) return -1;
-    const int g = __ffsll((long long)fr) - 1;
-    const unsigned long long old = atomicOr(mask, 1ull << g);
-    if (!(old & (1ull << g))) return g;
-    m = old | (1ull << g);
-  }
-  return -1;
-}
-__device__ __forceinline__ void pool_release(const HullParams& p, int g) {
-  __threadfence();
-  atomicAnd(reinterpret_cast<unsigned long long*>(p.ws + SP_WS_POOL_OFF), ~(1ull << g));
-}
-
 // log slot of layer m (1-based), lane-major within a pass: [pass][slot k][lane]
 __device__ __forceinline__ int hull_layer_slot(int K, int m) {
   const int L = 32 * K;
@@ -211,8 +192,8 @@ struct Line {
 };
 
 // Ring storage policies, [slot][pos][lane] so that every lane has its own banks: SRingI (int32
-// lines, below) and SRingW (int64 / fp64 lines) in shared memory, GRing for a global overflow
-// ring from the pool.
+// lines, below) and SRingW (int64 / fp64 lines) in shared memory; WRing (int64 / fp64) = an
+// SRingW window + per-layer global arrays for large hulls.
 
 // double-double sums for the fp64 path (prefix sums rounded once, T_N, the definitional cost)
 struct hdd {
@@ -273,6 +254,14 @@ struct SRingI {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a + ds), "h"((unsigned short)v.s) : "memory");
   }
   static constexpr int cap(int k) { return k ? C1 : C0; }
+  __device__ __forceinline__ Line<int> ldh(int k, int pos, int) const { return ld(k, pos); }
+  __device__ __forceinline__ void sth(int k, int pos, Line<int> v, int, int) const { st(k, pos, v); }
+  __device__ __forceinline__ int span_cap(int k) const { return cap(k); }
+  __device__ __forceinline__ void begin_pass(uint8_t*, int, int, int, int) {}
+  __device__ __forceinline__ Line<int> ldw(int k, int pos) const { return ld(k, pos); }
+  __device__ __forceinline__ void stw(int k, int pos, Line<int> v) const { st(k, pos, v); }
+  static constexpr bool kWindowed = false;
+  static constexpr int window(int k) { return cap(k); }
   static constexpr int UNIT = 1;
   static constexpr size_t bytes(int K) { return (size_t)(C0 + (K == 2 ? C1 : 0)) * 192; }
   __device__ __forceinline__ void ld2(int k, int pos, int& b, int& sv) const {
@@ -316,17 +305,98 @@ struct SRingW {
   static constexpr int cap(int k) { return k ? C1 : C0; }
 };
 
-template <typename VT, int C>
-struct GRing {
-  Line<VT>* base;   // one ring of the global pool
-  __device__ __forceinline__ int idx(int k, int pos) const {
-    return k * C * 32 + ((pos & (C - 1)) << 5) + lane_id();
+// Windowed ring.  hi = the largest position written since the entry's pass began.  Invariant for
+// every live position q (fr <= q <= bk): q > hi - C -> the shared-memory window slot q mod C
+// holds q; otherwise the global array holds it at q mod cap.  A push at pos = hi + 1 moves line
+// pos - C (if live) from the window to the global array; a push at pos <= hi - C (after deep
+// back pops) writes the global array as well.  So the hot end -- the back, and the front of
+// small hulls -- stays in shared memory and only large hulls touch global memory.
+//   int32 lines: window SRingI<HC0, HC1> (64 / 32 lines), global arrays of WSMALL lines: a hull
+//     past them goes to the int64 instantiation;
+//   int64 / fp64 lines: window SRingW<WC, WC>, global arrays of wring_cap(N, m) lines: a hull
+//     past them goes to the D&C kernel.
+constexpr int WSMALL = 256;
+template <typename VT>
+struct GLineT {   // a global line
+  long long b;
+  int s, pad;
+};
+template <>
+struct GLineT<int> {
+  int b, s;
+};
+template <typename VT>
+__host__ __device__ __forceinline__ int wring_cap_t(int N, int m) {
+  return std::is_same<VT, int>::value ? WSMALL : wring_cap(N, m);
+}
+// bytes of one CTA's global arrays: the largest pass (the first: lowest layers, largest caps)
+template <typename VT>
+__host__ __device__ __forceinline__ size_t wring_pass_bytes_t(int N, int M) {
+  const int L = 32 * hull_K(M);
+  size_t n = 0;
+  for (int m = 1; m <= L; ++m) n += (size_t)wring_cap_t<VT>(N, m);
+  return hull_align(n * sizeof(GLineT<VT>));
+}
+
+template <typename VT, class SM>
+struct WRing {
+  SM sm;
+  GLineT<VT>* g[2];   // this lane's chain for slot 0 / 1 in the current pass
+  int gm[2];          // its capacity - 1
+  __device__ __forceinline__ Line<VT> gld(int k, int pos) const {
+    const GLineT<VT> l = g[k][pos & gm[k]];
+    Line<VT> v;
+    if constexpr (std::is_same<VT, double>::value) v.b = __longlong_as_double(l.b);
+    else v.b = (VT)l.b;
+    v.s = l.s;
+    return v;
   }
-  __device__ __forceinline__ Line<VT> ld(int k, int pos) const { return base[idx(k, pos)]; }
-  __device__ __forceinline__ Line<VT> ld_back(int k, int b, int t) const { return ld(k, b - t); }
-  __device__ __forceinline__ Line<VT> ld_front(int k, int f, int t) const { return ld(k, f + t); }
-  __device__ __forceinline__ void st(int k, int pos, Line<VT> v) const { base[idx(k, pos)] = v; }
-  static constexpr int cap(int) { return C; }
+  __device__ __forceinline__ void gst(int k, int pos, Line<VT> v) const {
+    GLineT<VT> l;
+    if constexpr (std::is_same<VT, double>::value) l.b = __double_as_longlong(v.b);
+    else l.b = v.b;
+    l.s = v.s;
+    if constexpr (!std::is_same<VT, int>::value) l.pad = 0;
+    g[k][pos & gm[k]] = l;
+  }
+  __device__ __forceinline__ Line<VT> ldh(int k, int pos, int hi) const {
+    return pos > hi - SM::cap(k) ? sm.ld(k, pos) : gld(k, pos);
+  }
+  __device__ __forceinline__ void sth(int k, int pos, Line<VT> v, int hi, int fr) const {
+    const int C = SM::cap(k);
+    if (pos > hi) {
+      if (pos - C >= fr) gst(k, pos - C, sm.ld(k, pos));   // the slot holds pos - C
+    } else if (pos <= hi - C) {
+      gst(k, pos, v);
+    }
+    sm.st(k, pos, v);
+  }
+  __device__ __forceinline__ int span_cap(int k) const { return gm[k] + 1; }
+  // plain window accesses (exact while the deque lies within C - 2 of hi: see hull_dp)
+  __device__ __forceinline__ Line<VT> ldw(int k, int pos) const { return sm.ld(k, pos); }
+  __device__ __forceinline__ void stw(int k, int pos, Line<VT> v) const { sm.st(k, pos, v); }
+  static constexpr bool kWindowed = true;
+  static constexpr int window(int k) { return SM::cap(k); }
+  // point g[] at this pass's chains: the layers of a pass are laid out in order
+  __device__ __forceinline__ void begin_pass(uint8_t* base, int N, int M, int ps, int L) {
+    const int lane = lane_id();
+    size_t off = 0;
+    for (int q = 0; q < L; ++q) {   // every slot, active or not (inactive lanes still load/store)
+      const int m = ps * L + q + 1;
+      const int c = wring_cap_t<VT>(N, m);
+      if ((q & 31) == lane) {   // (constant indices: g[] stays in registers)
+        GLineT<VT>* gp = reinterpret_cast<GLineT<VT>*>(base) + off;
+        if ((q >> 5) == 0) {
+          g[0] = gp;
+          gm[0] = c - 1;
+        } else {
+          g[1] = gp;
+          gm[1] = c - 1;
+        }
+      }
+      off += (size_t)c;
+    }
+  }
 };
 
 // value of the dummy front line (above every candidate)
@@ -375,7 +445,7 @@ struct SplitSync {
 // predicates vanish at compile time
 template <typename WT, typename VT, int K, bool ALLACT, class RING>
 __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
-                                        HullCT<VT> TN, VT nV, const RING rg, uint32_t* logs,
+                                        HullCT<VT> TN, VT nV, RING rg, uint32_t* logs,
                                         int32_t* logn, VT* ebuf0, VT* ebuf1,
                                         unsigned& pops_e, unsigned& ev_e, bool& logfull,
                                         const SplitSync* ss = nullptr, int ps_only = -1) {
@@ -396,7 +466,8 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
     // below the back and the two above the front are loaded from the ring at the top of every
     // support row (positions known a row ahead, so the loads overlap the shuffle).  A line is
     // (intercept b_s, s).  eo = e_m(j) (the running row value), op = opt_m(j).
-    int f[K], b[K], op[K], cnt[K];
+    int f[K], b[K], op[K], cnt[K], hi[K];
+    rg.begin_pass(p.wg + (size_t)blockIdx.x * p.wgb, N, M, ps, L);
     VT eo[K];
     Line<VT> B0[K], F0[K];
     bool act[K];
@@ -415,17 +486,25 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       // the deque starts with a dummy line of value +inf at every query: the first push pops
       // it from the front, so the deque is never empty at a push
       B0[k] = F0[k] = Line<VT>{hull_inf<VT>(), 0};
-      rg.st(k, 0, F0[k]);
+      rg.sth(k, 0, F0[k], -1, 0);
+      hi[k] = 0;   // the largest position written (the windowed ring's threshold)
     }
     VT carry = 0, Pm1 = 0;
     hdd carry_dd{0.0, 0.0};
     int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
-    // the counts of the next 32-row chunk are loaded one chunk ahead (HBM latency off the path)
-    VT cnext = 1 + lane <= N ? (VT)we[1 + lane] : (VT)0;
+    // the counts are loaded HULL_PF chunks (32 rows each) ahead: a chunk of W5's rows holds ~5
+    // support rows, but sparse rows (W2/W3: ~0.2-2% support) would otherwise wait for HBM on
+    // every 32 rows
+    VT cq[HULL_PF];
+#pragma unroll
+    for (int c = 0; c < HULL_PF; ++c)
+      cq[c] = 32 * c + 1 + lane <= N ? (VT)we[32 * c + 1 + lane] : (VT)0;
     for (int jb = 0; jb < N; jb += 32) {
       const int jr = jb + 1 + lane;
-      const VT craw = cnext;
-      cnext = jr + 32 <= N ? (VT)we[jr + 32] : (VT)0;
+      const VT craw = cq[0];
+#pragma unroll
+      for (int c = 0; c + 1 < HULL_PF; ++c) cq[c] = cq[c + 1];
+      cq[HULL_PF - 1] = jr + 32 * HULL_PF <= N ? (VT)we[jr + 32 * HULL_PF] : (VT)0;
       unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
       if (evmask == 0) continue;                          // 32 zero rows: nothing changes
       VT Pc;
@@ -476,14 +555,33 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         const int i = __ffs(evmask) - 1;
         evmask &= evmask - 1;
         const int j = jb + 1 + i;
-        // ring lines around both ends (positions fixed by the previous row)
-        Line<VT> L1[K], L2[K], G1[K], G2[K];
+        // ring lines around both ends (positions fixed by the previous row).  Windowed rings:
+        // while every lane's deque lies within C - 2 positions of its high-water mark (the
+        // common case) every line it touches this row is in the shared window -- plain shared
+        // loads and stores; otherwise (warp-uniform) the checked window / global accesses.
+        bool wbig = false;
+        if constexpr (RING::kWindowed) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          L1[k] = rg.ld_back(k, b[k], 1);
-          L2[k] = rg.ld_back(k, b[k], 2);
-          G1[k] = rg.ld_front(k, f[k], 1);
-          G2[k] = rg.ld_front(k, f[k], 2);
+          for (int k = 0; k < K; ++k) wbig |= act[k] & (hi[k] - f[k] >= RING::window(k) - 2);
+        }
+        const bool win = RING::kWindowed && __any_sync(FULL, wbig);
+        Line<VT> L1[K], L2[K], G1[K], G2[K];
+        if (win) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            L1[k] = rg.ldh(k, b[k] - 1, hi[k]);
+            L2[k] = rg.ldh(k, b[k] - 2, hi[k]);
+            G1[k] = rg.ldh(k, f[k] + 1, hi[k]);
+            G2[k] = rg.ldh(k, f[k] + 2, hi[k]);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            L1[k] = rg.ldw(k, b[k] - 1);
+            L2[k] = rg.ldw(k, b[k] - 2);
+            G1[k] = rg.ldw(k, f[k] + 1);
+            G2[k] = rg.ldw(k, f[k] + 2);
+          }
         }
         // e_{m-1}(j-1): from the lane below (its value at the previous support row);
         // lane 0 slot 0 from the previous pass (or e_0 = 0)
@@ -541,7 +639,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
             int cs = L2[k].s - j;
             VT cb = L2[k].b - bj[k];
             while (top[k] - f[k] >= 1) {
-              const Line<VT> l1 = rg.ld(k, top[k] - 1);
+              const Line<VT> l1 = rg.ldh(k, top[k] - 1, hi[k]);
               const int ls = l1.s - j;
               const VT lb = l1.b - bj[k];
               if (pop_test(ls, lb, cs, cb)) {
@@ -560,14 +658,18 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         for (int k = 0; k < K; ++k) {
           const int nb = skip[k] ? b[k] : top[k] + 1;
           const Line<VT> nl{bj[k], j};
-          if (!skip[k]) rg.st(k, nb, nl);
+          if (!skip[k]) {
+            if (win) rg.sth(k, nb, nl, hi[k], f[k]);
+            else rg.stw(k, nb, nl);
+            hi[k] = max(hi[k], nb);
+          }
           const int d = nb - f[k];
           const bool fresh = !skip[k];
           const Line<VT> F1 = (fresh & (d == 1)) ? nl : G1[k];   // lines f+1 / f+2 popped or new
           const Line<VT> F2 = (fresh & (d == 2)) ? nl : G2[k];
           B0[k] = skip[k] ? B0[k] : nl;
           b[k] = nb;
-          ovf |= act[k] & (d >= RING::cap(k));
+          ovf |= act[k] & (d >= rg.span_cap(k));
           // ---- query x = P_j: up to one front pop decided from the loaded lines -------------
           v0[k] = F0[k].b + (VT)F0[k].s * nPj;
           v1[k] = F1.b + (VT)F1.s * nPj;
@@ -591,7 +693,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
             if (!q2[k]) continue;
             f[k] += 2;   // F0 = line f+2 already
             while (f[k] < b[k]) {
-              const Line<VT> l1 = rg.ld(k, f[k] + 1);
+              const Line<VT> l1 = rg.ldh(k, f[k] + 1, hi[k]);
               const VT vl = l1.b + (VT)l1.s * nPj;
               if (vl < v0[k]) {
                 ++f[k];
@@ -715,18 +817,18 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
   constexpr bool F64 = std::is_same<VT, double>::value;
   constexpr bool WIDE = std::is_same<VT, long long>::value;
   const int lane = threadIdx.x;
-  constexpr int C0 = WIDE ? HW0 : HC0, C1 = WIDE ? HW1 : HC1;
   extern __shared__ __align__(16) uint8_t sring[];   // ring_bytes<K, VT>()
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
-  using SR = typename std::conditional<std::is_same<VT, int>::value, SRingI<C0, C1>,
-                                       SRingW<VT, C0, C1>>::type;
+  using SR = typename std::conditional<std::is_same<VT, int>::value,
+                                       WRing<int, SRingI<HC0, HC1>>,
+                                       WRing<VT, SRingW<VT, WC, WC>>>::type;
   SR srg;
   if constexpr (sizeof(VT) == 8) {
-    srg.b0 = sbase + 8u * (uint32_t)lane;
-    srg.ds = 256u - 4u * (uint32_t)lane;
+    srg.sm.b0 = sbase + 8u * (uint32_t)lane;
+    srg.sm.ds = 256u - 4u * (uint32_t)lane;
   } else {
-    srg.b0 = sbase + 4u * (uint32_t)lane;
-    srg.ds = 128u - 2u * (uint32_t)lane;
+    srg.sm.b0 = sbase + 4u * (uint32_t)lane;
+    srg.sm.ds = 128u - 2u * (uint32_t)lane;
   }
   const int N = p.N, M = p.M;
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
@@ -830,27 +932,37 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
     unsigned pops_e = 0, ev_e = 0;
     bool logfull = false;
     const bool fullm = M % (32 * K) == 0;
-    bool ovf = fullm ? hull_dp<WT, VT, K, true>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1,
-                                                pops_e, ev_e, logfull)
-                     : hull_dp<WT, VT, K, false>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1,
-                                                 pops_e, ev_e, logfull);
-    if (ovf && !logfull) {   // retry with a global overflow ring from the pool (rare)
-      int g = -1;
-      if (lane == 0) g = pool_acquire(p);
-      g = __shfl_sync(FULL, g, 0);
-      if (g >= 0) {
+    bool ovf;
+    if constexpr (std::is_same<VT, int>::value) {
+      // int32: plain shared rings first (W5: 16 of 16384 entries outgrow them); an entry whose
+      // hull outgrows a ring is re-run at once with the windowed ring (the same window plus
+      // global arrays of WSMALL lines)
+      ovf = fullm ? hull_dp<WT, VT, K, true>(p, we, e, TN, nV, srg.sm, logs, logn, ebuf0, ebuf1,
+                                             pops_e, ev_e, logfull)
+                  : hull_dp<WT, VT, K, false>(p, we, e, TN, nV, srg.sm, logs, logn, ebuf0, ebuf1,
+                                              pops_e, ev_e, logfull);
+      if (ovf && !logfull) {
         pops_e = ev_e = 0;
-        Line<VT>* gr = reinterpret_cast<Line<VT>*>(p.gring) + (size_t)g * K * HCG * 32;
-        ovf = hull_dp<WT, VT, K, false>(p, we, e, TN, nV, GRing<VT, HCG>{gr}, logs, logn, ebuf0,
-                                        ebuf1, pops_e, ev_e, logfull);
         __syncwarp();
-        if (lane == 0) pool_release(p, g);
+        ovf = hull_dp<WT, VT, K, false>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1, pops_e,
+                                        ev_e, logfull);
       }
+    } else {
+      ovf = fullm ? hull_dp<WT, VT, K, true>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1,
+                                             pops_e, ev_e, logfull)
+                  : hull_dp<WT, VT, K, false>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1,
+                                              pops_e, ev_e, logfull);
     }
     pops += pops_e;
     events += ev_e;
     if (ovf) {
-      if (lane == 0) p.fb[atomicAdd(fb_n, 1u)] = e;
+      // int32: a shared ring or a log filled -- the int64 instantiation (windowed rings, exact
+      // for narrow entries too) re-runs the entry; int64 / fp64: a global array or a log
+      // filled -- the D&C kernel
+      if (lane == 0) {
+        if (!WIDE && !F64) p.wide[atomicAdd(wide_n, 1u)] = e;
+        else p.fb[atomicAdd(fb_n, 1u)] = e;
+      }
       continue;
     }
     __threadfence_block();
@@ -1466,10 +1578,8 @@ __global__ void __launch_bounds__(256) row_stats_kernel(const WT* __restrict__ w
 
 template <int K, typename VT>
 static constexpr size_t ring_bytes() {
-  constexpr bool W = std::is_same<VT, long long>::value;
-  constexpr int NPOS = (W ? HW0 : HC0) + (K == 2 ? (W ? HW1 : HC1) : 0);
-  if constexpr (sizeof(VT) == 8) return (size_t)NPOS * 384;
-  return (size_t)NPOS * 192;
+  if constexpr (sizeof(VT) == 8) return (size_t)(WC + (K == 2 ? WC : 0)) * 384;
+  return (size_t)(HC0 + (K == 2 ? HC1 : 0)) * 192;
 }
 
 // Host-side launch facts cached per device (the verdict's host-overhead item: no attribute,
@@ -1557,10 +1667,12 @@ static int lean_grid_t(int E) {
 static bool hull_lean() { return sp_debug_get(SP_DBG_HULL_LEAN) != 0; }
 
 template <typename WT, int K>
-static void hull_launch_t(const HullParams& p, const HullRowStat* rstat, int gn, cudaStream_t st) {
+static void hull_launch_t(HullParams p, const HullRowStat* rstat, int gn, cudaStream_t st) {
   if constexpr (std::is_same<WT, double>::value) {
+    p.wgb = wring_pass_bytes_t<double>(p.N, p.M);
     dp_hull_kernel<double, K, double><<<gn, 32, ring_bytes<K, double>(), st>>>(p);
   } else {
+    p.wgb = wring_pass_bytes_t<int>(p.N, p.M);
     if (K == 2 && !hull_lean() && p.rstat &&
         use_split(p.E, p.M, std::min(gn, hull_grid_t<WT, K, int>(p.E)))) {
       const int gs = std::min(gn, split_grid_t<WT>(p.E));
@@ -1574,6 +1686,7 @@ static void hull_launch_t(const HullParams& p, const HullRowStat* rstat, int gn,
     // the int64 instantiation on the listed entries (its warps exit at once if the list is
     // empty); its grid is clamped to the slots allocated for the widest launch
     const int gw = std::min(gn, hull_grid_t<WT, K, long long>(p.E));
+    p.wgb = wring_pass_bytes_t<long long>(p.N, p.M);
     dp_hull_kernel<WT, K, long long><<<gw, 32, ring_bytes<K, long long>(), st>>>(p);
   }
 }
@@ -1603,7 +1716,17 @@ int sp_hull_grid(int E, int N, int M, int wtype) {
 }
 
 size_t sp_hull_slot_bytes(int N, int M) { return sp::hull_slot_bytes(N, M); }
-size_t sp_hull_pool_bytes(int M) { return sp::hull_pool_bytes(M); }
+// the windowed rings' global arrays: one region per CTA, shared by the int32 and the int64 / fp64
+// instantiations (they run one after the other on the stream)
+size_t sp_hull_wg_bytes(int E, int N, int M) {
+  const bool k2 = sp::hull_K(M) == 2;
+  const size_t gi = (size_t)(k2 ? sp::hull_grid_t<int32_t, 2, int>(E) : sp::hull_grid_t<int32_t, 1, int>(E)) *
+                    sp::wring_pass_bytes_t<int>(N, M);
+  int g = k2 ? std::max(sp::hull_grid_t<int32_t, 2, long long>(E), sp::hull_grid_t<double, 2, double>(E))
+             : std::max(sp::hull_grid_t<int32_t, 1, long long>(E), sp::hull_grid_t<double, 1, double>(E));
+  g = std::max(g, k2 ? sp::hull_grid_t<int64_t, 2, long long>(E) : sp::hull_grid_t<int64_t, 1, long long>(E));
+  return std::max(gi, (size_t)g * sp::wring_pass_bytes_t<long long>(N, M));
+}
 
 // ordering scratch: key/val in, key/val out (int32 [E] each) | cub temp | row stats [E]
 static size_t order_cub_bytes(int E) {
@@ -1654,7 +1777,8 @@ cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, 
       p.order = vout;
   }
   p.rstat = wtype == SP_W_PROB_F64 ? nullptr : rstat;
-  p.gring = pool;
+  p.wg = pool;
+  p.wgb = 0;   // per instantiation, set by hull_launch_t
   p.wide = wide;
   p.w = weights;
   p.E = E;

@@ -9,16 +9,15 @@
 // internal counters, zeroed by the launch's header memset:
 #define SP_WS_FB_COUNT_OFF 192    // unsigned: entries handed from the hull kernel to the D&C
 #define SP_WS_ENTRY_CTR_OFF 200   // unsigned: next entry for the hull kernel's warps
-#define SP_WS_POOL_OFF 208        // uint64: occupancy mask of the hull kernel's overflow rings
 #define SP_WS_WIDE_COUNT_OFF 216  // unsigned: entries listed for the int64 hull instantiation
 #define SP_WS_WIDE_CTR_OFF 220    // unsigned: next listed entry for the int64 instantiation
 
-// Workspace after the head:  fallback list int32[E] | int64-path list int32[E] | overflow-ring pool
+// Workspace after the head:  fallback list int32[E] | int64-path list int32[E] | windowed rings' global arrays (int64 / fp64 instantiations)
 // | ordering scratch (support counts, radix sort) | hull slots | D&C slots
 // (each 256-B aligned)
 int sp_hull_grid(int E, int N, int M, int wtype);
 size_t sp_hull_slot_bytes(int N, int M);
-size_t sp_hull_pool_bytes(int M);
+size_t sp_hull_wg_bytes(int E, int N, int M);
 size_t sp_hull_order_bytes(int E);
 cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
                            int32_t* npos, void* cost, void* cbb, int32_t* fpos,

@@ -1611,7 +1611,7 @@ extern "C" size_t sp_place_checkpoints_workspace_bytes(int32_t n_entries, int32_
     const int gh = std::max(std::max(sp_hull_grid(n_entries, N, M, SP_W_COUNTS_I32),
                                      sp_hull_grid(n_entries, N, M, SP_W_COUNTS_I64)),
                             sp_hull_grid(n_entries, N, M, SP_W_PROB_F64));
-    hull = 2 * sp::align256(4 * (size_t)n_entries) + sp::align256(sp_hull_pool_bytes(M)) +
+    hull = 2 * sp::align256(4 * (size_t)n_entries) + sp::align256(sp_hull_wg_bytes(n_entries, N, M)) +
            sp::align256(sp_hull_order_bytes(n_entries)) + (size_t)gh * sp_hull_slot_bytes(N, M);
   }
   return SP_WS_STATS_BYTES + hull + (size_t)dp_grid(n_entries, N) * sp::slot_bytes(N, M);
@@ -1666,7 +1666,7 @@ static sp_status place_impl(const void* weights, sp_weight_type wtype,
   const size_t fb_off = SP_WS_STATS_BYTES;
   const size_t wide_off = fb_off + (use_hull ? sp::align256(4 * (size_t)n_entries) : 0);
   const size_t pool_off = wide_off + (use_hull ? sp::align256(4 * (size_t)n_entries) : 0);
-  const size_t order_off = pool_off + (use_hull ? sp::align256(sp_hull_pool_bytes(M)) : 0);
+  const size_t order_off = pool_off + (use_hull ? sp::align256(sp_hull_wg_bytes(n_entries, N, M)) : 0);
   const size_t hull_off = order_off + (use_hull ? sp::align256(sp_hull_order_bytes(n_entries)) : 0);
   const size_t dc_off = hull_off + (size_t)hgrid * (use_hull ? sp_hull_slot_bytes(N, M) : 0);
   const size_t need = dc_off + (size_t)grid * sp::slot_bytes(N, M);

@@ -399,6 +399,17 @@ struct WRing {
   }
 };
 
+template <int K, typename VT>
+__host__ __device__ constexpr size_t ring_bytes() {
+  if constexpr (sizeof(VT) == 8) return (size_t)(WC + (K == 2 ? WC : 0)) * 384;
+  return (size_t)(HC0 + (K == 2 ? HC1 : 0)) * 192;
+}
+// the row stage of one warp (a super-chunk of counts)
+template <typename VT>
+__host__ __device__ constexpr size_t stage_bytes() { return (size_t)32 * HULL_PF * sizeof(VT); }
+template <int K, typename VT>
+constexpr size_t hull_dyn_bytes() { return ring_bytes<K, VT>() + stage_bytes<VT>(); }
+
 // value of the dummy front line (above every candidate)
 template <typename VT>
 __device__ __forceinline__ VT hull_inf() {
@@ -448,7 +459,8 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
                                         HullCT<VT> TN, VT nV, RING rg, uint32_t* logs,
                                         int32_t* logn, VT* ebuf0, VT* ebuf1,
                                         unsigned& pops_e, unsigned& ev_e, bool& logfull,
-                                        const SplitSync* ss = nullptr, int ps_only = -1) {
+                                        VT* stage, const SplitSync* ss = nullptr,
+                                        int ps_only = -1) {
   const int lane = lane_id();
   const int N = p.N, M = p.M;
   const int LC = p.logcap;   // <= hull_log_cap(N), the allocated stride
@@ -495,251 +507,265 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
     // the counts are loaded HULL_PF chunks (32 rows each) ahead: a chunk of W5's rows holds ~5
     // support rows, but sparse rows (W2/W3: ~0.2-2% support) would otherwise wait for HBM on
     // every 32 rows
+    // Rows are read in super-chunks of HULL_PF chunks: the next super-chunk's counts are loaded
+    // into registers while the current one, staged in shared memory, is processed chunk by chunk
+    // (no register shuffling per chunk; an empty chunk costs a shared load and a ballot).
     VT cq[HULL_PF];
 #pragma unroll
     for (int c = 0; c < HULL_PF; ++c)
       cq[c] = 32 * c + 1 + lane <= N ? (VT)we[32 * c + 1 + lane] : (VT)0;
-    for (int jb = 0; jb < N; jb += 32) {
-      const int jr = jb + 1 + lane;
-      const VT craw = cq[0];
+    bool stop = false;
+    for (int sb = 0; sb < N && !stop; sb += 32 * HULL_PF) {
+      __syncwarp();   // the previous super-chunk's stage is consumed
 #pragma unroll
-      for (int c = 0; c + 1 < HULL_PF; ++c) cq[c] = cq[c + 1];
-      cq[HULL_PF - 1] = jr + 32 * HULL_PF <= N ? (VT)we[jr + 32 * HULL_PF] : (VT)0;
-      unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
-      if (evmask == 0) continue;                          // 32 zero rows: nothing changes
-      VT Pc;
-      if constexpr (std::is_same<VT, double>::value) {
-        // P_j from a double-double scan, rounded once (reading R10)
-        hdd inc{craw, 0.0};
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const hdd y = hdd_shfl_up(inc, o);
-          if (lane >= o) inc = hdd_add(inc, y);
-        }
-        const hdd full = hdd_add(carry_dd, inc);
-        Pc = full.hi + full.lo;
-        carry_dd = hdd_shfl(full, 31);
-      } else {
-        VT cnt32 = craw;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const VT y = __shfl_up_sync(FULL, cnt32, o);
-          if (lane >= o) cnt32 += y;
-        }
-        Pc = carry + cnt32;
-        carry = __shfl_sync(FULL, Pc, 31);
+      for (int c = 0; c < HULL_PF; ++c) {
+        stage[32 * c + lane] = cq[c];
+        const int t = sb + 32 * (HULL_PF + c) + 1 + lane;
+        cq[c] = t <= N ? (VT)we[t] : (VT)0;
       }
-      // previous pass's top layer at the support rows: e(j-1) of support row number t is its
-      // value at support row t-1 (constant over zero rows), 0 before the first
-      VT Ec = 0;
-      const int nev = __popc(evmask);
-      if (ss) {   // SPLIT mode: wait for the other warp (consumer: data; producer: ring space)
-        if (lane == 0) {
-          if (chain_in)
-            while (*ss->produced < evbase + nev - 1 && !*ss->abort_) __nanosleep(64);
-          else
-            while (evbase + nev - 1 - *ss->consumed >= SPLIT_RING && !*ss->abort_) __nanosleep(64);
+      __syncwarp();
+      for (int cc = 0; cc < HULL_PF && sb + 32 * cc < N; ++cc) {
+        const int jb = sb + 32 * cc;
+        const int jr = jb + 1 + lane;
+        const VT craw = stage[32 * cc + lane];
+        (void)jr;
+        unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
+        if (evmask == 0) continue;                          // 32 zero rows: nothing changes
+        VT Pc;
+        if constexpr (std::is_same<VT, double>::value) {
+          // P_j from a double-double scan, rounded once (reading R10)
+          hdd inc{craw, 0.0};
+  #pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const hdd y = hdd_shfl_up(inc, o);
+            if (lane >= o) inc = hdd_add(inc, y);
+          }
+          const hdd full = hdd_add(carry_dd, inc);
+          Pc = full.hi + full.lo;
+          carry_dd = hdd_shfl(full, 31);
+        } else {
+          VT cnt32 = craw;
+  #pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const VT y = __shfl_up_sync(FULL, cnt32, o);
+            if (lane >= o) cnt32 += y;
+          }
+          Pc = carry + cnt32;
+          carry = __shfl_sync(FULL, Pc, 31);
         }
-        __syncwarp();
-        if (*ss->abort_) {
+        // previous pass's top layer at the support rows: e(j-1) of support row number t is its
+        // value at support row t-1 (constant over zero rows), 0 before the first
+        VT Ec = 0;
+        const int nev = __popc(evmask);
+        if (ss) {   // SPLIT mode: wait for the other warp (consumer: data; producer: ring space)
+          if (lane == 0) {
+            if (chain_in)
+              while (*ss->produced < evbase + nev - 1 && !*ss->abort_) __nanosleep(64);
+            else
+              while (evbase + nev - 1 - *ss->consumed >= SPLIT_RING && !*ss->abort_) __nanosleep(64);
+          }
+          __syncwarp();
+          if (*ss->abort_) {
+            ovf = true;
+            break;
+          }
+          __threadfence_block();
+          if (chain_in && lane < nev)
+            Ec = evbase + lane >= 1 ? (VT)ss->ring[(evbase + lane - 1) & (SPLIT_RING - 1)] : (VT)0;
+        } else if (chain_in && lane < nev) {
+          Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
+        }
+        for (int q = 0; evmask; ++q) {
+          const int i = __ffs(evmask) - 1;
+          evmask &= evmask - 1;
+          const int j = jb + 1 + i;
+          // ring lines around both ends (positions fixed by the previous row).  Windowed rings:
+          // while every lane's deque lies within C - 2 positions of its high-water mark (the
+          // common case) every line it touches this row is in the shared window -- plain shared
+          // loads and stores; otherwise (warp-uniform) the checked window / global accesses.
+          bool wbig = false;
+          if constexpr (RING::kWindowed) {
+  #pragma unroll
+            for (int k = 0; k < K; ++k) wbig |= act[k] & (hi[k] - f[k] >= RING::window(k) - 2);
+          }
+          const bool win = RING::kWindowed && __any_sync(FULL, wbig);
+          Line<VT> L1[K], L2[K], G1[K], G2[K];
+          if (win) {
+  #pragma unroll
+            for (int k = 0; k < K; ++k) {
+              L1[k] = rg.ldh(k, b[k] - 1, hi[k]);
+              L2[k] = rg.ldh(k, b[k] - 2, hi[k]);
+              G1[k] = rg.ldh(k, f[k] + 1, hi[k]);
+              G2[k] = rg.ldh(k, f[k] + 2, hi[k]);
+            }
+          } else {
+  #pragma unroll
+            for (int k = 0; k < K; ++k) {
+              L1[k] = rg.ldw(k, b[k] - 1);
+              L2[k] = rg.ldw(k, b[k] - 2);
+              G1[k] = rg.ldw(k, f[k] + 1);
+              G2[k] = rg.ldw(k, f[k] + 2);
+            }
+          }
+          // e_{m-1}(j-1): from the lane below (its value at the previous support row);
+          // lane 0 slot 0 from the previous pass (or e_0 = 0)
+          VT in[K];
+          const VT t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
+          // unconditional (Ec = 0 without a previous pass): the row's shuffles stay in one
+          // converged region, so ptxas emits one divergence check (BRA.DIV) for all of them
+          const VT ext = __shfl_sync(FULL, Ec, q);
+          in[0] = lane ? t0 : ext;
+          if constexpr (K == 2) {
+            const VT t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
+            in[1] = lane ? t1 : t0;
+          }
+          const VT Pj = __shfl_sync(FULL, Pc, i);
+          const VT nPj = -Pj;
+          ++ev_e;
+          // ---- push line j: up to two back pops decided from the loaded lines ----------------
+          VT bj[K];
+          int top[K];
+          bool more[K], skip[K];
+  #pragma unroll
+          for (int k = 0; k < K; ++k) {
+            bj[k] = in[k] + (VT)j * Pm1;
+            // deltas of the back lines from the new point (j, bj)
+            const int s0 = B0[k].s - j, s1 = L1[k].s - j, s2 = L2[k].s - j;
+            const VT c0 = B0[k].b - bj[k], c1 = L1[k].b - bj[k], c2 = L2[k].b - bj[k];
+            // a line that overtakes the back line only beyond x = P_N = n is never optimal at a
+            // query (x <= n): it is neither pushed nor allowed to pop.
+            // x(back, new) > n  <=>  bj - B0.b > n (j - B0.s)  <=>  -c0 > -n s0
+            // (trimming pays only where hulls are large -- the int64 instantiation's accumulated
+            // rows; on W5's int32 rows it costs 1.5% net)
+            if constexpr (std::is_same<VT, long long>::value)
+              skip[k] = c0 < nV * (VT)s0;   // (the deque is never empty: the dummy line)
+            else
+              skip[k] = false;
+            const int sz = skip[k] ? 0 : b[k] - f[k];   // deque size - 1, before the push
+            const int p1 = (sz >= 1) & pop_test(s1, c1, s0, c0);
+            const int p2 = p1 & (sz >= 2) & pop_test(s2, c2, s1, c1);
+            // two pops decided eagerly; a lane with two pops may pop more: the warp-uniform loop
+            // below tests further lines (W5 34.3 -> 33.1 ms vs four eager tests)
+            top[k] = b[k] - (p1 + p2);   // position of the new second-to-back line
+            more[k] = act[k] & (p2 != 0);
+          }
+          bool anymore = more[0];
+          if constexpr (K == 2) anymore |= more[1];
+  #ifdef SP_HULL_BRSTATS   // instrumentation (tools/prof_dp.py, SP_BRSTATS_REPORT): rows, loops taken
+          if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(p.ws + 64), 1ull);
+          if (__any_sync(FULL, anymore) && lane == 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(p.ws + 72), 1ull);
+  #endif
+          if (__any_sync(FULL, anymore)) {   // a lane popped two lines: keep testing from the ring
+  #pragma unroll
+            for (int k = 0; k < K; ++k) {
+              if (!more[k]) continue;
+              int cs = L2[k].s - j;
+              VT cb = L2[k].b - bj[k];
+              while (top[k] - f[k] >= 1) {
+                const Line<VT> l1 = rg.ldh(k, top[k] - 1, hi[k]);
+                const int ls = l1.s - j;
+                const VT lb = l1.b - bj[k];
+                if (pop_test(ls, lb, cs, cb)) {
+                  --top[k];
+                  cs = ls;
+                  cb = lb;
+                } else {
+                  break;
+                }
+              }
+            }
+          }
+          VT v0[K], v1[K], v2[K];
+          bool q2[K];
+  #pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int nb = skip[k] ? b[k] : top[k] + 1;
+            const Line<VT> nl{bj[k], j};
+            if (!skip[k]) {
+              if (win) rg.sth(k, nb, nl, hi[k], f[k]);
+              else rg.stw(k, nb, nl);
+              hi[k] = max(hi[k], nb);
+            }
+            const int d = nb - f[k];
+            const bool fresh = !skip[k];
+            const Line<VT> F1 = (fresh & (d == 1)) ? nl : G1[k];   // lines f+1 / f+2 popped or new
+            const Line<VT> F2 = (fresh & (d == 2)) ? nl : G2[k];
+            B0[k] = skip[k] ? B0[k] : nl;
+            b[k] = nb;
+            ovf |= act[k] & (d >= rg.span_cap(k));
+            // ---- query x = P_j: up to one front pop decided from the loaded lines -------------
+            v0[k] = F0[k].b + (VT)F0[k].s * nPj;
+            v1[k] = F1.b + (VT)F1.s * nPj;
+            v2[k] = F2.b + (VT)F2.s * nPj;
+            const bool q1 = act[k] & (d >= 1) & (v1[k] < v0[k]);
+            q2[k] = q1 & (d >= 2) & (v2[k] < v1[k]);
+            const bool one = q1 & !q2[k];
+            f[k] += one;
+            F0[k] = one ? F1 : (q2[k] ? F2 : F0[k]);
+            v0[k] = one ? v1[k] : (q2[k] ? v2[k] : v0[k]);
+          }
+          bool anyq2 = q2[0];
+          if constexpr (K == 2) anyq2 |= q2[1];
+  #ifdef SP_HULL_BRSTATS
+          if (__any_sync(FULL, anyq2) && lane == 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(p.ws + 80), 1ull);
+  #endif
+          if (__any_sync(FULL, anyq2)) {   // rare: the front moves by two or more
+  #pragma unroll
+            for (int k = 0; k < K; ++k) {
+              if (!q2[k]) continue;
+              f[k] += 2;   // F0 = line f+2 already
+              while (f[k] < b[k]) {
+                const Line<VT> l1 = rg.ldh(k, f[k] + 1, hi[k]);
+                const VT vl = l1.b + (VT)l1.s * nPj;
+                if (vl < v0[k]) {
+                  ++f[k];
+                  F0[k] = l1;
+                  v0[k] = vl;
+                } else {
+                  break;
+                }
+              }
+            }
+          }
+          Pm1 = Pj;
+          // ---- row value, argmin change log ---------------------------------------------------
+  #pragma unroll
+          for (int k = 0; k < K; ++k) {
+            eo[k] = v0[k];
+            const int nop = F0[k].s;
+            if (act[k] & (nop != op[k])) {
+              lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop;   // < LC: checked per chunk
+              ++cnt[k];
+            }
+            op[k] = nop;
+          }
+          if (chain_out && lane == 31) {
+            if (ss) ss->ring[(evbase + q) & (SPLIT_RING - 1)] = (int)eo[K - 1];
+            else eout_buf[evbase + q] = eo[K - 1];
+          }
+        }
+        if (ss) {   // publish this chunk (producer) / release its ring slots (consumer)
+          __syncwarp();
+          __threadfence_block();
+          if (lane == 0) {
+            if (chain_out) *ss->produced = evbase + nev;
+            else *ss->consumed = evbase + nev - 1;
+          }
+        }
+        evbase += nev;
+        bool full = false;
+  #pragma unroll
+        for (int k = 0; k < K; ++k) full |= (LC <= N) & (cnt[k] > LC - 33);   // 32 rows of headroom
+        logfull = __any_sync(FULL, full);
+        if (__any_sync(FULL, ovf) || logfull) {
           ovf = true;
+          if (ss && lane == 0) *ss->abort_ = 1;
           break;
         }
-        __threadfence_block();
-        if (chain_in && lane < nev)
-          Ec = evbase + lane >= 1 ? (VT)ss->ring[(evbase + lane - 1) & (SPLIT_RING - 1)] : (VT)0;
-      } else if (chain_in && lane < nev) {
-        Ec = evbase + lane >= 1 ? ein[evbase + lane - 1] : 0;
       }
-      for (int q = 0; evmask; ++q) {
-        const int i = __ffs(evmask) - 1;
-        evmask &= evmask - 1;
-        const int j = jb + 1 + i;
-        // ring lines around both ends (positions fixed by the previous row).  Windowed rings:
-        // while every lane's deque lies within C - 2 positions of its high-water mark (the
-        // common case) every line it touches this row is in the shared window -- plain shared
-        // loads and stores; otherwise (warp-uniform) the checked window / global accesses.
-        bool wbig = false;
-        if constexpr (RING::kWindowed) {
-#pragma unroll
-          for (int k = 0; k < K; ++k) wbig |= act[k] & (hi[k] - f[k] >= RING::window(k) - 2);
-        }
-        const bool win = RING::kWindowed && __any_sync(FULL, wbig);
-        Line<VT> L1[K], L2[K], G1[K], G2[K];
-        if (win) {
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            L1[k] = rg.ldh(k, b[k] - 1, hi[k]);
-            L2[k] = rg.ldh(k, b[k] - 2, hi[k]);
-            G1[k] = rg.ldh(k, f[k] + 1, hi[k]);
-            G2[k] = rg.ldh(k, f[k] + 2, hi[k]);
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            L1[k] = rg.ldw(k, b[k] - 1);
-            L2[k] = rg.ldw(k, b[k] - 2);
-            G1[k] = rg.ldw(k, f[k] + 1);
-            G2[k] = rg.ldw(k, f[k] + 2);
-          }
-        }
-        // e_{m-1}(j-1): from the lane below (its value at the previous support row);
-        // lane 0 slot 0 from the previous pass (or e_0 = 0)
-        VT in[K];
-        const VT t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
-        // unconditional (Ec = 0 without a previous pass): the row's shuffles stay in one
-        // converged region, so ptxas emits one divergence check (BRA.DIV) for all of them
-        const VT ext = __shfl_sync(FULL, Ec, q);
-        in[0] = lane ? t0 : ext;
-        if constexpr (K == 2) {
-          const VT t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);
-          in[1] = lane ? t1 : t0;
-        }
-        const VT Pj = __shfl_sync(FULL, Pc, i);
-        const VT nPj = -Pj;
-        ++ev_e;
-        // ---- push line j: up to two back pops decided from the loaded lines ----------------
-        VT bj[K];
-        int top[K];
-        bool more[K], skip[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          bj[k] = in[k] + (VT)j * Pm1;
-          // deltas of the back lines from the new point (j, bj)
-          const int s0 = B0[k].s - j, s1 = L1[k].s - j, s2 = L2[k].s - j;
-          const VT c0 = B0[k].b - bj[k], c1 = L1[k].b - bj[k], c2 = L2[k].b - bj[k];
-          // a line that overtakes the back line only beyond x = P_N = n is never optimal at a
-          // query (x <= n): it is neither pushed nor allowed to pop.
-          // x(back, new) > n  <=>  bj - B0.b > n (j - B0.s)  <=>  -c0 > -n s0
-          // (trimming pays only where hulls are large -- the int64 instantiation's accumulated
-          // rows; on W5's int32 rows it costs 1.5% net)
-          if constexpr (std::is_same<VT, long long>::value)
-            skip[k] = c0 < nV * (VT)s0;   // (the deque is never empty: the dummy line)
-          else
-            skip[k] = false;
-          const int sz = skip[k] ? 0 : b[k] - f[k];   // deque size - 1, before the push
-          const int p1 = (sz >= 1) & pop_test(s1, c1, s0, c0);
-          const int p2 = p1 & (sz >= 2) & pop_test(s2, c2, s1, c1);
-          // two pops decided eagerly; a lane with two pops may pop more: the warp-uniform loop
-          // below tests further lines (W5 34.3 -> 33.1 ms vs four eager tests)
-          top[k] = b[k] - (p1 + p2);   // position of the new second-to-back line
-          more[k] = act[k] & (p2 != 0);
-        }
-        bool anymore = more[0];
-        if constexpr (K == 2) anymore |= more[1];
-#ifdef SP_HULL_BRSTATS   // instrumentation (tools/prof_dp.py, SP_BRSTATS_REPORT): rows, loops taken
-        if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(p.ws + 64), 1ull);
-        if (__any_sync(FULL, anymore) && lane == 0)
-          atomicAdd(reinterpret_cast<unsigned long long*>(p.ws + 72), 1ull);
-#endif
-        if (__any_sync(FULL, anymore)) {   // a lane popped two lines: keep testing from the ring
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            if (!more[k]) continue;
-            int cs = L2[k].s - j;
-            VT cb = L2[k].b - bj[k];
-            while (top[k] - f[k] >= 1) {
-              const Line<VT> l1 = rg.ldh(k, top[k] - 1, hi[k]);
-              const int ls = l1.s - j;
-              const VT lb = l1.b - bj[k];
-              if (pop_test(ls, lb, cs, cb)) {
-                --top[k];
-                cs = ls;
-                cb = lb;
-              } else {
-                break;
-              }
-            }
-          }
-        }
-        VT v0[K], v1[K], v2[K];
-        bool q2[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int nb = skip[k] ? b[k] : top[k] + 1;
-          const Line<VT> nl{bj[k], j};
-          if (!skip[k]) {
-            if (win) rg.sth(k, nb, nl, hi[k], f[k]);
-            else rg.stw(k, nb, nl);
-            hi[k] = max(hi[k], nb);
-          }
-          const int d = nb - f[k];
-          const bool fresh = !skip[k];
-          const Line<VT> F1 = (fresh & (d == 1)) ? nl : G1[k];   // lines f+1 / f+2 popped or new
-          const Line<VT> F2 = (fresh & (d == 2)) ? nl : G2[k];
-          B0[k] = skip[k] ? B0[k] : nl;
-          b[k] = nb;
-          ovf |= act[k] & (d >= rg.span_cap(k));
-          // ---- query x = P_j: up to one front pop decided from the loaded lines -------------
-          v0[k] = F0[k].b + (VT)F0[k].s * nPj;
-          v1[k] = F1.b + (VT)F1.s * nPj;
-          v2[k] = F2.b + (VT)F2.s * nPj;
-          const bool q1 = act[k] & (d >= 1) & (v1[k] < v0[k]);
-          q2[k] = q1 & (d >= 2) & (v2[k] < v1[k]);
-          const bool one = q1 & !q2[k];
-          f[k] += one;
-          F0[k] = one ? F1 : (q2[k] ? F2 : F0[k]);
-          v0[k] = one ? v1[k] : (q2[k] ? v2[k] : v0[k]);
-        }
-        bool anyq2 = q2[0];
-        if constexpr (K == 2) anyq2 |= q2[1];
-#ifdef SP_HULL_BRSTATS
-        if (__any_sync(FULL, anyq2) && lane == 0)
-          atomicAdd(reinterpret_cast<unsigned long long*>(p.ws + 80), 1ull);
-#endif
-        if (__any_sync(FULL, anyq2)) {   // rare: the front moves by two or more
-#pragma unroll
-          for (int k = 0; k < K; ++k) {
-            if (!q2[k]) continue;
-            f[k] += 2;   // F0 = line f+2 already
-            while (f[k] < b[k]) {
-              const Line<VT> l1 = rg.ldh(k, f[k] + 1, hi[k]);
-              const VT vl = l1.b + (VT)l1.s * nPj;
-              if (vl < v0[k]) {
-                ++f[k];
-                F0[k] = l1;
-                v0[k] = vl;
-              } else {
-                break;
-              }
-            }
-          }
-        }
-        Pm1 = Pj;
-        // ---- row value, argmin change log ---------------------------------------------------
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          eo[k] = v0[k];
-          const int nop = F0[k].s;
-          if (act[k] & (nop != op[k])) {
-            lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop;   // < LC: checked per chunk
-            ++cnt[k];
-          }
-          op[k] = nop;
-        }
-        if (chain_out && lane == 31) {
-          if (ss) ss->ring[(evbase + q) & (SPLIT_RING - 1)] = (int)eo[K - 1];
-          else eout_buf[evbase + q] = eo[K - 1];
-        }
-      }
-      if (ss) {   // publish this chunk (producer) / release its ring slots (consumer)
-        __syncwarp();
-        __threadfence_block();
-        if (lane == 0) {
-          if (chain_out) *ss->produced = evbase + nev;
-          else *ss->consumed = evbase + nev - 1;
-        }
-      }
-      evbase += nev;
-      bool full = false;
-#pragma unroll
-      for (int k = 0; k < K; ++k) full |= (LC <= N) & (cnt[k] > LC - 33);   // 32 rows of headroom
-      logfull = __any_sync(FULL, full);
-      if (__any_sync(FULL, ovf) || logfull) {
-        ovf = true;
-        if (ss && lane == 0) *ss->abort_ = 1;
-        break;
-      }
+      stop = ovf;   // (uniform: both breaks set ovf for the whole warp)
     }
     if (!ovf) {
 #pragma unroll
@@ -812,13 +838,20 @@ __device__ __forceinline__ void hull_cbb_f64(const HullParams& p, int e, int tfi
 
 // VT = int: every entry first; those beyond the int32 guard but within the int64 one are listed
 // for the VT = long long instantiation (launched next, same slots); the rest for the D&C kernel.
+#ifndef SP_HULL_MINB
+#define SP_HULL_MINB 1
+#endif
+// one layer per lane (M <= 32, K = 1) on int32 rows: cap the registers at 128 so that 16 warps
+// fit an SM (the ring allows 18); the other instantiations are shared-memory bound
 template <typename WT, int K, typename VT>
-__global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
+__global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL_MINB)
+    dp_hull_kernel(HullParams p) {
   constexpr bool F64 = std::is_same<VT, double>::value;
   constexpr bool WIDE = std::is_same<VT, long long>::value;
   const int lane = threadIdx.x;
-  extern __shared__ __align__(16) uint8_t sring[];   // ring_bytes<K, VT>()
+  extern __shared__ __align__(16) uint8_t sring[];   // ring_bytes<K, VT>() | row stage
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
+  VT* stage = reinterpret_cast<VT*>(sring + ring_bytes<K, VT>());
   using SR = typename std::conditional<std::is_same<VT, int>::value,
                                        WRing<int, SRingI<HC0, HC1>>,
                                        WRing<VT, SRingW<VT, WC, WC>>>::type;
@@ -937,21 +970,26 @@ __global__ void __launch_bounds__(32, 1) dp_hull_kernel(HullParams p) {
       // int32: plain shared rings first (W5: 16 of 16384 entries outgrow them); an entry whose
       // hull outgrows a ring is re-run at once with the windowed ring (the same window plus
       // global arrays of WSMALL lines)
-      ovf = fullm ? hull_dp<WT, VT, K, true>(p, we, e, TN, nV, srg.sm, logs, logn, ebuf0, ebuf1,
-                                             pops_e, ev_e, logfull)
-                  : hull_dp<WT, VT, K, false>(p, we, e, TN, nV, srg.sm, logs, logn, ebuf0, ebuf1,
-                                              pops_e, ev_e, logfull);
+#ifdef SP_HULL_WIN_FIRST
+      auto& rg1 = srg;
+#else
+      auto& rg1 = srg.sm;
+#endif
+      ovf = fullm ? hull_dp<WT, VT, K, true>(p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1,
+                                             pops_e, ev_e, logfull, stage)
+                  : hull_dp<WT, VT, K, false>(p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1,
+                                              pops_e, ev_e, logfull, stage);
       if (ovf && !logfull) {
         pops_e = ev_e = 0;
         __syncwarp();
         ovf = hull_dp<WT, VT, K, false>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1, pops_e,
-                                        ev_e, logfull);
+                                        ev_e, logfull, stage);
       }
     } else {
       ovf = fullm ? hull_dp<WT, VT, K, true>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1,
-                                             pops_e, ev_e, logfull)
+                                             pops_e, ev_e, logfull, stage)
                   : hull_dp<WT, VT, K, false>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1,
-                                              pops_e, ev_e, logfull);
+                                              pops_e, ev_e, logfull, stage);
     }
     pops += pops_e;
     events += ev_e;
@@ -1376,6 +1414,7 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
   srg.b0 = sbase + 4u * (uint32_t)lane;
   srg.ds = 128u - 2u * (uint32_t)lane;
   int* ring = reinterpret_cast<int*>(sring + 2 * RB);
+  int* stage = reinterpret_cast<int*>(sring + 2 * RB + SPLIT_RING * sizeof(int)) + w * 32 * HULL_PF;
   __shared__ int s_it, s_prod, s_cons, s_abort;
   SplitSync ss{ring, &s_prod, &s_cons, &s_abort};
   const int N = p.N, M = p.M;
@@ -1416,10 +1455,10 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
     bool logfull = false;
     if (fullm)
       hull_dp<WT, int, 1, true>(p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0, pops_e,
-                                ev_e, logfull, &ss, w);
+                                ev_e, logfull, stage, &ss, w);
     else
       hull_dp<WT, int, 1, false>(p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0,
-                                 pops_e, ev_e, logfull, &ss, w);
+                                 pops_e, ev_e, logfull, stage, &ss, w);
     __syncthreads();
     if (s_abort) {   // ring or log full in either warp: the int64 instantiation re-runs it
       if (threadIdx.x == 0) p.wide[atomicAdd(wide_n, 1u)] = e;
@@ -1576,11 +1615,7 @@ __global__ void __launch_bounds__(256) row_stats_kernel(const WT* __restrict__ w
   }
 }
 
-template <int K, typename VT>
-static constexpr size_t ring_bytes() {
-  if constexpr (sizeof(VT) == 8) return (size_t)(WC + (K == 2 ? WC : 0)) * 384;
-  return (size_t)(HC0 + (K == 2 ? HC1 : 0)) * 192;
-}
+
 
 // Host-side launch facts cached per device (the verdict's host-overhead item: no attribute,
 // occupancy or getenv calls on every sp_place_checkpoints call once warm).
@@ -1621,11 +1656,13 @@ static int clamp_grid(long g, int E) {
 template <typename WT, int K, typename VT>
 static int hull_grid_t(int E) {
   static int cache[HULL_MAX_DEV] = {0};
-  const int occ = occ_cached(dp_hull_kernel<WT, K, VT>, ring_bytes<K, VT>(), cache);
+  const int occ = occ_cached(dp_hull_kernel<WT, K, VT>, hull_dyn_bytes<K, VT>(), cache);
   return clamp_grid((long)dev_sms() * occ, E);
 }
 
-constexpr size_t split_smem_bytes() { return 2 * (size_t)HC0 * 192 + SPLIT_RING * sizeof(int); }
+constexpr size_t split_smem_bytes() {
+  return 2 * (size_t)HC0 * 192 + SPLIT_RING * sizeof(int) + 2 * stage_bytes<int>();
+}
 
 template <typename WT>
 static int split_grid_t(int E) {
@@ -1670,7 +1707,7 @@ template <typename WT, int K>
 static void hull_launch_t(HullParams p, const HullRowStat* rstat, int gn, cudaStream_t st) {
   if constexpr (std::is_same<WT, double>::value) {
     p.wgb = wring_pass_bytes_t<double>(p.N, p.M);
-    dp_hull_kernel<double, K, double><<<gn, 32, ring_bytes<K, double>(), st>>>(p);
+    dp_hull_kernel<double, K, double><<<gn, 32, hull_dyn_bytes<K, double>(), st>>>(p);
   } else {
     p.wgb = wring_pass_bytes_t<int>(p.N, p.M);
     if (K == 2 && !hull_lean() && p.rstat &&
@@ -1678,7 +1715,7 @@ static void hull_launch_t(HullParams p, const HullRowStat* rstat, int gn, cudaSt
       const int gs = std::min(gn, split_grid_t<WT>(p.E));
       dp_hull_split_kernel<WT><<<gs, 64, split_smem_bytes(), st>>>(p);
     } else if (!hull_lean()) {
-      dp_hull_kernel<WT, K, int><<<gn, 32, ring_bytes<K, int>(), st>>>(p);
+      dp_hull_kernel<WT, K, int><<<gn, 32, hull_dyn_bytes<K, int>(), st>>>(p);
     } else {
       const int gl = std::min(gn, lean_grid_t<WT, K>(p.E));
       dp_lean_kernel<WT, K><<<gl, 32, lean_smem_bytes<K>(), st>>>(p, rstat);
@@ -1687,7 +1724,7 @@ static void hull_launch_t(HullParams p, const HullRowStat* rstat, int gn, cudaSt
     // empty); its grid is clamped to the slots allocated for the widest launch
     const int gw = std::min(gn, hull_grid_t<WT, K, long long>(p.E));
     p.wgb = wring_pass_bytes_t<long long>(p.N, p.M);
-    dp_hull_kernel<WT, K, long long><<<gw, 32, ring_bytes<K, long long>(), st>>>(p);
+    dp_hull_kernel<WT, K, long long><<<gw, 32, hull_dyn_bytes<K, long long>(), st>>>(p);
   }
 }
 

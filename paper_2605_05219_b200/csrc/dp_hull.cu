@@ -1793,7 +1793,14 @@ cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, 
   const size_t tb = order_cub_bytes(E);
   sp::HullRowStat* rstat =
       reinterpret_cast<sp::HullRowStat*>(order_ws + 4 * a + sp::hull_align(tb));
-  const bool order = E > 1 && !no_order;
+  // the largest-first order matters only when warps take several entries each: with no more
+  // entries than resident warps of the one-warp kernel every entry starts in the first wave
+  const bool k2o = sp::hull_K(M) == 2;
+  const long first_wave =
+      wtype == SP_W_PROB_F64
+          ? (k2o ? sp::hull_grid_t<double, 2, double>(1 << 30) : sp::hull_grid_t<double, 1, double>(1 << 30))
+          : (k2o ? sp::hull_grid_t<int32_t, 2, int>(1 << 30) : sp::hull_grid_t<int32_t, 1, int>(1 << 30));
+  const bool order = E > 1 && E > first_wave && !no_order;
   int blocks = (E + 7) / 8;
   if (blocks > sp::dev_sms() * 8) blocks = sp::dev_sms() * 8;
   if (wtype == SP_W_PROB_F64) {

@@ -183,6 +183,64 @@ __device__ __forceinline__ int log_lookup_warp(const uint32_t* lg, int cnt, int 
   }
   return (int)(__ldcg(lg + lo) & 0xffffu);
 }
+// Small argmin logs (sparse rows: W2 / W3 hold ~20-50 entries per layer) are copied into the
+// free ring memory after the DP, so the backtrack's M dependent lookups hit shared memory instead
+// of L2.  Layout: offsets int32 [M+1] | entries uint32.  Returns false (nothing copied) when they
+// do not fit `cap_words`.  Layer m's log is slot m - 1 (hull_layer_slot).
+__device__ __forceinline__ bool logs_to_smem(const uint32_t* logs, const int32_t* logn, int M,
+                                             int LCstride, uint32_t* sm, int cap_words) {
+  const int lane = lane_id();
+  int base = 0;
+  bool fits = true;
+  for (int m0 = 0; m0 < M && fits; m0 += 32) {   // exclusive offsets in layer order
+    const int m = m0 + lane;
+    const int c = m < M ? logn[m] : 0;
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int tot = __shfl_sync(FULL, inc, 31);
+    fits = base + tot + M + 1 <= cap_words;
+    if (fits && m < M) sm[m] = (uint32_t)(base + inc - c);
+    base += tot;
+  }
+  if (!fits) return false;
+  if (lane == 0) sm[M] = (uint32_t)base;
+  __syncwarp();
+  uint32_t* ent = sm + M + 1;
+  for (int m = lane; m < M; m += 32) {   // one lane per layer: independent loads in flight
+    const uint32_t* lg = logs + (size_t)m * LCstride;
+    const int o = (int)sm[m], c = (int)sm[m + 1] - o;
+    for (int q = 0; q < c; ++q) ent[o + q] = __ldcg(lg + q);
+  }
+  __syncwarp();
+  return true;
+}
+// opt_m(j) from layer m's log in shared memory (copied by logs_to_smem): warp-cooperative
+__device__ __forceinline__ int log_lookup_smem(const uint32_t* sm, int M, int m, int j) {
+  const int lane = lane_id();
+  const uint32_t* lg = sm + M + 1 + sm[m - 1];
+  const int cnt = (int)(sm[m] - sm[m - 1]);
+  int lo = 0, hi = cnt - 1;
+  while (hi > lo) {
+    const int span = hi - lo;
+    const int pr = lo + (int)(((long long)span * (lane + 1) + 31) >> 5);
+    const bool ok = (int)(lg[pr] >> 16) <= j;
+    const unsigned bal = __ballot_sync(FULL, ok);
+    if (bal == 0) {
+      hi = __shfl_sync(FULL, pr, 0) - 1;
+    } else {
+      const int i = 31 - __clz(bal);
+      const int plo = __shfl_sync(FULL, pr, i);
+      const int pnx = __shfl_sync(FULL, pr, (i + 1) & 31);
+      lo = plo;
+      if (i < 31) hi = pnx - 1;
+    }
+  }
+  return (int)(lg[lo] & 0xffffu);
+}
 // single-thread version (one lane per budget in the frontier backtrack)
 __device__ __forceinline__ int log_lookup_lane(const uint32_t* lg, int cnt, int j) {
   int lo = 0, hi = cnt - 1;   // last index with row <= j
@@ -1045,10 +1103,14 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
     // ---- a5: rule-B backtrack (reading R3): the warp for budget M, lanes for the frontier --
     {
       int32_t* out = p.pos + (int64_t)e * M;
+      uint32_t* slog = reinterpret_cast<uint32_t*>(sring);   // the rings are free now
+      const bool in_smem = logs_to_smem(logs, logn, M, hull_log_cap(N), slog,
+                                        (int)(ring_bytes<K, VT>() / 4));
       int k = 0, j = N, m = M;
       while (m > 0 && j >= tfirst) {   // P_j > 0  <=>  j >= first non-zero bin
         const int ls = hull_layer_slot(K, m);
-        const int s = log_lookup_warp(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
+        const int s = in_smem ? log_lookup_smem(slog, M, m, j)
+                              : log_lookup_warp(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
         if (lane == 0) out[k] = s;
         ++k;
         j = s - 1;
@@ -1388,14 +1450,17 @@ __device__ __forceinline__ bool lean_dp(const HullParams& p, const WT* __restric
 // per budget for the f3 frontier.  Shared by dp_hull_kernel and dp_lean_kernel.
 template <int K>
 __device__ __forceinline__ void hull_backtrack(const HullParams& p, int e, int tfirst,
-                                               const uint32_t* logs, const int32_t* logn) {
+                                               const uint32_t* logs, const int32_t* logn,
+                                               uint32_t* slog = nullptr, int slog_words = 0) {
   const int lane = lane_id();
   const int N = p.N, M = p.M;
   int32_t* out = p.pos + (int64_t)e * M;
+  const bool in_smem = slog && logs_to_smem(logs, logn, M, hull_log_cap(N), slog, slog_words);
   int k = 0, j = N, m = M;
   while (m > 0 && j >= tfirst) {   // P_j > 0  <=>  j >= first non-zero bin
     const int ls = hull_layer_slot(K, m);
-    const int s = log_lookup_warp(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
+    const int s = in_smem ? log_lookup_smem(slog, M, m, j)
+                          : log_lookup_warp(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
     if (lane == 0) out[k] = s;
     ++k;
     j = s - 1;
@@ -1508,7 +1573,8 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
     events += w == 0 ? ev_e : 0;
     if (w == 0) {
       __threadfence_block();
-      hull_backtrack<1>(p, e, rs.tfirst, logs, logn);
+      hull_backtrack<1>(p, e, rs.tfirst, logs, logn, reinterpret_cast<uint32_t*>(sring),
+                        (int)(2 * RB / 4));   // both warps' rings are free now
       ++done_entries;
     }
   }
@@ -1614,6 +1680,7 @@ __global__ void __launch_bounds__(32, 1) dp_lean_kernel(HullParams p, const Hull
 // One pass over every row (one warp per row): the support count (the largest-first order's key),
 // and for integer weights n = P_N, T_N, the first non-zero bin and the guards that dp_lean_kernel
 // needs before it starts (so the DP itself reads each row once).
+constexpr int RS_U = 32;   // row pre-pass: 32-bin chunks in flight per lane (4 KB per warp)
 template <typename WT>
 __global__ void __launch_bounds__(256) row_stats_kernel(const WT* __restrict__ w, int E, int N,
                                                         int32_t* __restrict__ key,
@@ -1628,17 +1695,17 @@ __global__ void __launch_bounds__(256) row_stats_kernel(const WT* __restrict__ w
     int c = 0, bad = 0, tfirst = INT_MAX;
     long long n = 0, tn = 0;
     int2* sp_e = sparse ? sparse + (size_t)e * HULL_KC : nullptr;
-    // 16 chunks of 32 bins in flight per lane (all loads issued before any is used), then the
+    // RS_U chunks of 32 bins in flight per lane (all loads issued before any is used), then the
     // chunks in order: sums, guards, and the support rows compacted while they fit HULL_KC
-    for (int base = 0; base < N; base += 32 * 16) {   // (warp-uniform trip count: ballots)
-      WT v[16];
+    for (int base = 0; base < N; base += 32 * RS_U) {   // (warp-uniform trip count: ballots)
+      WT v[RS_U];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < RS_U; ++u) {
         const int t = base + 32 * u + 1 + lane;
         v[u] = t <= N ? __ldcs(we + t) : WT(0);
       }
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < RS_U; ++u) {
         const int t = base + 32 * u + 1 + lane;
         const unsigned nz = __ballot_sync(FULL, v[u] != WT(0));
         if constexpr (!std::is_same<WT, double>::value) {

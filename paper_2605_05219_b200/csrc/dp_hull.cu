@@ -856,6 +856,244 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
   return ovf;
 }
 
+// The skewed step (int32, K = 2, one pass, dense rows; compiled in with -DSP_HULL_SKEW; measured
+// slower than hull_dp on W5, 49.3 vs 29.6 ms): slot k of lane l runs layer 32k + l + 1 on support row t - l - 32k at step t, so the
+// e_{m-1}(j-1) it needs from the lane below is two steps old and the shuffle that brings it (and
+// the lane below's front work) leave the row's critical path; row data (j, P_j) move one lane up
+// per step (a systolic shift), lane 0 taking the next support row.  The CHT step itself is the
+// one of hull_dp.  The pipeline fills and drains over 63 extra steps per entry.
+template <typename WT, bool ALLACT, class RING>
+__device__ __forceinline__ bool hull_dp_skew(const HullParams& p, const WT* __restrict__ we, int e,
+                                             long long TN, RING rg, uint32_t* logs, int32_t* logn,
+                                             unsigned& pops_e, unsigned& ev_e, bool& logfull) {
+  constexpr int K = 2;
+  using VT = int;
+  const int lane = lane_id();
+  const int N = p.N, M = p.M;
+  const int LC = p.logcap;
+  logfull = false;
+  bool ovf = false;
+  int f[K], b[K], op[K], cnt[K];
+  VT eo[K];
+  Line<VT> B0[K], F0[K];
+  bool act[K];
+  uint32_t* lg[K];
+  int rj[K], rP[K], pm[K];   // this step's row (j = 0: none) and P_j, and P_{j-1}
+  VT q0[K], q1[K];           // e_{m-1} from the lane below, one and two steps old
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int mk = 32 * k + lane + 1;
+    act[k] = ALLACT || mk <= M;
+    f[k] = 0;
+    b[k] = 0;
+    eo[k] = 0;   // e_m(0) = 0 (reading R1)
+    op[k] = 1;
+    cnt[k] = 1;
+    lg[k] = logs + (size_t)(32 * k + lane) * LC;
+    if (act[k]) lg[k][0] = (1u << 16) | 1u;
+    B0[k] = F0[k] = Line<VT>{hull_inf<VT>(), 0};
+    rg.st(k, 0, F0[k]);
+    rj[k] = rP[k] = pm[k] = 0;
+    q0[k] = q1[k] = 0;
+  }
+  // the row source: 32-row chunks, HULL_PF in flight
+  VT cq[HULL_PF];
+#pragma unroll
+  for (int c = 0; c < HULL_PF; ++c)
+    cq[c] = 32 * c + 1 + lane <= N ? (VT)we[32 * c + 1 + lane] : (VT)0;
+  int jn = 0;              // next chunk base
+  int jbc = 0;             // current chunk base
+  unsigned evmask = 0;     // support rows of the current chunk not yet supplied
+  VT Pc = 0, carry = 0;
+  int supplied = 0, drain = 0;
+  for (int t = 0; drain < 64; ++t) {
+    // ---- supply: the next support row for lane 0, slot 0 -------------------------------------
+    while (evmask == 0 && jn < N) {   // (warp-uniform)
+      const VT craw = cq[0];
+#pragma unroll
+      for (int c = 0; c + 1 < HULL_PF; ++c) cq[c] = cq[c + 1];
+      const int jr = jn + 1 + lane;
+      cq[HULL_PF - 1] = jr + 32 * HULL_PF <= N ? (VT)we[jr + 32 * HULL_PF] : (VT)0;
+      evmask = __ballot_sync(FULL, craw > 0);
+      VT c32 = craw;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const VT y = __shfl_up_sync(FULL, c32, o);
+        if (lane >= o) c32 += y;
+      }
+      Pc = carry + c32;
+      carry = __shfl_sync(FULL, Pc, 31);
+      jbc = jn;
+      jn += 32;
+    }
+    int nj = 0, nP = 0;
+    if (evmask) {
+      const int i = __ffs(evmask) - 1;
+      evmask &= evmask - 1;
+      nj = jbc + 1 + i;
+      nP = __shfl_sync(FULL, Pc, i);
+      ++supplied;
+    } else {
+      ++drain;   // no more rows: 63 more steps carry the last one through every slot
+    }
+    // ---- the systolic shift of the rows --------------------------------------------------
+    {
+      const int src = (lane + 31) & 31;
+      const int sj0 = __shfl_sync(FULL, rj[0], src), sP0 = __shfl_sync(FULL, rP[0], src);
+      const int sj1 = __shfl_sync(FULL, rj[1], src), sP1 = __shfl_sync(FULL, rP[1], src);
+#pragma unroll
+      for (int k = 0; k < K; ++k) pm[k] = rj[k] ? rP[k] : pm[k];   // P_{j-1}: the last row's P
+      rj[1] = lane ? sj1 : sj0;
+      rP[1] = lane ? sP1 : sP0;
+      rj[0] = lane ? sj0 : nj;
+      rP[0] = lane ? sP0 : nP;
+    }
+    // ---- the CHT step of every (valid) slot ----------------------------------------------
+    bool val[K];
+    VT in[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      val[k] = act[k] & (rj[k] > 0);
+      in[k] = q1[k];
+    }
+    Line<VT> L1[K], L2[K], G1[K], G2[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      L1[k] = rg.ld(k, b[k] - 1);
+      L2[k] = rg.ld(k, b[k] - 2);
+      G1[k] = rg.ld(k, f[k] + 1);
+      G2[k] = rg.ld(k, f[k] + 2);
+    }
+    VT bj[K];
+    int top[K];
+    bool more[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int j = rj[k];
+      bj[k] = in[k] + (VT)j * pm[k];
+      const int s0 = B0[k].s - j, s1 = L1[k].s - j, s2 = L2[k].s - j;
+      const VT c0 = B0[k].b - bj[k], c1 = L1[k].b - bj[k], c2 = L2[k].b - bj[k];
+      const int sz = val[k] ? b[k] - f[k] : 0;
+      const int p1 = (sz >= 1) & pop_test(s1, c1, s0, c0);
+      const int p2 = p1 & (sz >= 2) & pop_test(s2, c2, s1, c1);
+      top[k] = b[k] - (p1 + p2);
+      more[k] = val[k] & (p2 != 0);
+    }
+    bool anymore = more[0] | more[1];
+    if (__any_sync(FULL, anymore)) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (!more[k]) continue;
+        const int j = rj[k];
+        int cs = L2[k].s - j;
+        VT cb = L2[k].b - bj[k];
+        while (top[k] - f[k] >= 1) {
+          const Line<VT> l1 = rg.ld(k, top[k] - 1);
+          const int ls = l1.s - j;
+          const VT lb = l1.b - bj[k];
+          if (pop_test(ls, lb, cs, cb)) {
+            --top[k];
+            cs = ls;
+            cb = lb;
+          } else {
+            break;
+          }
+        }
+      }
+    }
+    VT v0[K];
+    bool q2[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int j = rj[k];
+      const VT nPj = -rP[k];
+      const int nb = val[k] ? top[k] + 1 : b[k];
+      const Line<VT> nl{bj[k], j};
+      if (val[k]) rg.st(k, nb, nl);
+      const int d = nb - f[k];
+      const Line<VT> F1 = (val[k] & (d == 1)) ? nl : G1[k];
+      const Line<VT> F2 = (val[k] & (d == 2)) ? nl : G2[k];
+      B0[k] = val[k] ? nl : B0[k];
+      b[k] = nb;
+      ovf |= val[k] & (d >= RING::cap(k));
+      v0[k] = F0[k].b + (VT)F0[k].s * nPj;
+      const VT v1 = F1.b + (VT)F1.s * nPj;
+      const VT v2 = F2.b + (VT)F2.s * nPj;
+      const bool q1 = val[k] & (d >= 1) & (v1 < v0[k]);
+      q2[k] = q1 & (d >= 2) & (v2 < v1);
+      const bool one = q1 & !q2[k];
+      f[k] += one;
+      F0[k] = one ? F1 : (q2[k] ? F2 : F0[k]);
+      v0[k] = one ? v1 : (q2[k] ? v2 : v0[k]);
+    }
+    if (__any_sync(FULL, q2[0] | q2[1])) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (!q2[k]) continue;
+        const VT nPj = -rP[k];
+        f[k] += 2;
+        while (f[k] < b[k]) {
+          const Line<VT> l1 = rg.ld(k, f[k] + 1);
+          const VT vl = l1.b + (VT)l1.s * nPj;
+          if (vl < v0[k]) {
+            ++f[k];
+            F0[k] = l1;
+            v0[k] = vl;
+          } else {
+            break;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (val[k]) eo[k] = v0[k];
+      const int nop = F0[k].s;
+      if (val[k] & (nop != op[k])) {
+        lg[k][cnt[k]] = ((uint32_t)rj[k] << 16) | (uint32_t)nop;   // < LC: checked below
+        ++cnt[k];
+      }
+      op[k] = val[k] ? nop : op[k];
+    }
+    // ---- e_{m-1} for the lane above, two steps ahead ---------------------------------------
+    {
+      const int src = (lane + 31) & 31;
+      const VT t0 = __shfl_sync(FULL, eo[0], src);
+      const VT t1 = __shfl_sync(FULL, eo[1], src);
+      q1[0] = q0[0];
+      q1[1] = q0[1];
+      q0[0] = lane ? t0 : 0;    // layer 1: e_0 = 0
+      q0[1] = lane ? t1 : t0;   // layer 33: layer 32 is lane 31's slot 0
+    }
+    if ((t & 31) == 31) {   // ring / log capacity (the log takes <= 1 entry per step)
+      bool full = false;
+#pragma unroll
+      for (int k = 0; k < K; ++k) full |= (LC <= N) & (cnt[k] > LC - 33);
+      logfull = __any_sync(FULL, full);
+      if (__any_sync(FULL, ovf) || logfull) {
+        ovf = true;
+        break;
+      }
+    }
+  }
+  if (__any_sync(FULL, ovf)) ovf = true;
+  ev_e += supplied;
+  if (!ovf) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!act[k]) continue;
+      pops_e += (unsigned)(supplied - b[k]) + (unsigned)(f[k] - 1);
+      const int mk = 32 * k + lane + 1;
+      logn[32 * k + lane] = cnt[k];
+      const long long V = TN + (long long)eo[k];
+      if (p.cbb) reinterpret_cast<long long*>(p.cbb)[(int64_t)e * (M + 1) + mk] = V;
+      if (mk == M) reinterpret_cast<long long*>(p.cost)[e] = V;
+    }
+  }
+  __syncwarp();
+  return ovf;
+}
+
 // dispatch to the compact-list walk (sparse rows) or the row scan (CMP: compile-time)
 template <typename WT, typename VT, int K, bool ALLACT, class RING>
 __device__ __forceinline__ bool hull_dp_any(const HullParams& p, const WT* __restrict__ we, int e,
@@ -1068,6 +1306,13 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
       auto& rg1 = srg;
 #else
       auto& rg1 = srg.sm;
+#endif
+#ifdef SP_HULL_SKEW
+      if (K == 2 && kcomp < 0 && M <= 64)
+        ovf = fullm ? hull_dp_skew<WT, true>(p, we, e, TN, srg.sm, logs, logn, pops_e, ev_e, logfull)
+                    : hull_dp_skew<WT, false>(p, we, e, TN, srg.sm, logs, logn, pops_e, ev_e,
+                                              logfull);
+      else
 #endif
       ovf = fullm ? hull_dp_any<WT, VT, K, true>(p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1,
                                              pops_e, ev_e, logfull, stage, kcomp, klist)

@@ -323,12 +323,14 @@ __global__ void __launch_bounds__(EP_NT)
 #define SP_EVAL_BCAST_NT 1024
 #endif
 #ifndef SP_EVAL_BCAST_U
-#define SP_EVAL_BCAST_U 16
+#define SP_EVAL_BCAST_U 12
 #endif
 constexpr int EB_NT = SP_EVAL_BCAST_NT;
 constexpr int EB_U = SP_EVAL_BCAST_U;
 constexpr int EB_MAXS = 4;
-constexpr size_t EB_SMEM_MAX = 200 * 1024;   // tables: S (N+1) 2 bytes
+static_assert(EB_U >= 1 && EB_U <= 16, "the 32-bit fast path needs EB_U <= 16");
+constexpr int EB_FB = EB_U <= 1 ? 16 : EB_U <= 2 ? 15 : EB_U <= 4 ? 14 : EB_U <= 8 ? 13 : 12;
+constexpr size_t EB_SMEM_MAX = 200 * 1024;   // tables: S (N+1+SL) 2 bytes
 
 __device__ __forceinline__ long long mad_wide(int a, int b, long long c) {   // c + a b, exact
   long long d;
@@ -346,6 +348,8 @@ __global__ void __launch_bounds__(EB_NT, 1)
   constexpr int NW = EB_NT / 32;
   const int lane = lane_id(), wid = warp_id();
   const int rowlen = N + 1;
+  constexpr int SL = 32 * EB_U;
+  const int tstride = rowlen + SL;   // table stride: padded with l = 0 past the row
   // ---- sets: validity and worst case (warp q: set q) ---------------------------------------
   if (wid < S) {
     const int32_t* pc = positions + (int64_t)wid * max_pos;
@@ -374,12 +378,13 @@ __global__ void __launch_bounds__(EB_NT, 1)
     if (!sh_ok[s]) continue;
     const int32_t* pc = positions + (int64_t)s * max_pos;
     const int k = npos[s];
-    uint16_t* lt = ltab + (size_t)s * rowlen;
+    uint16_t* lt = ltab + (size_t)s * tstride;
     for (int i = wid; i <= k; i += NW) {
       const int ci = i == 0 ? 0 : pc[i - 1];
       const int cn = i == k ? N + 1 : pc[i];
       for (int t = ci + lane; t < cn; t += 32) lt[t] = (uint16_t)ci;
     }
+    for (int t = rowlen + (int)threadIdx.x; t < tstride; t += EB_NT) lt[t] = 0;
   }
   __syncthreads();
   // ---- work items: (entry, 32 EB_U-bin slice of its row).  Warp w takes the contiguous item
@@ -390,53 +395,81 @@ __global__ void __launch_bounds__(EB_NT, 1)
   // the entry; the slice-0 item writes the worst case and the flag of a malformed set (which
   // receives no atomics).
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(ltab);
-  const uint32_t sstride = 2u * (uint32_t)rowlen;   // bytes between two sets' tables
-  constexpr int SL = 32 * EB_U;
+  const uint32_t sstride = 2u * (uint32_t)tstride;   // bytes between two sets' tables
   const int nsl = (N + SL) / SL;   // slices per row (N + 1 bins)
   const int64_t items = (int64_t)E * nsl;
   const int64_t gw = (int64_t)blockIdx.x * NW + wid, nwt = (int64_t)gridDim.x * NW;
   const int64_t i0 = items * gw / nwt, i1 = items * (gw + 1) / nwt;
   if (i0 >= i1) return;
   int e = (int)(i0 / nsl), sl = (int)(i0 - (int64_t)e * nsl);
-  int c[EB_U];
-  {
-    const int32_t* we = w + (int64_t)e * rowlen;
+  // one slice of a row into registers: unpredicated unless it is the row's ragged last slice
+  auto load_slice = [&](int ee, int ss, int (&dst)[EB_U]) {
+    const int32_t* we = w + (int64_t)ee * rowlen + ss * SL + lane;
+    if (ss * SL + SL <= rowlen) {
 #pragma unroll
-    for (int u = 0; u < EB_U; ++u) {
-      const int t = sl * SL + 32 * u + lane;
-      c[u] = t <= N ? __ldcs(we + t) : 0;
+      for (int u = 0; u < EB_U; ++u) dst[u] = __ldcs(we + 32 * u);
+    } else {
+      const int lim = rowlen - ss * SL - lane;   // bins of this lane still inside the row: > 32 u
+#pragma unroll
+      for (int u = 0; u < EB_U; ++u) dst[u] = 32 * u < lim ? __ldcs(we + 32 * u) : 0;
     }
-  }
+  };
+  int c[EB_U];
+  load_slice(e, sl, c);
   long long tsum = 0, acc[SN];
 #pragma unroll
   for (int q = 0; q < SN; ++q) acc[q] = 0;
-  for (int64_t it = i0; it < i1; ++it) {
+  for (int rem = (int)(i1 - i0); rem > 0; --rem) {
     int en = e, sn = sl + 1;
     if (sn == nsl) {
       sn = 0;
       ++en;
     }
-    const bool more = it + 1 < i1;
+    const bool more = rem > 1;
     int cn[EB_U];
-    {
-      const int32_t* we = w + (int64_t)en * rowlen;
-#pragma unroll
-      for (int u = 0; u < EB_U; ++u) {
-        const int t = sn * SL + 32 * u + lane;
-        cn[u] = more && t <= N ? __ldcs(we + t) : 0;
-      }
-    }
+    if (more) load_slice(en, sn, cn);
     const int tb = sl * SL;
+    // 32-bit fast path: when every count of the slice is in [0, 2^EB_FB), a lane's EB_U products
+    // c_t t and c_t l sum to < EB_U 2^EB_FB 2^16 <= 2^32 (t, l <= SP_MAX_N < 2^16), so each lane
+    // accumulates the slice in uint32 and widens once; the tables are padded by SL entries
+    // (l = 0 past the row, c = 0 there) so the lookups need no clamp.  Otherwise int64 per bin.
+    unsigned orc = 0;
 #pragma unroll
-    for (int u = 0; u < EB_U; ++u) {
-      const int t = min(tb + 32 * u + lane, N);   // c = 0 past the row
-      tsum = mad_wide(c[u], t, tsum);
-      const uint32_t a = sbase + 2u * (uint32_t)t;
+    for (int u = 0; u < EB_U; ++u) orc |= (unsigned)c[u];
+    if (__all_sync(FULL, (orc >> EB_FB) == 0)) {
+      const uint32_t a0 = sbase + 2u * (uint32_t)(tb + lane);
+      uint32_t aq[SN], s32[SN];
 #pragma unroll
       for (int q = 0; q < SN; ++q) {
-        unsigned short l;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(l) : "r"(a + q * sstride));
-        acc[q] = mad_wide(c[u], (int)l, acc[q]);
+        aq[q] = a0 + (uint32_t)q * sstride;
+        s32[q] = 0;
+      }
+      uint32_t t32 = 0;
+#pragma unroll
+      for (int u = 0; u < EB_U; ++u) {
+        t32 += (uint32_t)c[u] * (uint32_t)(tb + 32 * u + lane);
+#pragma unroll
+        for (int q = 0; q < SN; ++q) {
+          unsigned short l;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(l) : "r"(aq[q] + 64u * u));
+          s32[q] += (uint32_t)c[u] * (uint32_t)l;
+        }
+      }
+      tsum += (long long)t32;
+#pragma unroll
+      for (int q = 0; q < SN; ++q) acc[q] += (long long)s32[q];
+    } else {
+#pragma unroll
+      for (int u = 0; u < EB_U; ++u) {
+        const int t = tb + 32 * u + lane;   // <= N + SL: c = 0 and l = 0 past the row
+        tsum = mad_wide(c[u], t, tsum);
+        const uint32_t a = sbase + 2u * (uint32_t)t;
+#pragma unroll
+        for (int q = 0; q < SN; ++q) {
+          unsigned short l;
+          asm volatile("ld.shared.u16 %0, [%1];" : "=h"(l) : "r"(a + q * sstride));
+          acc[q] = mad_wide(c[u], (int)l, acc[q]);
+        }
       }
     }
     if (sl == 0 && lane == 0) {
@@ -535,7 +568,7 @@ extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type w
   const int grid = n_entries < sms * 8 ? n_entries : sms * 8;
   cudaStream_t st = (cudaStream_t)stream;
   const int path = sp_debug_get(SP_DBG_EVAL_PATH);   // 0 auto; 1 chunked, 2 p32, 3 prefix
-  const size_t tab = (size_t)n_sets * (N + 1) * sizeof(uint16_t);
+  const size_t tab = (size_t)n_sets * (N + 1 + 32 * sp::EB_U) * sizeof(uint16_t);
   if (wtype == SP_W_COUNTS_I32 && path == 0 && broadcast && n_sets <= sp::EB_MAXS &&
       tab <= sp::EB_SMEM_MAX) {
     auto kern = n_sets == 1   ? sp::eval_bcast_kernel<1>

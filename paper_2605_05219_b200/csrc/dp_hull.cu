@@ -88,6 +88,9 @@ __host__ __device__ __forceinline__ int hull_layers_padded(int M) {
 // argmin-log capacity per layer: opt changes at a fraction of the support rows (W5: ~500 of
 // ~5170); an entry that fills a log goes to the D&C kernel (never on W5)
 __host__ __device__ __forceinline__ int hull_log_cap(int N) {
+#ifdef SP_HULL_BIGLOG
+  return N + 1;
+#endif
   const int c = (N + 1 + 7) / 8;
   return c < 1024 ? (N + 1 < 1024 ? N + 1 : 1024) : c;
 }

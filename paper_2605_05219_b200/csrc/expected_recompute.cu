@@ -200,8 +200,8 @@ template <typename ST, int EP_NT>
 __global__ void __launch_bounds__(EP_NT)
     eval_p32_kernel(const int32_t* __restrict__ w, int E, int N,
                     const int32_t* __restrict__ positions, const int32_t* __restrict__ npos,
-                    int S, int max_pos, int broadcast, int64_t* __restrict__ cost,
-                    int32_t* __restrict__ worst) {
+                    int S, int max_pos, int broadcast, int stage_sets,
+                    int64_t* __restrict__ cost, int32_t* __restrict__ worst) {
   constexpr int EP_NW = EP_NT / 32;
   extern __shared__ __align__(16) unsigned char seg_raw[];
   ST* seg = reinterpret_cast<ST*>(seg_raw);   // [nseg * 1024] in-segment prefixes
@@ -211,6 +211,32 @@ __global__ void __launch_bounds__(EP_NT)
   __shared__ int sh_big;
   const int lane = lane_id(), wid = warp_id();
   const int nseg = (N + 1 + 1023) / 1024;
+  // broadcast sets staged once per CTA (stage_sets: the host checked they fit): positions as
+  // uint16 (<= SP_MAX_N), and per set its worst case, or -1 for a malformed set
+  uint16_t* spos = reinterpret_cast<uint16_t*>(seg_raw + (size_t)nseg * 1024 * sizeof(ST));
+  int* sgap = reinterpret_cast<int*>(spos + (((size_t)S * max_pos + 1) & ~(size_t)1));
+  if (stage_sets) {
+    for (int q = wid; q < S; q += EP_NW) {
+      const int32_t* pc = positions + (int64_t)q * max_pos;
+      const int k = npos[q];
+      bool ok = k >= 0 && k <= max_pos;
+      int gmax = 0;
+      if (ok) {
+        for (int i = lane; i <= k; i += 32) {
+          const int ci = i == 0 ? 0 : pc[i - 1];
+          const int cn = i == k ? N + 1 : pc[i];
+          if (cn <= ci || cn > N + 1 || (i > 0 && ci < 1)) ok = false;
+          gmax = max(gmax, cn - ci);
+          if (i < k) spos[(size_t)q * max_pos + i] = (uint16_t)cn;
+        }
+      }
+      ok = __all_sync(FULL, ok);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) gmax = max(gmax, __shfl_xor_sync(FULL, gmax, o));
+      if (lane == 0) sgap[q] = ok ? gmax : -1;
+    }
+    __syncthreads();
+  }
   for (int e = blockIdx.x; e < E; e += gridDim.x) {
     const int32_t* we = w + (int64_t)e * (N + 1);
     long long tpart = 0;
@@ -281,6 +307,31 @@ __global__ void __launch_bounds__(EP_NT)
       for (int t = max((x >> 10) << 10, 1); t <= x; ++t) s += we[t];
       return s;
     };
+    if (stage_sets) {
+      // (set, 32-gap group) items over all warps: gap i >= 1 of set q adds c_i (P(c_{i+1} - 1) -
+      // P(c_i - 1)), both positions read from the staged copy
+      for (int q = wid; q < S; q += EP_NW) {
+        const int k = npos[q];
+        const int g = sgap[q];
+        long long acc = 0;
+        if (g >= 0) {
+          const uint16_t* sp = spos + (size_t)q * max_pos;
+          for (int i = 1 + lane; i <= k; i += 32) {
+            const int ci = sp[i - 1];
+            const int cn = i == k ? N + 1 : sp[i];
+            acc += (long long)ci * (Pof(cn - 1) - Pof(ci - 1));
+          }
+          acc = warp_sum(acc);
+        }
+        if (lane == 0) {
+          const int64_t oi = (int64_t)e * S + q;
+          cost[oi] = g >= 0 ? TN - acc : -1;
+          if (worst) worst[oi] = g >= 0 ? g - 1 : -SP_ERR_BAD_POSITIONS;
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     for (int q = wid; q < S; q += EP_NW) {
       const int64_t set = broadcast ? q : (int64_t)e * S + q;
       const int32_t* pc = positions + set * max_pos;
@@ -584,7 +635,11 @@ extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type w
   } else if (wtype == SP_W_COUNTS_I32 && path != 1) {
     const int nseg = (N + 1 + 1023) / 1024;
     const bool wide = path == 2;   // 4-byte prefixes (tests / comparison)
-    const size_t dyn = (size_t)nseg * 1024 * (wide ? 4 : 2);
+    size_t dyn = (size_t)nseg * 1024 * (wide ? 4 : 2);
+    // broadcast sets staged in shared memory when they fit in 32 KB more
+    const size_t sets_bytes = (((size_t)n_sets * max_pos + 1) & ~(size_t)1) * 2 + (size_t)n_sets * 4;
+    const int stage = broadcast && sets_bytes <= 32 * 1024;
+    if (stage) dyn += sets_bytes;
     const int occ = wide ? eval_occ(sp::eval_p32_kernel<int32_t, 512>, 512, dyn, 4)
                          : eval_occ(sp::eval_p32_kernel<uint16_t, 256>, 256, dyn, 5);
     const long gcap = (long)sms * (occ < 1 ? 1 : occ);
@@ -592,11 +647,11 @@ extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type w
     if (wide)
       sp::eval_p32_kernel<int32_t, 512><<<g2, 512, dyn, st>>>(
           (const int32_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
-          broadcast, (int64_t*)cost, worst_case);
+          broadcast, stage, (int64_t*)cost, worst_case);
     else
       sp::eval_p32_kernel<uint16_t, 256><<<g2, 256, dyn, st>>>(
           (const int32_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
-          broadcast, (int64_t*)cost, worst_case);
+          broadcast, stage, (int64_t*)cost, worst_case);
   } else if (wtype == SP_W_COUNTS_I32)
     sp::eval_kernel<int32_t><<<grid, sp::EV_NT, 0, st>>>(
         (const int32_t*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,

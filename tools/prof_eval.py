@@ -15,13 +15,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--entries", type=int, default=16384)
 ap.add_argument("--workload", default="W5")
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--sweep", action="store_true", help="the workload's budget sweep (W4: M = 1..64)")
 a = ap.parse_args()
 cfg = wl.scaled(wl.CONFIGS[a.workload], a.entries)
 dev = torch.device("cuda:0")
 H = wl.make_dense_hist(cfg, seed=0, device=dev)
-bpos, bnpos, _ = sp.baseline_sets(cfg.N, budgets=(cfg.M,), blocks=(64, 128), device=dev)
+budgets = cfg.M_sweep if a.sweep and cfg.M_sweep else (cfg.M,)
+bpos, bnpos, _ = sp.baseline_sets(cfg.N, budgets=budgets, blocks=(64, 128), device=dev)
+print(f"{cfg.name}: {cfg.n_entries} entries, N={cfg.N}, {bpos.shape[0]} broadcast sets")
 out = {}
-for name, path in (("bcast", 0), ("prefix", 3)):
+for name, path in (("auto", 0), ("prefix", 3), ("chunked", 1)):
     dbg = sp.debug(SP_DBG_EVAL_PATH=path)
     dbg.__enter__()
     ts = []
@@ -37,5 +40,5 @@ for name, path in (("bcast", 0), ("prefix", 3)):
     gb = H.numel() * 4 / 1e9
     print(f"{name}: " + " ".join(f"{t:.3f}" for t in ts) + f" ms  ({gb:.2f} GB row bytes, "
           f"{gb / min(ts) * 1e3:.0f} GB/s at best)", flush=True)
-print("agree:", bool(torch.equal(out["bcast"][0], out["prefix"][0])
-                     and torch.equal(out["bcast"][1], out["prefix"][1])))
+print("agree:", all(bool(torch.equal(out["auto"][i], out[k][i])) for k in ("prefix", "chunked")
+                    for i in (0, 1)))

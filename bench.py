@@ -26,8 +26,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DP cells/s (entries*N*M)"
-TRAFFIC_JSON = "r02b_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
-PIPES_JSON = "r02b_ncu_pipes.json"       # the same capture: issue / ALU / FMA / LSU pipe %
+TRAFFIC_JSON = "r02c_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
+PIPES_JSON = "r02c_ncu_pipes.json"       # the same capture: issue / ALU / FMA / LSU pipe %
 
 
 def dp_update_cost():
@@ -684,8 +684,11 @@ def run_ours(args):
                          "frac": lcp_bytes_all * K / (lcp_ms / 1e3) / 1e9 / world / hbm_peak,
                          "traffic": traffic.get("lcp_hist_kernel", {}).get("traffic_bytes"),
                          "algorithmic_bytes": lcp_bytes_all / world},
-        # a6 (eval_bcast_kernel): reads every histogram row once, writes E x S costs
-        "roofline_eval": {"bound": "hbm", "kernel": "eval_bcast_kernel",
+        # a6: reads every histogram row once, writes E x S costs (eval_bcast_kernel for <= 4
+        # broadcast sets whose l tables fit shared memory, else eval_p32_kernel)
+        "roofline_eval": {"bound": "hbm", "kernel": (f"eval_bcast_kernel<{S}>"
+                                                     if S <= 4 and S * (N + 1 + 384) * 2 <= 200 * 1024
+                                                     else "eval_p32_kernel<uint16_t, 256>"),
                           "achieved": eval_bytes * K / (eval_ms / 1e3) / 1e9,
                           "peak": hbm_peak, "unit": "GB/s",
                           "frac": eval_bytes * K / (eval_ms / 1e3) / 1e9 / hbm_peak,

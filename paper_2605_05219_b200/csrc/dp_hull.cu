@@ -474,9 +474,10 @@ __host__ __device__ constexpr size_t ring_bytes() {
   if constexpr (sizeof(VT) == 8) return (size_t)(WC + (K == 2 ? WC : 0)) * 384;
   return (size_t)(HC0 + (K == 2 ? HC1 : 0)) * 192;
 }
-// the row stage of one warp (a super-chunk of counts)
+// per-warp row staging in shared memory: none (the counts wait in a register queue, HULL_PF
+// chunks deep; a shared stage cost a warp per SM and was dropped)
 template <typename VT>
-__host__ __device__ constexpr size_t stage_bytes() { return 0; }   // (no row stage)
+__host__ __device__ constexpr size_t stage_bytes() { return 0; }
 template <int K, typename VT>
 constexpr size_t hull_dyn_bytes() { return ring_bytes<K, VT>() + stage_bytes<VT>(); }
 
@@ -577,9 +578,6 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
     // the counts are loaded HULL_PF chunks (32 rows each) ahead: a chunk of W5's rows holds ~5
     // support rows, but sparse rows (W2/W3: ~0.2-2% support) would otherwise wait for HBM on
     // every 32 rows
-    // Rows are read in super-chunks of HULL_PF chunks: the next super-chunk's counts are loaded
-    // into registers while the current one, staged in shared memory, is processed chunk by chunk
-    // (no register shuffling per chunk; an empty chunk costs a shared load and a ballot).
     // Rows: dense rows are read 32 at a time with HULL_PF chunks in flight (a register queue);
     // sparse rows (K <= HULL_KC, compacted by the pre-pass) are walked as their list of (j, c_j)
     // pairs instead -- no scan over the N bins (CMP: a compile-time path).

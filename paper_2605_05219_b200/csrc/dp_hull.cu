@@ -481,6 +481,12 @@ __host__ __device__ constexpr size_t stage_bytes() { return 0; }
 template <int K, typename VT>
 constexpr size_t hull_dyn_bytes() { return ring_bytes<K, VT>() + stage_bytes<VT>(); }
 
+// prefetch one global address into L1 (no register written, nothing to wait on)
+template <typename T>
+__device__ __forceinline__ void prefetch_l1(const T* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // value of the dummy front line (above every candidate)
 template <typename VT>
 __device__ __forceinline__ VT hull_inf() {
@@ -585,9 +591,16 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
     const int total = compact ? kc : N;
     VT cq[HULL_PF];
     if constexpr (!compact) {
+#ifdef SP_HULL_REGQ
 #pragma unroll
       for (int c = 0; c < HULL_PF; ++c)
         cq[c] = 32 * c + 1 + lane <= N ? (VT)we[32 * c + 1 + lane] : (VT)0;
+#else
+      cq[0] = 1 + lane <= N ? (VT)we[1 + lane] : (VT)0;
+#pragma unroll
+      for (int c = 1; c < HULL_PF; ++c)
+        if (32 * c + 1 + lane <= N) prefetch_l1(we + 32 * c + 1 + lane);
+#endif
     }
     for (int jb = 0; jb < total; jb += 32) {
       int jr;
@@ -599,9 +612,17 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       } else {
         jr = jb + 1 + lane;
         craw = cq[0];
+#ifdef SP_HULL_REGQ
 #pragma unroll
         for (int c = 0; c + 1 < HULL_PF; ++c) cq[c] = cq[c + 1];
         cq[HULL_PF - 1] = jr + 32 * HULL_PF <= N ? (VT)we[jr + 32 * HULL_PF] : (VT)0;
+#else
+        // the next chunk into a register (an L1 hit: prefetched HULL_PF chunks ago), the chunk
+        // HULL_PF ahead into L1.  (A register queue HULL_PF deep made every chunk's queue shift
+        // wait on the newest load: the prefetch distance was one chunk.)
+        cq[0] = jr + 32 <= N ? (VT)we[jr + 32] : (VT)0;
+        if (jr + 32 * HULL_PF <= N) prefetch_l1(we + jr + 32 * HULL_PF);
+#endif
       }
       unsigned evmask = __ballot_sync(FULL, craw > 0);   // support rows of this chunk
       if (evmask == 0) continue;                          // 32 zero rows: nothing changes
@@ -685,9 +706,10 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         // lane 0 slot 0 from the previous pass (or e_0 = 0)
         VT in[K];
         const VT t0 = __shfl_sync(FULL, eo[0], (lane + 31) & 31);
-        // unconditional (Ec = 0 without a previous pass): the row's shuffles stay in one
-        // converged region, so ptxas emits one divergence check (BRA.DIV) for all of them
-        const VT ext = __shfl_sync(FULL, Ec, q);
+        // only after a previous pass (warp-uniform): Ec's register is the target of a load that
+        // is predicated off in a single pass, and a shuffle reading it waited on its scoreboard
+        VT ext = 0;
+        if (chain_in) ext = __shfl_sync(FULL, Ec, q);
         in[0] = lane ? t0 : ext;
         if constexpr (K == 2) {
           const VT t1 = __shfl_sync(FULL, eo[1], (lane + 31) & 31);

@@ -465,6 +465,56 @@ def test_expected_recompute_broadcast_tables(dev, N, E):
                 assert (np_(worst)[:, 3] == -sp.SP_ERR_BAD_POSITIONS).all()
 
 
+@pytest.mark.parametrize("N", [383, 384, 385, 1000])
+def test_expected_recompute_bcast_fast_path_thresholds(dev, N):
+    """eval_bcast_kernel's uint32 slice sums hold while every count of a 384-bin slice lies in
+    [0, 2^13): counts at 2^13 - 1 (fast), 2^13 (int64 path), negative counts and INT32_MAX (int64
+    path) are mixed per slice, rows ragged against the slice width; against the oracle."""
+    E = 37
+    rng = np.random.default_rng(N)
+    H = rng.integers(0, 2 ** 13, size=(E, N + 1)).astype(np.int64)
+    H[rng.random((E, N + 1)) < 0.5] = 0
+    H[:, 0] = rng.integers(0, 5, size=E)                    # bin 0 (misses) is never weighted
+    H[1, :] = 2 ** 13 - 1                                   # the fast path's largest count
+    H[2, rng.integers(1, N + 1, size=3)] = 2 ** 13          # one count past it per few slices
+    H[3, rng.integers(1, N + 1, size=5)] = -1               # negative counts (int64 path)
+    H[4, N] = 2 ** 31 - 1                                   # the last bin, INT32_MAX
+    H[5, 1:] = 2 ** 31 - 1                                  # a full row of INT32_MAX
+    H = H.astype(np.int32)
+    sets = [sp.balanced_positions(N, 64), sp.block_positions(N, 64), sp.block_positions(N, 128)]
+    width = max(len(x) for x in sets)
+    pos = np.zeros((3, width), np.int32)
+    npos = np.array([len(x) for x in sets], np.int32)
+    for i, x in enumerate(sets):
+        pos[i, :len(x)] = x
+    rc, rw = oracle.eval_batch(H, pos, npos, broadcast=True, nthreads=8)
+    cost, worst = sp.expected_recompute(torch.from_numpy(H).to(dev), torch.from_numpy(pos).to(dev),
+                                        torch.from_numpy(npos).to(dev), broadcast=True)
+    torch.cuda.synchronize()
+    assert (np_(cost) == rc).all() and (np_(worst) == rw).all()
+
+
+def test_expected_recompute_staged_sweep_sets(dev):
+    """eval_p32_kernel with the broadcast sets staged in shared memory (W4's 66-set budget
+    sweep, plus an empty and a malformed set): every cost and worst case against the oracle."""
+    cfg = wl.scaled(wl.CONFIGS["W4"], 45)
+    H = wl.make_dense_hist(cfg, seed=21).numpy()
+    pos, npos, _ = sp.baseline_sets(cfg.N, budgets=cfg.M_sweep, blocks=(64, 128), device=dev)
+    P = np.zeros((pos.shape[0] + 2, pos.shape[1]), np.int32)
+    K = np.zeros(pos.shape[0] + 2, np.int32)
+    P[:-2], K[:-2] = np_(pos), np_(npos)
+    K[-2] = 0                                   # empty set: cost T_N, worst N
+    P[-1, :3] = [10, 9, 30]                     # malformed
+    K[-1] = 3
+    rc, rw = oracle.eval_batch(H, P[:-1].copy(), K[:-1].copy(), broadcast=True, nthreads=8)
+    cost, worst = sp.expected_recompute(torch.from_numpy(H).to(dev), torch.from_numpy(P).to(dev),
+                                        torch.from_numpy(K).to(dev), broadcast=True)
+    torch.cuda.synchronize()
+    assert (np_(cost)[:, :-1] == rc).all() and (np_(worst)[:, :-1] == rw).all()
+    assert (np_(cost)[:, -1] == -1).all()
+    assert (np_(worst)[:, -1] == -sp.SP_ERR_BAD_POSITIONS).all()
+
+
 def test_expected_recompute_dp_positions_and_bad_sets(dev):
     """E[r](DP output) == V_M, per-entry (non-broadcast) sets, malformed sets flagged."""
     cfg = wl.scaled(wl.CONFIGS["W3"], 16)

@@ -68,6 +68,11 @@ def parse():
                     help="DP input rows: dense depth-mode (default, SURVEY 8(d) W5); ones: all-ones "
                          "rows (full support, the D&C worst case and Thm 1's uniform law); accum: "
                          "accumulated rows with n ~ U[1.2e5, 1.8e5] draws (past the int32 guard)")
+    ap.add_argument("--weights", default="i32", choices=["i32", "f64"],
+                    help="i32: integer counts (exact int32 path, the default); f64: the paper's "
+                         "probability weights (a7) kept by the gamma-estimator (f2, P:323-343, "
+                         "P:380): each step's LCPs are observed into fp64 rows W (initialised from "
+                         "the dense rows) and the fp64 DP and evaluation run on W (N = 1 only)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the config's entries split over the GPUs (BASELINE configs[4]); "
                          "weak: the config's entries on every GPU")
@@ -332,6 +337,9 @@ def workload_config(args, world, extra):
                          getattr(args, "dp_hist", "dense"))
                      or (f"dense depth-mode, n~U{list(cfg.dense_n)} draws/entry, {cfg.dense_shape} "
                          f"laws, + the step's requests" if cfg.dense_n else "from the LCP requests")),
+         "weights": ("f64: gamma-estimator rows W (gamma = 0.99), initialised from the dense "
+                     "rows, the step's LCPs observed into them (P:323-343, P:380)"
+                     if getattr(args, "weights", "i32") == "f64" else "int32 counts"),
          "parallelism": f"entries sharded over {world} GPU(s) ({args.scaling} scaling)",
          "merge": None if world == 1 else args.merge,
          "l2": "inputs larger than L2 (request tokens and histograms >> 126 MB)"}
@@ -365,7 +373,7 @@ class HotPath:
     entries, a6 baseline evaluation."""
 
     def __init__(self, cfg, E_tot, E_own, world, rank, merge, seed, dev, ops=None,
-                 dp_hist="dense"):
+                 dp_hist="dense", weights="i32"):
         import torch
         from paper_2605_05219_b200 import workload as wl
         if ops is None:
@@ -389,15 +397,27 @@ class HotPath:
                                            n_entries=E_own)
         else:
             self.hist = torch.zeros(E_own, N + 1, dtype=torch.int32, device=dev)
+        self.gest = None
+        if weights == "f64":
+            # a7 on the paper's probability weights: the gamma-estimator's rows W (f2; its
+            # observe kernel folds each step's LCPs in, misses skipped, R15), W initialised
+            # from the resident counts; the DP and the evaluation run on W (scale invariant)
+            assert world == 1, "--weights f64 runs at N = 1"
+            self.gest = ops.GammaEstimator(E_own, N, gamma=0.99, device=dev)
+            self.gest.W.copy_(self.hist)
+            re_ = tr["req_entry"].long()
+            bounds = torch.arange(E_own + 1, device=dev, dtype=torch.int64)
+            self.obs_off = torch.searchsorted(re_, bounds).to(torch.int64)
+        cdt = torch.float64 if weights == "f64" else torch.int64
         budgets = cfg.M_sweep if cfg.M_sweep else (M,)
         self.bpos, self.bnpos, self.labels = ops.baseline_sets(N, budgets=budgets,
                                                                blocks=(64, 128), device=dev)
         self.S = S = self.bpos.shape[0]
         self.positions = torch.empty(E_own, M, dtype=torch.int32, device=dev)
         self.npos = torch.empty(E_own, dtype=torch.int32, device=dev)
-        self.cost = torch.empty(E_own, dtype=torch.int64, device=dev)
-        self.cbb = torch.empty(E_own, M + 1, dtype=torch.int64, device=dev)
-        self.bcost = torch.empty(E_own, S, dtype=torch.int64, device=dev)
+        self.cost = torch.empty(E_own, dtype=cdt, device=dev)
+        self.cbb = torch.empty(E_own, M + 1, dtype=cdt, device=dev)
+        self.bcost = torch.empty(E_own, S, dtype=cdt, device=dev)
         self.bworst = torch.empty(E_own, S, dtype=torch.int32, device=dev)
         self.ws = torch.empty(ops.place_checkpoints_workspace_bytes(E_own, N, M),
                               dtype=torch.uint8, device=dev)
@@ -413,7 +433,11 @@ class HotPath:
         if marks:
             marks[0].record(stream)
         # a1 + a2
-        if self.world == 1:
+        if self.gest is not None:   # f64: the LCPs only; the estimator takes them below
+            ops.overlap_hist(tr["entry_tokens"], tr["entry_off"], tr["req_tokens"], tr["req_off"],
+                             tr["req_entry"], N, lcp_out=self.lcp, n_entries=self.E_tot,
+                             stream=stream, with_hist=False)
+        elif self.world == 1:
             ops.overlap_hist(tr["entry_tokens"], tr["entry_off"], tr["req_tokens"], tr["req_off"],
                              tr["req_entry"], N, hist=self.hist, lcp_out=self.lcp,
                              n_entries=self.E_tot, stream=stream)
@@ -430,16 +454,19 @@ class HotPath:
         # merge (the one exchange step)
         if self.world > 1:
             self.merger.merge(self.hist, stream=stream)
+        if self.gest is not None:   # f2: observe the step's depths into W
+            self.gest.observe(self.obs_off, self.lcp, stream=stream)
         if marks:
             marks[2].record(stream)
+        w = self.hist if self.gest is None else self.gest.W
         # a3 - a5
-        ops.place_checkpoints(self.hist, M, positions=self.positions, n_positions=self.npos,
+        ops.place_checkpoints(w, M, positions=self.positions, n_positions=self.npos,
                               cost=self.cost, cost_by_budget=self.cbb, workspace=self.ws,
                               stream=stream)
         if marks:
             marks[3].record(stream)
         # a6
-        ops.expected_recompute(self.hist, self.bpos, self.bnpos, broadcast=True, cost=self.bcost,
+        ops.expected_recompute(w, self.bpos, self.bnpos, broadcast=True, cost=self.bcost,
                                worst=self.bworst, stream=stream)
         if marks:
             marks[4].record(stream)
@@ -473,7 +500,7 @@ def run_ours(args):
     e0 = rank * E_own
     N, M = cfg.N, cfg.M
     hp = HotPath(cfg, E_tot, E_own, world, rank, args.merge, args.seed, dev,
-                 dp_hist=args.dp_hist)
+                 dp_hist=args.dp_hist, weights=args.weights)
     tr, hist, R = hp.tr, hp.hist, hp.R
     positions, npos, cost, cbb, bcost, bworst = (hp.positions, hp.npos, hp.cost, hp.cbb,
                                                  hp.bcost, hp.bworst)
@@ -542,9 +569,9 @@ def run_ours(args):
         h_ent = req_entry.cpu().pin_memory()
         o_pos = torch.empty(positions.shape, dtype=torch.int32, pin_memory=True)
         o_npos = torch.empty(npos.shape, dtype=torch.int32, pin_memory=True)
-        o_cost = torch.empty(cost.shape, dtype=torch.int64, pin_memory=True)
-        o_bcost = torch.empty(bcost.shape, dtype=torch.int64, pin_memory=True)
-        o_cbb = torch.empty(cbb.shape, dtype=torch.int64, pin_memory=True)
+        o_cost = torch.empty(cost.shape, dtype=cost.dtype, pin_memory=True)
+        o_bcost = torch.empty(bcost.shape, dtype=bcost.dtype, pin_memory=True)
+        o_cbb = torch.empty(cbb.shape, dtype=cbb.dtype, pin_memory=True)
         bi = (h_tok.numel() * 4 + h_off.numel() * 8 + h_ent.numel() * 4)
         bo = (o_pos.numel() * 4 + o_npos.numel() * 4 + o_cost.numel() * 8 + o_bcost.numel() * 8
               + o_cbb.numel() * 8)
@@ -584,14 +611,22 @@ def run_ours(args):
                 for c in range(C):
                     stream.wait_event(cev[c])
                     r0, r1, a0, a1 = rb[c], rb[c + 1], eb[c], eb[c + 1]
+                    g = hp.gest
                     if r1 > r0:
                         sp.overlap_hist(tr["entry_tokens"], tr["entry_off"], req_tokens,
-                                        req_off[r0:r1 + 1], req_entry[r0:r1], N, hist=hist,
-                                        lcp_out=lcp[r0:r1], n_entries=E_tot, stream=stream)
-                    sp.place_checkpoints(hist[a0:a1], M, positions=positions[a0:a1],
+                                        req_off[r0:r1 + 1], req_entry[r0:r1], N,
+                                        hist=hist if g is None else None,
+                                        lcp_out=lcp[r0:r1], n_entries=E_tot, stream=stream,
+                                        with_hist=g is None)
+                    w = hist
+                    if g is not None:   # f64: observe the block's depths, then solve on W
+                        sp.gamma_observe(g.W[a0:a1], g.t[a0:a1], g.tau[a0:a1],
+                                         hp.obs_off[a0:a1 + 1], lcp, g.gamma, stream)
+                        w = g.W
+                    sp.place_checkpoints(w[a0:a1], M, positions=positions[a0:a1],
                                          n_positions=npos[a0:a1], cost=cost[a0:a1],
                                          cost_by_budget=cbb[a0:a1], workspace=ws, stream=stream)
-                    sp.expected_recompute(hist[a0:a1], bpos, bnpos, broadcast=True,
+                    sp.expected_recompute(w[a0:a1], bpos, bnpos, broadcast=True,
                                           cost=bcost[a0:a1], worst=bworst[a0:a1], stream=stream)
                     o_pos[a0:a1].copy_(positions[a0:a1], non_blocking=True)
                     o_npos[a0:a1].copy_(npos[a0:a1], non_blocking=True)
@@ -630,7 +665,8 @@ def run_ours(args):
     value = E_tot * N * M * K / (ms_max / 1e3)
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    eval_bytes = E_own * (N + 1) * 4 + E_own * S * (8 + 4)   # rows read once; costs + worst
+    wbytes = 8 if args.weights == "f64" else 4
+    eval_bytes = E_own * (N + 1) * wbytes + E_own * S * (8 + 4)   # rows read once; costs + worst
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
@@ -642,8 +678,9 @@ def run_ours(args):
     upd = dp_update_cost()
     updates = stats["hull_event_rows"] * M
     traffic, pipes = {}, {}
+    f64 = args.weights == "f64"
     try:   # DRAM bytes and pipe utilisation per launch from the committed `ncu --set full`
-        if args.workload == "W5" and E_own == 16384 and args.dp_hist == "dense":
+        if args.workload == "W5" and E_own == 16384 and args.dp_hist == "dense" and not f64:
             traffic = json.load(open(os.path.join(ROOT, "profiles", TRAFFIC_JSON)))
             pipes = json.load(open(os.path.join(ROOT, "profiles", PIPES_JSON)))
     except Exception:
@@ -654,25 +691,31 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None, "dtype": "int32-exact (int64 costs)",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": ("f64 (double-double P_j and costs, reading R10)" if f64
+                                                  else "int32-exact (int64 costs)"),
         "data": "synthetic (seeded; SURVEY 8(d) recipe)",
         "config": workload_config(args, world, None),
         "lcp_tokens_per_s": tokens_all * K / (lcp_ms / 1e3),
-        "stage_ms_per_step": {"lcp_hist": lcp_ms / K, "merge": merge_ms / K, "dp": dp_ms / K,
-                              "eval": eval_ms / K},
-        "roofline": {"bound": "alu", "kernel": "dp_hull_kernel<int32> (dp_hull_split_kernel for < 1.5 entries per resident warp)", "achieved": achieved,
+        "stage_ms_per_step": {"lcp_hist": lcp_ms / K,
+                              ("gamma_observe" if f64 else "merge"): merge_ms / K,
+                              "dp": dp_ms / K, "eval": eval_ms / K},
+        "roofline": {"bound": "alu", "kernel": ("dp_hull_kernel<double, 2, double>" if f64 else
+                                                         "dp_hull_kernel<int32> (dp_hull_split_kernel for < 1.5 entries per resident warp)"), "achieved": achieved,
                      "peak": peak, "unit": "Gupd/s", "frac": achieved / peak,
                      "traffic": traffic.get("dp_hull_kernel<int, 2, int>", {}).get("traffic_bytes"),
                      "work": f"{updates} hull updates per launch = {stats['hull_event_rows']} "
                              f"support rows x M (support rows = {stats['hull_event_rows'] / max(1, stats['entries_hull']) / N:.3f} "
                              f"of N per entry; zero-count rows are exact no-ops); "
-                             f"{stats['entries_hull']} entries on the hull kernel, "
+                             f"{stats['entries_hull']} entries on the hull kernel "
+                             f"({stats.get('entries_hull_big', 0)} in its large-hull mode), "
                              f"{E_own - stats['entries_hull']} on the D&C fallback "
                              f"({stats['evaluations']} candidate evaluations)",
                      "peak_basis": (f"{sms} SMs x {sm_max:.0f} MHz / {upd['clk_per_update_per_sm']:.4f} "
                                     f"SM-cycles per update (binding pipe: {upd['binding']}); "
                                     f"minimal amortised update = {upd['ops']} at measured lanes/clk/SM "
-                                    f"{upd['rates']}"),
+                                    f"{upd['rates']}"
+                                    + ("; the int32 step's peak: the fp64 step's own minimal SASS "
+                                       "(DFMA / DSETP) is not derived" if f64 else "")),
                      "pipes_ncu": pipes.get("dp_hull_kernel<int, 2, int>"),
                      "support_fraction": stats["hull_event_rows"] / max(1, stats["entries_hull"]) / N
                      if stats["entries_hull"] else None,
@@ -686,7 +729,8 @@ def run_ours(args):
                          "algorithmic_bytes": lcp_bytes_all / world},
         # a6: reads every histogram row once, writes E x S costs (eval_bcast_kernel for <= 4
         # broadcast sets whose l tables fit shared memory, else eval_p32_kernel)
-        "roofline_eval": {"bound": "hbm", "kernel": (f"eval_bcast_kernel<{S}>"
+        "roofline_eval": {"bound": "hbm", "kernel": ("eval_kernel<double>" if f64 else
+                                                     f"eval_bcast_kernel<{S}>"
                                                      if S <= 4 and S * (N + 1 + 384) * 2 <= 200 * 1024
                                                      else "eval_p32_kernel<uint16_t, 256>"),
                           "achieved": eval_bytes * K / (eval_ms / 1e3) / 1e9,
@@ -696,10 +740,12 @@ def run_ours(args):
                           "algorithmic_bytes": eval_bytes},
         "dp_paths": {k: v for k, v in stats.items()},
         # per step: lcp_hist, row_stats (+ CUB's radix-sort kernels), dp_hull<int32> (or
-        # dp_hull_split for small batches), dp_hull<int64> (its list; exits at once when empty),
-        # dp_place (the D&C list; ditto), eval (+ accumulate_depths for the sparse merge).
-        # Counted: our kernels only.
-        "gpu_launches": K * (6 + (1 if world > 1 and args.merge == "sparse" else 0)),
+        # dp_hull_split for small batches), its large-hull mode and dp_hull<int64> (their lists;
+        # each exits at once when empty), dp_place (the D&C list; ditto), eval (+
+        # accumulate_depths for the sparse merge).  f64: lcp_hist, gamma_observe, row_stats,
+        # dp_hull<double>, dp_place, eval.  Counted: our kernels only.
+        "gpu_launches": K * (6 if f64 else
+                             7 + (1 if world > 1 and args.merge == "sparse" else 0)),
         "clocks": clk,
         "e2e": e2e,
     }

@@ -128,6 +128,9 @@ typedef struct {
   unsigned long long hull_pops;        /* hull kernel: lines popped (back + front)            */
   unsigned long long entries_hull;     /* entries solved by the hull kernel (rest: D&C)       */
   unsigned long long hull_event_rows;  /* hull kernel: rows with c_j > 0 (line push + query)  */
+  unsigned long long entries_hull_big; /* of entries_hull: solved by the int32 large-hull mode
+                                          (hulls past the shared rings, e.g. all-ones rows;
+                                          unary argmin logs)                    */
 } sp_dp_stats;
 
 sp_status sp_place_checkpoints(const void* weights, sp_weight_type wtype, int32_t n_entries,

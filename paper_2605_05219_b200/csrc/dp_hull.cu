@@ -254,6 +254,51 @@ __device__ __forceinline__ int log_lookup_lane(const uint32_t* lg, int cnt, int 
   return (int)(__ldcg(lg + lo) & 0xffffu);
 }
 
+// The large-hull mode's unary argmin logs (hull_dp<.., BIG>): layer m's stream holds, per stepped
+// (support) row in order, opt_m(j) - opt_m(j_prev) zeros then a one (opt = 0 before the first row),
+// so opt_m at the r-th support row = the zeros before the r-th one.  Warp-cooperative, scanning
+// from the end (the backtrack's ranks are large for the high layers it starts with).
+__device__ __forceinline__ int unary_lookup_warp(const uint32_t* lg, int nw, int r) {
+  const int lane = lane_id();
+  int total = 0;   // ones in the stream (= stepped rows)
+  for (int w = lane; w < nw; w += 32) total += __popc(__ldcg(lg + w));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(FULL, total, o);
+  int need = total - r + 1;   // the need-th one counted from the end
+  for (int w1 = nw; w1 > 0; w1 -= 32) {
+    const int w = w1 - 1 - lane;   // lane 0 takes the highest word
+    const uint32_t v = w >= 0 ? __ldcg(lg + w) : 0u;
+    const int c = __popc(v);
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int tot = __shfl_sync(FULL, inc, 31);
+    if (tot >= need) {
+      const int L = __ffs(__ballot_sync(FULL, inc >= need)) - 1;
+      const int q = need - __shfl_sync(FULL, inc - c, L);   // the q-th one from the top of word L
+      uint32_t vw = __shfl_sync(FULL, v, L);
+      for (int i = __popc(vw) - q; i > 0; --i) vw &= vw - 1;   // drop the lower ones
+      const int g = (w1 - 1 - L) * 32 + (__ffs(vw) - 1);       // bit index of the r-th one
+      return g - (r - 1);
+    }
+    need -= tot;
+  }
+  return 0;
+}
+// support rows (c_t > 0) with a <= t <= b: one coalesced pass over the bins
+template <typename WT>
+__device__ __forceinline__ int count_support_warp(const WT* __restrict__ we, int a, int b) {
+  int c = 0;
+  for (int t0 = a; t0 <= b; t0 += 32) {
+    const int t = t0 + lane_id();
+    c += __popc(__ballot_sync(FULL, t <= b && we[t] > 0));
+  }
+  return c;
+}
+
 // A hull line: intercept b_s (value type VT) and s.
 template <typename VT>
 struct Line {
@@ -395,20 +440,22 @@ template <>
 struct GLineT<int> {
   int b, s;
 };
-template <typename VT>
+// BIGCAP: the int32 large-hull mode (dp_hull_kernel<.., int, BIG>) sizes its int32 arrays like
+// the int64 instantiation's, wring_cap(N, m)
+template <typename VT, bool BIGCAP = false>
 __host__ __device__ __forceinline__ int wring_cap_t(int N, int m) {
-  return std::is_same<VT, int>::value ? WSMALL : wring_cap(N, m);
+  return std::is_same<VT, int>::value && !BIGCAP ? WSMALL : wring_cap(N, m);
 }
 // bytes of one CTA's global arrays: the largest pass (the first: lowest layers, largest caps)
-template <typename VT>
+template <typename VT, bool BIGCAP = false>
 __host__ __device__ __forceinline__ size_t wring_pass_bytes_t(int N, int M) {
   const int L = 32 * hull_K(M);
   size_t n = 0;
-  for (int m = 1; m <= L; ++m) n += (size_t)wring_cap_t<VT>(N, m);
+  for (int m = 1; m <= L; ++m) n += (size_t)wring_cap_t<VT, BIGCAP>(N, m);
   return hull_align(n * sizeof(GLineT<VT>));
 }
 
-template <typename VT, class SM>
+template <typename VT, class SM, bool BIGCAP = false>
 struct WRing {
   SM sm;
   GLineT<VT>* g[2];   // this lane's chain for slot 0 / 1 in the current pass
@@ -442,6 +489,7 @@ struct WRing {
     sm.st(k, pos, v);
   }
   __device__ __forceinline__ int span_cap(int k) const { return gm[k] + 1; }
+  __device__ __forceinline__ const GLineT<VT>* gaddr(int k, int pos) const { return g[k] + (pos & gm[k]); }
   // plain window accesses (exact while the deque lies within C - 2 of hi: see hull_dp)
   __device__ __forceinline__ Line<VT> ldw(int k, int pos) const { return sm.ld(k, pos); }
   __device__ __forceinline__ void stw(int k, int pos, Line<VT> v) const { sm.st(k, pos, v); }
@@ -453,7 +501,7 @@ struct WRing {
     size_t off = 0;
     for (int q = 0; q < L; ++q) {   // every slot, active or not (inactive lanes still load/store)
       const int m = ps * L + q + 1;
-      const int c = wring_cap_t<VT>(N, m);
+      const int c = wring_cap_t<VT, BIGCAP>(N, m);
       if ((q & 31) == lane) {   // (constant indices: g[] stays in registers)
         GLineT<VT>* gp = reinterpret_cast<GLineT<VT>*>(base) + off;
         if ((q >> 5) == 0) {
@@ -485,6 +533,12 @@ constexpr size_t hull_dyn_bytes() { return ring_bytes<K, VT>() + stage_bytes<VT>
 template <typename T>
 __device__ __forceinline__ void prefetch_l1(const T* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+// prefetch one global address into L2
+template <typename T>
+__device__ __forceinline__ void prefetch_l2(const T* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 // value of the dummy front line (above every candidate)
@@ -531,7 +585,11 @@ struct SplitSync {
 
 // ALLACT: every slot of every pass holds a layer (M a multiple of 32 K) -- the per-slot "active"
 // predicates vanish at compile time
-template <typename WT, typename VT, int K, bool ALLACT, class RING, bool CMP = false>
+// BIG (int32, the large-hull mode): argmin logs in unary form -- per stepped (support) row,
+// opt_m(j) - opt_m(j_prev) zero bits then a one bit, LSB first -- at most K + N <= 2N bits per
+// layer whatever the hull does (a change log fills when opt moves on most rows, e.g. all-ones);
+// the front lines of hulls that outgrow the window are prefetched into L2 16 positions ahead.
+template <typename WT, typename VT, int K, bool ALLACT, class RING, bool CMP = false, bool BIG = false>
 __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
                                         HullCT<VT> TN, VT nV, RING rg, uint32_t* logs,
                                         int32_t* logn, VT* ebuf0, VT* ebuf1,
@@ -556,6 +614,8 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
     // support row (positions known a row ahead, so the loads overlap the shuffle).  A line is
     // (intercept b_s, s).  eo = e_m(j) (the running row value), op = opt_m(j).
     int f[K], b[K], op[K], cnt[K], hi[K];
+    uint32_t uw[K];   // BIG: the unary log's current word and its used bits
+    int ub[K];
     rg.begin_pass(p.wg + (size_t)blockIdx.x * p.wgb, N, M, ps, L);
     VT eo[K];
     Line<VT> B0[K], F0[K];
@@ -568,10 +628,12 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       f[k] = 0;
       b[k] = 0;
       eo[k] = 0;   // e_m(0) = 0 (reading R1)
-      op[k] = 1;   // opt_m(1) = 1 whatever the row type: logged up front
-      cnt[k] = 1;
+      op[k] = BIG ? 0 : 1;   // opt_m(1) = 1 whatever the row type: logged up front (BIG: the
+      cnt[k] = BIG ? 0 : 1;  // unary stream starts from opt = 0)
+      uw[k] = 0;
+      ub[k] = 0;
       lg[k] = logs + (size_t)(ps * L + 32 * k + lane) * LC;
-      if (act[k]) lg[k][0] = (1u << 16) | 1u;
+      if (!BIG && act[k]) lg[k][0] = (1u << 16) | 1u;
       // the deque starts with a dummy line of value +inf at every query: the first push pops
       // it from the front, so the deque is never empty at a push
       B0[k] = F0[k] = Line<VT>{hull_inf<VT>(), 0};
@@ -692,6 +754,10 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
             L2[k] = rg.ldh(k, b[k] - 2, hi[k]);
             G1[k] = rg.ldh(k, f[k] + 1, hi[k]);
             G2[k] = rg.ldh(k, f[k] + 2, hi[k]);
+            if constexpr (BIG) {   // the front walks a global array: pull it into L2 ahead
+              const int q = f[k] + 16;
+              if (act[k] & (q <= hi[k] - RING::window(k))) prefetch_l2(rg.gaddr(k, q));
+            }
           }
         } else {
 #pragma unroll
@@ -831,7 +897,23 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
         for (int k = 0; k < K; ++k) {
           eo[k] = v0[k];
           const int nop = F0[k].s;
-          if (act[k] & (nop != op[k])) {
+          if constexpr (BIG) {
+            if (act[k]) {   // unary: nop - op zeros, then a one (<= 2N bits: never full)
+              int t = ub[k] + (nop - op[k]);
+              while (t >= 32) {
+                lg[k][cnt[k]++] = uw[k];
+                uw[k] = 0;
+                t -= 32;
+              }
+              uw[k] |= 1u << t;
+              ub[k] = t + 1;
+              if (ub[k] == 32) {
+                lg[k][cnt[k]++] = uw[k];
+                uw[k] = 0;
+                ub[k] = 0;
+              }
+            }
+          } else if (act[k] & (nop != op[k])) {
             lg[k][cnt[k]] = ((uint32_t)j << 16) | (uint32_t)nop;   // < LC: checked per chunk
             ++cnt[k];
           }
@@ -853,7 +935,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       evbase += nev;
       bool full = false;
 #pragma unroll
-      for (int k = 0; k < K; ++k) full |= (LC <= N) & (cnt[k] > LC - 33);   // 32 rows of headroom
+      for (int k = 0; k < K; ++k) full |= !BIG & (LC <= N) & (cnt[k] > LC - 33);   // 32 rows of headroom
       logfull = __any_sync(FULL, full);
       if (__any_sync(FULL, ovf) || logfull) {
         ovf = true;
@@ -865,6 +947,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (!act[k]) continue;
+        if (BIG && ub[k] > 0) lg[k][cnt[k]++] = uw[k];   // the unary log's last word
         // stats: pushes (support rows, less trimmed lines) = back pops + b; front pops = f - 1
         pops_e += (unsigned)(evbase - b[k]) + (unsigned)(f[k] - 1);
         const int mk = ps * L + 32 * k + lane + 1;
@@ -1118,7 +1201,7 @@ __device__ __forceinline__ bool hull_dp_skew(const HullParams& p, const WT* __re
 }
 
 // dispatch to the compact-list walk (sparse rows) or the row scan (CMP: compile-time)
-template <typename WT, typename VT, int K, bool ALLACT, class RING>
+template <typename WT, typename VT, int K, bool ALLACT, class RING, bool BIG = false>
 __device__ __forceinline__ bool hull_dp_any(const HullParams& p, const WT* __restrict__ we, int e,
                                             HullCT<VT> TN, VT nV, RING rg, uint32_t* logs,
                                             int32_t* logn, VT* ebuf0, VT* ebuf1, unsigned& pops_e,
@@ -1126,12 +1209,12 @@ __device__ __forceinline__ bool hull_dp_any(const HullParams& p, const WT* __res
                                             const int2* klist, const SplitSync* ss = nullptr,
                                             int ps_only = -1) {
   if (kc >= 0)
-    return hull_dp<WT, VT, K, ALLACT, RING, true>(p, we, e, TN, nV, rg, logs, logn, ebuf0, ebuf1,
-                                                  pops_e, ev_e, logfull, stage, kc, klist, ss,
-                                                  ps_only);
-  return hull_dp<WT, VT, K, ALLACT, RING, false>(p, we, e, TN, nV, rg, logs, logn, ebuf0, ebuf1,
-                                                 pops_e, ev_e, logfull, stage, -1, nullptr, ss,
-                                                 ps_only);
+    return hull_dp<WT, VT, K, ALLACT, RING, true, BIG>(p, we, e, TN, nV, rg, logs, logn, ebuf0,
+                                                       ebuf1, pops_e, ev_e, logfull, stage, kc,
+                                                       klist, ss, ps_only);
+  return hull_dp<WT, VT, K, ALLACT, RING, false, BIG>(p, we, e, TN, nV, rg, logs, logn, ebuf0,
+                                                      ebuf1, pops_e, ev_e, logfull, stage, -1,
+                                                      nullptr, ss, ps_only);
 }
 
 // a7: V_0..V_M for fp64 weights as the definitional cost sum_t w_t (t - l(t; C_m)) of the
@@ -1192,17 +1275,18 @@ __device__ __forceinline__ void hull_cbb_f64(const HullParams& p, int e, int tfi
 #endif
 // one layer per lane (M <= 32, K = 1) on int32 rows: cap the registers at 128 so that 16 warps
 // fit an SM (the ring allows 18); the other instantiations are shared-memory bound
-template <typename WT, int K, typename VT>
+template <typename WT, int K, typename VT, bool BIG = false>
 __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL_MINB)
     dp_hull_kernel(HullParams p) {
   constexpr bool F64 = std::is_same<VT, double>::value;
   constexpr bool WIDE = std::is_same<VT, long long>::value;
+  static_assert(!BIG || std::is_same<VT, int>::value, "the large-hull mode is an int32 mode");
   const int lane = threadIdx.x;
   extern __shared__ __align__(16) uint8_t sring[];   // ring_bytes<K, VT>() | row stage
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sring);
   VT* stage = reinterpret_cast<VT*>(sring + ring_bytes<K, VT>());
   using SR = typename std::conditional<std::is_same<VT, int>::value,
-                                       WRing<int, SRingI<HC0, HC1>>,
+                                       WRing<int, SRingI<HC0, HC1>, BIG>,
                                        WRing<VT, SRingW<VT, WC, WC>>>::type;
   SR srg;
   if constexpr (sizeof(VT) == 8) {
@@ -1216,8 +1300,14 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
   sp_dp_stats* stats = reinterpret_cast<sp_dp_stats*>(p.ws);
   unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
   unsigned* wide_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_WIDE_COUNT_OFF);
-  unsigned* ectr = reinterpret_cast<unsigned*>(p.ws + (WIDE ? SP_WS_WIDE_CTR_OFF : SP_WS_ENTRY_CTR_OFF));
-  const int n_items = WIDE ? (int)*reinterpret_cast<volatile unsigned*>(wide_n) : p.E;
+  unsigned* big_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_BIG_COUNT_OFF);
+  unsigned* ectr = reinterpret_cast<unsigned*>(
+      p.ws + (WIDE ? SP_WS_WIDE_CTR_OFF : BIG ? SP_WS_BIG_CTR_OFF : SP_WS_ENTRY_CTR_OFF));
+  const int n_items = WIDE ? (int)*reinterpret_cast<volatile unsigned*>(wide_n)
+                      : BIG ? (int)*reinterpret_cast<volatile unsigned*>(big_n) : p.E;
+  // the large-hull list shares the int64 list's array, filled from its end
+  const int LC = p.logcap;
+  const bool big_ok = !F64 && !WIDE && p.M <= 64 && !p.fpos && LC >= (2 * p.N + 31) / 32 + 2;
   uint8_t* slot = p.slots + (size_t)blockIdx.x * p.slot;
   uint32_t* logs = reinterpret_cast<uint32_t*>(slot);
   int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
@@ -1235,7 +1325,7 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
     if (lane == 0) it = (int)atomicAdd(ectr, 1u);
     it = __shfl_sync(FULL, it, 0);
     if (it >= n_items) break;
-    const int e = WIDE ? p.wide[it] : (p.order ? p.order[it] : it);
+    const int e = WIDE ? p.wide[it] : BIG ? p.wide[p.E - 1 - it] : (p.order ? p.order[it] : it);
     const WT* we = reinterpret_cast<const WT*>(p.w) + (int64_t)e * (N + 1);
 
     // ---- a3 pre-pass: n = P_N, T_N, first non-zero bin, sign / size guards ---------------
@@ -1297,10 +1387,12 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tfirst = min(tfirst, __shfl_xor_sync(FULL, tfirst, o));
       }
-      // int32 path: 2 n N < 2^31 (the D&C kernel's "narrow" condition: every intercept,
-      // candidate and difference exact in int32); int64 path: n N < 2^46 (differences < 2^46,
-      // cross products < 2^62); otherwise (or negative counts) the D&C kernel
-      const bool narrow = !bad && n < (1ll << 30) / N;
+      // int32 path: n N + T_N < 2^31 -- every intercept b_s = e_{m-1}(s-1) + s P_{s-1} and every
+      // value lies in [-T_N, n N] and every difference and query value within n N + T_N of 0, so
+      // all are exact in int32 (e.g. all-ones rows at N = 32768: 2^30 + 2^29); int64 path:
+      // n N < 2^46 (differences < 2^46, cross products < 2^62); otherwise (or negative counts)
+      // the D&C kernel
+      const bool narrow = !bad && n * (long long)N + tn < (1ll << 31);
       const bool wide_ok = !bad && n < (1ll << 46) / N;
       if (!WIDE && !narrow) {
         if (lane == 0) {
@@ -1321,7 +1413,14 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
     bool logfull = false;
     const bool fullm = M % (32 * K) == 0;
     bool ovf;
-    if constexpr (std::is_same<VT, int>::value) {
+    if constexpr (BIG) {
+      ovf = fullm ? hull_dp_any<WT, VT, K, true, SR, true>(p, we, e, TN, nV, srg, logs, logn, ebuf0,
+                                                           ebuf1, pops_e, ev_e, logfull, stage,
+                                                           kcomp, klist)
+                  : hull_dp_any<WT, VT, K, false, SR, true>(p, we, e, TN, nV, srg, logs, logn,
+                                                            ebuf0, ebuf1, pops_e, ev_e, logfull,
+                                                            stage, kcomp, klist);
+    } else if constexpr (std::is_same<VT, int>::value) {
       // int32: plain shared rings first (W5: 16 of 16384 entries outgrow them); an entry whose
       // hull outgrows a ring is re-run at once with the windowed ring (the same window plus
       // global arrays of WSMALL lines)
@@ -1359,8 +1458,10 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
       // int32: a shared ring or a log filled -- the int64 instantiation (windowed rings, exact
       // for narrow entries too) re-runs the entry; int64 / fp64: a global array or a log
       // filled -- the D&C kernel
+      // (int32 entries go to the large-hull mode when it applies: it never fills a log)
       if (lane == 0) {
-        if (!WIDE && !F64) p.wide[atomicAdd(wide_n, 1u)] = e;
+        if (!WIDE && !F64 && !BIG && big_ok) p.wide[p.E - 1 - (int)atomicAdd(big_n, 1u)] = e;
+        else if (!WIDE && !F64 && !BIG) p.wide[atomicAdd(wide_n, 1u)] = e;
         else p.fb[atomicAdd(fb_n, 1u)] = e;
       }
       continue;
@@ -1372,13 +1473,20 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
     {
       int32_t* out = p.pos + (int64_t)e * M;
       uint32_t* slog = reinterpret_cast<uint32_t*>(sring);   // the rings are free now
-      const bool in_smem = logs_to_smem(logs, logn, M, hull_log_cap(N), slog,
-                                        (int)(ring_bytes<K, VT>() / 4));
+      const bool in_smem = !BIG && logs_to_smem(logs, logn, M, hull_log_cap(N), slog,
+                                                (int)(ring_bytes<K, VT>() / 4));
       int k = 0, j = N, m = M;
+      int rk = (int)ev_e;   // BIG: support rows <= j (every support row was stepped)
       while (m > 0 && j >= tfirst) {   // P_j > 0  <=>  j >= first non-zero bin
         const int ls = hull_layer_slot(K, m);
-        const int s = in_smem ? log_lookup_smem(slog, M, m, j)
-                              : log_lookup_warp(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
+        int s;
+        if constexpr (BIG) {
+          s = unary_lookup_warp(logs + (size_t)ls * hull_log_cap(N), logn[ls], rk);
+          rk -= count_support_warp(we, s, j);   // support rows in (s - 1, j]
+        } else {
+          s = in_smem ? log_lookup_smem(slog, M, m, j)
+                      : log_lookup_warp(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
+        }
         if (lane == 0) out[k] = s;
         ++k;
         j = s - 1;
@@ -1444,6 +1552,7 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
     atomicAdd(F64 ? &stats->entries_f64 : WIDE ? &stats->entries_i64 : &stats->entries_i32,
               (unsigned long long)done_entries);
     atomicAdd(&stats->hull_event_rows, events);
+    if (BIG) atomicAdd(&stats->entries_hull_big, (unsigned long long)done_entries);
   }
 #ifdef SP_HULL_TAIL
   if (!WIDE && lane == 0) {
@@ -1771,9 +1880,9 @@ __device__ __forceinline__ void hull_backtrack(const HullParams& p, int e, int t
 // layers of pass w of the K = 1 lockstep DP, chained through a shared-memory ring (SplitSync).
 // For batches with few entries per resident warp (a GPU's share at 8-way strong scaling: 2048
 // W5 entries on 1776 warps) an entry's time halves, and the largest-first order has twice the
-// work items to balance.  Entries that overflow a ring or a log go to the int64 instantiation
-// (launched after, exact for them too); entries beyond the int32 guard likewise, bad rows to the
-// D&C kernel.
+// work items to balance.  Entries that overflow a ring or a log go to the large-hull mode
+// (dp_hull_kernel<.., int, BIG>, launched after); entries beyond the int32 guard to the int64
+// instantiation, bad rows to the D&C kernel.
 template <typename WT>
 __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
   const int lane = lane_id(), w = warp_id();
@@ -1792,6 +1901,8 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
   unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
   unsigned* wide_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_WIDE_COUNT_OFF);
   unsigned* ectr = reinterpret_cast<unsigned*>(p.ws + SP_WS_ENTRY_CTR_OFF);
+  unsigned* big_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_BIG_COUNT_OFF);
+  const bool big_ok = !p.fpos && p.logcap >= (2 * N + 31) / 32 + 2;
   uint8_t* slot = p.slots + (size_t)blockIdx.x * p.slot;
   uint32_t* logs = reinterpret_cast<uint32_t*>(slot);
   int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
@@ -1812,7 +1923,7 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
     if (it >= p.E) break;
     const int e = p.order ? p.order[it] : it;
     const HullRowStat rs = p.rstat[e];
-    if (rs.bad || rs.n >= (1ll << 30) / N) {   // int32 guard: 2 n N < 2^31
+    if (rs.bad || rs.n * (long long)N + rs.tn >= (1ll << 31)) {   // int32 guard (dp_hull_kernel)
       if (threadIdx.x == 0) {
         if (!rs.bad && rs.n < (1ll << 46) / N) p.wide[atomicAdd(wide_n, 1u)] = e;
         else p.fb[atomicAdd(fb_n, 1u)] = e;
@@ -1833,8 +1944,11 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
       hull_dp_any<WT, int, 1, false>(p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0,
                                  pops_e, ev_e, logfull, stage, kcomp, klist, &ss, w);
     __syncthreads();
-    if (s_abort) {   // ring or log full in either warp: the int64 instantiation re-runs it
-      if (threadIdx.x == 0) p.wide[atomicAdd(wide_n, 1u)] = e;
+    if (s_abort) {   // ring or log full in either warp: the large-hull mode (else the int64
+      if (threadIdx.x == 0) {   // instantiation) re-runs it
+        if (big_ok) p.wide[p.E - 1 - (int)atomicAdd(big_n, 1u)] = e;
+        else p.wide[atomicAdd(wide_n, 1u)] = e;
+      }
       continue;
     }
     pops += pops_e;
@@ -2049,6 +2163,13 @@ static int hull_grid_t(int E) {
   const int occ = occ_cached(dp_hull_kernel<WT, K, VT>, hull_dyn_bytes<K, VT>(), cache);
   return clamp_grid((long)dev_sms() * occ, E);
 }
+// the int32 large-hull mode (same shared memory as the int32 kernel)
+template <typename WT, int K>
+static int big_grid_t(int E) {
+  static int cache[HULL_MAX_DEV] = {0};
+  const int occ = occ_cached(dp_hull_kernel<WT, K, int, true>, hull_dyn_bytes<K, int>(), cache);
+  return clamp_grid((long)dev_sms() * occ, E);
+}
 
 constexpr size_t split_smem_bytes() {
   return 2 * (size_t)HC0 * 192 + SPLIT_RING * sizeof(int) + 2 * stage_bytes<int>();
@@ -2109,6 +2230,15 @@ static void hull_launch_t(HullParams p, const HullRowStat* rstat, int gn, cudaSt
     } else {
       const int gl = std::min(gn, lean_grid_t<WT, K>(p.E));
       dp_lean_kernel<WT, K><<<gl, 32, lean_smem_bytes<K>(), st>>>(p, rstat);
+    }
+    // the large-hull mode on its listed entries (int32 entries whose hull outgrew the rings or
+    // whose change log filled; exits at once when the list is empty): its grid is clamped to the
+    // slots and to the regions of big-capacity arrays the pool holds
+    if (p.M <= 64 && !p.fpos) {
+      p.wgb = wring_pass_bytes_t<int, true>(p.N, p.M);
+      const long regions = (long)(sp_hull_wg_bytes(p.E, p.N, p.M) / p.wgb);
+      const int gb = (int)std::min<long>(std::min(gn, big_grid_t<WT, K>(p.E)), regions);
+      if (gb >= 1) dp_hull_kernel<WT, K, int, true><<<gb, 32, hull_dyn_bytes<K, int>(), st>>>(p);
     }
     // the int64 instantiation on the listed entries (its warps exit at once if the list is
     // empty); its grid is clamped to the slots allocated for the widest launch

@@ -11,8 +11,11 @@
 #define SP_WS_ENTRY_CTR_OFF 200   // unsigned: next entry for the hull kernel's warps
 #define SP_WS_WIDE_COUNT_OFF 216  // unsigned: entries listed for the int64 hull instantiation
 #define SP_WS_WIDE_CTR_OFF 220    // unsigned: next listed entry for the int64 instantiation
+#define SP_WS_BIG_COUNT_OFF 224   // unsigned: entries listed for the int32 large-hull mode
+#define SP_WS_BIG_CTR_OFF 228     // unsigned: next listed entry for the large-hull mode
 
-// Workspace after the head:  fallback list int32[E] | int64-path list int32[E] | windowed rings' global arrays (int64 / fp64 instantiations)
+// Workspace after the head:  fallback list int32[E] | int64-path list int32[E] (the large-hull
+// list fills the same array from its end) | windowed rings' global arrays (int64 / fp64 instantiations)
 // | ordering scratch (support counts, radix sort) | hull slots | D&C slots
 // (each 256-B aligned)
 int sp_hull_grid(int E, int N, int M, int wtype);

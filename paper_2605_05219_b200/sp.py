@@ -159,9 +159,10 @@ SP_WS_STATS_BYTES = 256
 
 def dp_stats(workspace) -> dict:
     """Launch statistics from the head of a DP workspace (sp_dp_stats; synchronises)."""
-    v = workspace[:56].view(torch.int64).cpu().tolist()
+    v = workspace[:64].view(torch.int64).cpu().tolist()
     return {"evaluations": v[0], "entries_i32": v[1], "entries_i64": v[2], "entries_f64": v[3],
-            "hull_pops": v[4], "entries_hull": v[5], "hull_event_rows": v[6]}
+            "hull_pops": v[4], "entries_hull": v[5], "hull_event_rows": v[6],
+            "entries_hull_big": v[7]}
 
 
 def place_checkpoints(weights, M, positions=None, n_positions=None, cost=None,

@@ -97,29 +97,55 @@ def test_hull_sparse_ties_and_plateaus(dev):
 
 
 def test_hull_overflow_falls_back_exactly(dev):
-    """Uniform mass: the layer-1 hull holds ~N/2 lines and opt changes every other row.  At
-    N = 1000 the hull outgrows the shared ring but fits a global overflow ring (solved by the
-    hull kernel on its retry); at N = 3000 its argmin log fills too (capacity max(1024, N/8))
-    and the D&C kernel solves it.  Mixed in one batch with dense entries, an int64-range entry
+    """Uniform mass: the layer-1 hull holds ~N/2 lines and opt changes every other row, so the
+    hull outgrows the shared rings (and the int32 retry's 256-line arrays) and, at N = 3000, a
+    change log of max(1024, N/8) entries would fill too: the int32 large-hull mode (unary logs,
+    big global arrays) solves both.  Mixed in one batch with dense entries, an int64-range entry
     (int64 hull instantiation) and a bad entry (D&C)."""
     M = 40
-    for N, uniform_on_hull in ((1000, True), (3000, False)):
+    for N in (1000, 3000):
         H = dense(8, N, seed=1).astype(np.int64)
         H[2, 1:] = 1
         H[5, 1:] = 3
-        H[6] *= (2 ** 31 // N) // max(1, H[6].sum()) + 1   # 2 n N >= 2^31: int64 instantiation
-        assert H[6].sum() * N * 2 >= 2 ** 31
+        H[6] *= (2 ** 31 // N) // max(1, H[6].sum()) + 1   # n N + T_N >= 2^31: int64 instantiation
+        assert H[6].sum() * N >= 2 ** 31 // 2
         r = place(H, M, dev, dtype=torch.int64)
-        assert r["stats"]["entries_hull"] == (8 if uniform_on_hull else 6)
-        # the int64 entry, plus -- in SPLIT mode (small batches) -- the ring-overflow entries,
-        # which SPLIT hands to the int64 instantiation (its larger rings / global ring)
-        assert r["stats"]["entries_i64"] in ((1, 3) if uniform_on_hull else (1,))
+        assert r["stats"]["entries_hull"] == 8
+        assert r["stats"]["entries_hull_big"] == 2
+        assert r["stats"]["entries_i64"] == 1
+        assert r["stats"]["evaluations"] == 0
         check(H, M, r)
         Hb = H.copy()
         Hb[3, 9] = -1
         r = place(Hb, M, dev, dtype=torch.int64)
         assert r["npos"][3] == -sp.SP_ERR_BAD_ARGUMENT
         check(Hb, M, r, rows=[0, 1, 2, 4, 5, 6, 7])
+
+
+@pytest.mark.parametrize("N,M,E", [(2048, 16, 6), (4096, 33, 6), (4096, 64, 40), (32768, 64, 5)])
+def test_hull_large_hull_mode(dev, N, M, E):
+    """Full-support rows -- all-ones (Thm 1's uniform law; n N + T_N < 2^31 keeps N = 32768 on
+    the int32 path) and near-uniform noise in {1, 2, 3} -- have hulls of ~N/(m+1) lines and an
+    argmin that moves on most rows: the int32 large-hull mode solves them (no D&C), next to
+    sparse W5-like rows on the ordinary kernel; positions, counts, V_M and V_0..V_M against the
+    oracle's CHT.  E = 40 runs the one-warp kernel's hand-off, E <= 6 SPLIT's (M > 32)."""
+    rng = np.random.default_rng(N + M)
+    H = dense(E, N, seed=N + M, lo=N // 8, hi=N // 4).astype(np.int64)
+    big = list(range(0, E, 2))
+    for e in big:
+        H[e, 1:] = 1 if e % 4 == 0 else rng.integers(1, 4, N)
+    for dtype in (torch.int32, torch.int64):
+        r = place(H, M, dev, dtype=dtype)
+        assert r["stats"]["entries_hull"] == E
+        # (a noise row's hull may still fit the int32 retry's arrays at small N)
+        assert 1 <= r["stats"]["entries_hull_big"] <= len(big)
+        assert r["stats"]["evaluations"] == 0
+        check(H, M, r)
+    # Thm 1 (P:211-226): under the uniform law the balanced spacing is optimal -- its cost
+    # equals V_M of the all-ones row
+    bpos, bnpos, _ = sp.baseline_sets(N, budgets=(M,), blocks=(), device=dev)
+    bc, _ = sp.expected_recompute(torch.ones(1, N + 1, dtype=torch.int32, device=dev), bpos, bnpos)
+    assert int(bc[0, 0]) == int(r["cost"][0])
 
 
 def test_hull_matches_dc_kernel_w5_rows(dev):

@@ -90,7 +90,8 @@ def main():
     for m in ms:
         add("dp", m, fn[:, m - 1].sum().item(), cbb[:, m].sum().item())
     base = [("balanced", m, sp.balanced_positions(N, m)) for m in ms]
-    base += [("logarithmic", m, sp.log_positions(N, m)) for m in ms]
+    # (the logarithmic schedule's 2^M - 1 denominator: M <= 62, sp_log_positions)
+    base += [("logarithmic", m, sp.log_positions(N, m)) for m in ms if m <= 62]
     base += [("sqrt", len(sp.sqrt_positions(N)), sp.sqrt_positions(N))]
     base += [("block", B, sp.block_positions(N, B)) for B in map(int, a.blocks.split(","))]
     pos, npos = pack([s for _, _, s in base], dev)

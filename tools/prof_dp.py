@@ -17,6 +17,7 @@ ap.add_argument("--M", type=int, default=None)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--lcp", action="store_true")
 ap.add_argument("--plus1", action="store_true", help="add 1 to every bin (full support, K = N)")
+ap.add_argument("--ones", action="store_true", help="all-ones rows (the large-hull mode)")
 ap.add_argument("--dense-n", type=int, nargs=2, default=None, help="draws per entry (lo hi)")
 ap.add_argument("--no-hull", action="store_true", help="D&C kernel only (SP_NO_HULL)")
 ap.add_argument("--f64", action="store_true", help="fp64 weights w = c / n (a7)")
@@ -30,7 +31,7 @@ if a.no_hull:
     os.environ["SP_NO_HULL"] = "1"
 M = a.M or cfg.M
 dev = torch.device("cuda:0")
-H = wl.make_dense_hist(cfg, seed=0, device=dev) if cfg.dense_n else wl.uniform_hist(a.entries, cfg.N, dev)
+H = wl.make_dense_hist(cfg, seed=0, device=dev) if cfg.dense_n and not a.ones else wl.uniform_hist(a.entries, cfg.N, dev)
 if a.plus1:
     H[:, 1:] += 1
 if a.sort_support:
@@ -48,7 +49,7 @@ for r in range(a.reps):
     print(f"dp rep {r}: {s.elapsed_time(e):.3f} ms  cells={a.entries*cfg.N*M:.3e} "
           f"evals/cell={st['evaluations']/(a.entries*cfg.N*M):.2f}  "
           f"Mcells/s={a.entries*cfg.N*M/s.elapsed_time(e)/1e3:.1f}  "
-          f"hull={st['entries_hull']} support_rows/entry={st['hull_event_rows']/max(1,st['entries_hull']):.0f} "
+          f"hull={st['entries_hull']} big={st['entries_hull_big']} support_rows/entry={st['hull_event_rows']/max(1,st['entries_hull']):.0f} "
           f"pops/support-cell={st['hull_pops']/max(1,st['hull_event_rows']*M):.3f}", flush=True)
 if os.environ.get("SP_TAIL_REPORT"):   # needs SP_NVCC_EXTRA=-DSP_HULL_TAIL; last rep
     v = ws[:128].view(torch.int64).cpu().tolist()

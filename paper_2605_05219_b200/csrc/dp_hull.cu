@@ -145,6 +145,7 @@ struct HullParams {
   int logcap;             // argmin-log entries usable per layer (hull_log_cap(N); tests lower it)
   const HullRowStat* rstat;   // n, T_N, first bin, guards per entry (integer weights), or NULL
   const int2* sparse;         // [E][HULL_KC] compacted support rows (valid when rstat[e].K <= HULL_KC)
+  int fwd;                    // the large-hull mode ran: the int64 list is its forwarded list
 };
 
 // Global capacity (lines, a power of two) of layer m's windowed ring: ~1.125x the hull size of
@@ -599,6 +600,13 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
   const int lane = lane_id();
   const int N = p.N, M = p.M;
   const int LC = p.logcap;   // <= hull_log_cap(N), the allocated stride
+  // the two lines above the front loaded a row ahead, the front prefetched into L2: the
+  // large-hull mode, and (SP_HULL_AHEAD_WIDE) the int64 / fp64 windowed instantiations
+#ifdef SP_HULL_AHEAD_WIDE
+  constexpr bool AHEAD = BIG || (RING::kWindowed && sizeof(VT) == 8);
+#else
+  constexpr bool AHEAD = BIG;
+#endif
   logfull = false;
   constexpr int L = 32 * K;
   const int passes = (M + L - 1) / L;
@@ -642,6 +650,9 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
     }
     VT carry = 0, Pm1 = 0;
     hdd carry_dd{0.0, 0.0};
+    Line<VT> NG1[K], NG2[K];   // BIG: lines f + 1, f + 2 for the next row
+#pragma unroll
+    for (int k = 0; k < K; ++k) NG1[k] = NG2[k] = Line<VT>{hull_inf<VT>(), 0};
     int evbase = 0;   // support rows (c_j > 0) before this chunk = index into the e-row buffers
     // the counts are loaded HULL_PF chunks (32 rows each) ahead: a chunk of W5's rows holds ~5
     // support rows, but sparse rows (W2/W3: ~0.2-2% support) would otherwise wait for HBM on
@@ -752,11 +763,14 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           for (int k = 0; k < K; ++k) {
             L1[k] = rg.ldh(k, b[k] - 1, hi[k]);
             L2[k] = rg.ldh(k, b[k] - 2, hi[k]);
-            G1[k] = rg.ldh(k, f[k] + 1, hi[k]);
-            G2[k] = rg.ldh(k, f[k] + 2, hi[k]);
-            if constexpr (BIG) {   // the front walks a global array: pull it into L2 ahead
+            if constexpr (AHEAD) {   // loaded a row ahead (below); the front walks a global array:
+              G1[k] = NG1[k];      // pull it into L2 further ahead
+              G2[k] = NG2[k];
               const int q = f[k] + 16;
               if (act[k] & (q <= hi[k] - RING::window(k))) prefetch_l2(rg.gaddr(k, q));
+            } else {
+              G1[k] = rg.ldh(k, f[k] + 1, hi[k]);
+              G2[k] = rg.ldh(k, f[k] + 2, hi[k]);
             }
           }
         } else {
@@ -764,8 +778,8 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           for (int k = 0; k < K; ++k) {
             L1[k] = rg.ldw(k, b[k] - 1);
             L2[k] = rg.ldw(k, b[k] - 2);
-            G1[k] = rg.ldw(k, f[k] + 1);
-            G2[k] = rg.ldw(k, f[k] + 2);
+            G1[k] = AHEAD ? NG1[k] : rg.ldw(k, f[k] + 1);
+            G2[k] = AHEAD ? NG2[k] : rg.ldw(k, f[k] + 2);
           }
         }
         // e_{m-1}(j-1): from the lane below (its value at the previous support row);
@@ -892,6 +906,13 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           }
         }
         Pm1 = Pj;
+        if constexpr (AHEAD) {   // the next row's two lines above the front, a row ahead: a front in
+#pragma unroll                 // the global array then has a whole row to arrive (the only writes
+          for (int k = 0; k < K; ++k) {   // before their use are covered by the d <= 2 selects)
+            NG1[k] = rg.ldh(k, f[k] + 1, hi[k]);
+            NG2[k] = rg.ldh(k, f[k] + 2, hi[k]);
+          }
+        }
         // ---- row value, argmin change log ---------------------------------------------------
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -1275,8 +1296,12 @@ __device__ __forceinline__ void hull_cbb_f64(const HullParams& p, int e, int tfi
 #endif
 // one layer per lane (M <= 32, K = 1) on int32 rows: cap the registers at 128 so that 16 warps
 // fit an SM (the ring allows 18); the other instantiations are shared-memory bound
+#ifndef SP_HULL_BIG_MINB
+#define SP_HULL_BIG_MINB 1
+#endif
 template <typename WT, int K, typename VT, bool BIG = false>
-__global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL_MINB)
+__global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
+                                          : (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL_MINB)
     dp_hull_kernel(HullParams p) {
   constexpr bool F64 = std::is_same<VT, double>::value;
   constexpr bool WIDE = std::is_same<VT, long long>::value;
@@ -1303,11 +1328,14 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
   unsigned* big_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_BIG_COUNT_OFF);
   unsigned* ectr = reinterpret_cast<unsigned*>(
       p.ws + (WIDE ? SP_WS_WIDE_CTR_OFF : BIG ? SP_WS_BIG_CTR_OFF : SP_WS_ENTRY_CTR_OFF));
-  const int n_items = WIDE ? (int)*reinterpret_cast<volatile unsigned*>(wide_n)
-                      : BIG ? (int)*reinterpret_cast<volatile unsigned*>(big_n) : p.E;
-  // the large-hull list shares the int64 list's array, filled from its end
-  const int LC = p.logcap;
-  const bool big_ok = !F64 && !WIDE && p.M <= 64 && !p.fpos && LC >= (2 * p.N + 31) / 32 + 2;
+  // Lists: the int32 kernel hands what it cannot solve to the int64 list (p.wide from the front);
+  // when the large-hull mode runs (p.fwd) it takes that list and forwards the entries beyond its
+  // own guard to the int64 instantiation through the same array's back (SP_WS_BIG_COUNT_OFF).
+  // (The int32 kernel's hot loop is sensitive to any code around it -- routing there cost 2% on
+  // W5 -- so the hand-offs live in the other two instantiations.)
+  const bool from_fwd = WIDE && p.fwd;
+  const int n_items = (WIDE && !from_fwd) || BIG ? (int)*reinterpret_cast<volatile unsigned*>(wide_n)
+                      : from_fwd ? (int)*reinterpret_cast<volatile unsigned*>(big_n) : p.E;
   uint8_t* slot = p.slots + (size_t)blockIdx.x * p.slot;
   uint32_t* logs = reinterpret_cast<uint32_t*>(slot);
   int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
@@ -1325,7 +1353,8 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
     if (lane == 0) it = (int)atomicAdd(ectr, 1u);
     it = __shfl_sync(FULL, it, 0);
     if (it >= n_items) break;
-    const int e = WIDE ? p.wide[it] : BIG ? p.wide[p.E - 1 - it] : (p.order ? p.order[it] : it);
+    const int e = from_fwd ? p.wide[p.E - 1 - it] : (WIDE || BIG) ? p.wide[it]
+                                                  : (p.order ? p.order[it] : it);
     const WT* we = reinterpret_cast<const WT*>(p.w) + (int64_t)e * (N + 1);
 
     // ---- a3 pre-pass: n = P_N, T_N, first non-zero bin, sign / size guards ---------------
@@ -1387,16 +1416,18 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tfirst = min(tfirst, __shfl_xor_sync(FULL, tfirst, o));
       }
-      // int32 path: n N + T_N < 2^31 -- every intercept b_s = e_{m-1}(s-1) + s P_{s-1} and every
-      // value lies in [-T_N, n N] and every difference and query value within n N + T_N of 0, so
-      // all are exact in int32 (e.g. all-ones rows at N = 32768: 2^30 + 2^29); int64 path:
-      // n N < 2^46 (differences < 2^46, cross products < 2^62); otherwise (or negative counts)
-      // the D&C kernel
-      const bool narrow = !bad && n * (long long)N + tn < (1ll << 31);
+      // int32 path: 2 n N < 2^31 (the D&C kernel's "narrow" condition); int64 path: n N < 2^46
+      // (differences < 2^46, cross products < 2^62); otherwise (or negative counts) the D&C
+      // kernel.  The large-hull mode takes n N + T_N < 2^31: every intercept
+      // b_s = e_{m-1}(s-1) + s P_{s-1} and every value lies in [-T_N, n N] and every difference
+      // and query value within n N + T_N of 0, so all are exact in int32 (e.g. all-ones rows at
+      // N = 32768: 2^30 + 2^29) -- heavy rows between the two guards go to it directly.
+      const bool narrow = !bad && (BIG ? n * (long long)N + tn < (1ll << 31) : n < (1ll << 30) / N);
       const bool wide_ok = !bad && n < (1ll << 46) / N;
       if (!WIDE && !narrow) {
         if (lane == 0) {
-          if (wide_ok) p.wide[atomicAdd(wide_n, 1u)] = e;
+          if (BIG && wide_ok) p.wide[p.E - 1 - (int)atomicAdd(big_n, 1u)] = e;   // forwarded
+          else if (wide_ok) p.wide[atomicAdd(wide_n, 1u)] = e;
           else p.fb[atomicAdd(fb_n, 1u)] = e;
         }
         continue;
@@ -1458,10 +1489,9 @@ __global__ void __launch_bounds__(32, (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL
       // int32: a shared ring or a log filled -- the int64 instantiation (windowed rings, exact
       // for narrow entries too) re-runs the entry; int64 / fp64: a global array or a log
       // filled -- the D&C kernel
-      // (int32 entries go to the large-hull mode when it applies: it never fills a log)
+      // (the int64 list is the large-hull mode's input when it runs: it never fills a log)
       if (lane == 0) {
-        if (!WIDE && !F64 && !BIG && big_ok) p.wide[p.E - 1 - (int)atomicAdd(big_n, 1u)] = e;
-        else if (!WIDE && !F64 && !BIG) p.wide[atomicAdd(wide_n, 1u)] = e;
+        if (!WIDE && !F64 && !BIG) p.wide[atomicAdd(wide_n, 1u)] = e;
         else p.fb[atomicAdd(fb_n, 1u)] = e;
       }
       continue;
@@ -1880,9 +1910,9 @@ __device__ __forceinline__ void hull_backtrack(const HullParams& p, int e, int t
 // layers of pass w of the K = 1 lockstep DP, chained through a shared-memory ring (SplitSync).
 // For batches with few entries per resident warp (a GPU's share at 8-way strong scaling: 2048
 // W5 entries on 1776 warps) an entry's time halves, and the largest-first order has twice the
-// work items to balance.  Entries that overflow a ring or a log go to the large-hull mode
-// (dp_hull_kernel<.., int, BIG>, launched after); entries beyond the int32 guard to the int64
-// instantiation, bad rows to the D&C kernel.
+// work items to balance.  Entries that overflow a ring or a log, and entries beyond the int32
+// guard, are listed for the large-hull mode / the int64 instantiation (launched after), bad rows
+// for the D&C kernel.
 template <typename WT>
 __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
   const int lane = lane_id(), w = warp_id();
@@ -1901,8 +1931,6 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
   unsigned* fb_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_FB_COUNT_OFF);
   unsigned* wide_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_WIDE_COUNT_OFF);
   unsigned* ectr = reinterpret_cast<unsigned*>(p.ws + SP_WS_ENTRY_CTR_OFF);
-  unsigned* big_n = reinterpret_cast<unsigned*>(p.ws + SP_WS_BIG_COUNT_OFF);
-  const bool big_ok = !p.fpos && p.logcap >= (2 * N + 31) / 32 + 2;
   uint8_t* slot = p.slots + (size_t)blockIdx.x * p.slot;
   uint32_t* logs = reinterpret_cast<uint32_t*>(slot);
   int32_t* logn = reinterpret_cast<int32_t*>(slot + hull_log_bytes(N, M));
@@ -1923,7 +1951,7 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
     if (it >= p.E) break;
     const int e = p.order ? p.order[it] : it;
     const HullRowStat rs = p.rstat[e];
-    if (rs.bad || rs.n * (long long)N + rs.tn >= (1ll << 31)) {   // int32 guard (dp_hull_kernel)
+    if (rs.bad || rs.n >= (1ll << 30) / N) {   // int32 guard: 2 n N < 2^31
       if (threadIdx.x == 0) {
         if (!rs.bad && rs.n < (1ll << 46) / N) p.wide[atomicAdd(wide_n, 1u)] = e;
         else p.fb[atomicAdd(fb_n, 1u)] = e;
@@ -1944,11 +1972,8 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
       hull_dp_any<WT, int, 1, false>(p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0,
                                  pops_e, ev_e, logfull, stage, kcomp, klist, &ss, w);
     __syncthreads();
-    if (s_abort) {   // ring or log full in either warp: the large-hull mode (else the int64
-      if (threadIdx.x == 0) {   // instantiation) re-runs it
-        if (big_ok) p.wide[p.E - 1 - (int)atomicAdd(big_n, 1u)] = e;
-        else p.wide[atomicAdd(wide_n, 1u)] = e;
-      }
+    if (s_abort) {   // ring or log full in either warp: the large-hull mode or the int64
+      if (threadIdx.x == 0) p.wide[atomicAdd(wide_n, 1u)] = e;   // instantiation re-runs it
       continue;
     }
     pops += pops_e;
@@ -2234,11 +2259,15 @@ static void hull_launch_t(HullParams p, const HullRowStat* rstat, int gn, cudaSt
     // the large-hull mode on its listed entries (int32 entries whose hull outgrew the rings or
     // whose change log filled; exits at once when the list is empty): its grid is clamped to the
     // slots and to the regions of big-capacity arrays the pool holds
-    if (p.M <= 64 && !p.fpos) {
+    p.fwd = 0;
+    if (p.M <= 64 && !p.fpos && p.logcap >= (2 * p.N + 31) / 32 + 2) {
       p.wgb = wring_pass_bytes_t<int, true>(p.N, p.M);
       const long regions = (long)(sp_hull_wg_bytes(p.E, p.N, p.M) / p.wgb);
       const int gb = (int)std::min<long>(std::min(gn, big_grid_t<WT, K>(p.E)), regions);
-      if (gb >= 1) dp_hull_kernel<WT, K, int, true><<<gb, 32, hull_dyn_bytes<K, int>(), st>>>(p);
+      if (gb >= 1) {
+        dp_hull_kernel<WT, K, int, true><<<gb, 32, hull_dyn_bytes<K, int>(), st>>>(p);
+        p.fwd = 1;
+      }
     }
     // the int64 instantiation on the listed entries (its warps exit at once if the list is
     // empty); its grid is clamped to the slots allocated for the widest launch
@@ -2306,6 +2335,7 @@ cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, 
   const int logcap_env = sp_debug_get(SP_DBG_HULL_LOGCAP);   // test hook: force the log-full fallback
   sp::HullParams p;
   p.order = nullptr;
+  p.fwd = 0;
   const size_t a = sp::hull_align(4 * (size_t)E);
   int32_t* kin = (int32_t*)order_ws;
   int32_t* vin = (int32_t*)(order_ws + a);

@@ -26,8 +26,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DP cells/s (entries*N*M)"
-TRAFFIC_JSON = "r02d_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
-PIPES_JSON = "r02d_ncu_pipes.json"       # the same capture: issue / ALU / FMA / LSU pipe %
+TRAFFIC_JSON = "r02e_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
+PIPES_JSON = "r02e_ncu_pipes.json"       # the same capture: issue / ALU / FMA / LSU pipe %
 
 
 def dp_update_cost():
@@ -52,6 +52,15 @@ def dp_update_cost():
                     "lsu": round(lsu, 3)},
             "rates": rates, "clk_per_update_per_sm": t[binding], "binding": binding}
 UNIT = "cells/s"
+
+
+def _kget(d, prefix):
+    """The entry of a per-kernel ncu summary for the int32 hull kernel, whatever the spelling of
+    its trailing template arguments (", 0>" / ", false>" / ">")."""
+    for k in (prefix + ">", prefix + ", 0>", prefix + ", false>"):
+        if k in d:
+            return d[k]
+    return {}
 
 
 def parse():
@@ -702,7 +711,7 @@ def run_ours(args):
         "roofline": {"bound": "alu", "kernel": ("dp_hull_kernel<double, 2, double>" if f64 else
                                                          "dp_hull_kernel<int32> (dp_hull_split_kernel for < 1.5 entries per resident warp)"), "achieved": achieved,
                      "peak": peak, "unit": "Gupd/s", "frac": achieved / peak,
-                     "traffic": traffic.get("dp_hull_kernel<int, 2, int>", {}).get("traffic_bytes"),
+                     "traffic": _kget(traffic, "dp_hull_kernel<int, 2, int").get("traffic_bytes"),
                      "work": f"{updates} hull updates per launch = {stats['hull_event_rows']} "
                              f"support rows x M (support rows = {stats['hull_event_rows'] / max(1, stats['entries_hull']) / N:.3f} "
                              f"of N per entry; zero-count rows are exact no-ops); "
@@ -716,7 +725,7 @@ def run_ours(args):
                                     f"{upd['rates']}"
                                     + ("; the int32 step's peak: the fp64 step's own minimal SASS "
                                        "(DFMA / DSETP) is not derived" if f64 else "")),
-                     "pipes_ncu": pipes.get("dp_hull_kernel<int, 2, int>"),
+                     "pipes_ncu": _kget(pipes, "dp_hull_kernel<int, 2, int") or None,
                      "support_fraction": stats["hull_event_rows"] / max(1, stats["entries_hull"]) / N
                      if stats["entries_hull"] else None,
                      "support_updates_per_s": updates / dp_launch_s,
@@ -729,7 +738,7 @@ def run_ours(args):
                          "algorithmic_bytes": lcp_bytes_all / world},
         # a6: reads every histogram row once, writes E x S costs (eval_bcast_kernel for <= 4
         # broadcast sets whose l tables fit shared memory, else eval_p32_kernel)
-        "roofline_eval": {"bound": "hbm", "kernel": ("eval_kernel<double>" if f64 else
+        "roofline_eval": {"bound": "hbm", "kernel": (f"eval_bcast_f64_kernel<{S}>" if f64 else
                                                      f"eval_bcast_kernel<{S}>"
                                                      if S <= 4 and S * (N + 1 + 384) * 2 <= 200 * 1024
                                                      else "eval_p32_kernel<uint16_t, 256>"),

@@ -100,13 +100,8 @@ __host__ __device__ __forceinline__ size_t hull_log_bytes(int N, int M) {
 __host__ __device__ __forceinline__ size_t hull_cnt_bytes(int M) {
   return hull_align((size_t)hull_layers_padded(M) * 4);
 }
-// fp64 (a7) scratch: the canonical placement of every budget, int32 [M][M]
-__host__ __device__ __forceinline__ size_t hull_fscr_bytes(int M) {
-  return hull_align(4 * (size_t)M * (size_t)M);
-}
 __host__ __device__ __forceinline__ size_t hull_slot_bytes(int N, int M) {
-  return hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(8 * (size_t)(N + 1)) +
-         hull_fscr_bytes(M);
+  return hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(8 * (size_t)(N + 1));
 }
 __host__ __device__ __forceinline__ size_t hull_smem_bytes(int) { return 0; }   // static rings
 
@@ -1238,54 +1233,105 @@ __device__ __forceinline__ bool hull_dp_any(const HullParams& p, const WT* __res
                                                       nullptr, ss, ps_only);
 }
 
-// a7: V_0..V_M for fp64 weights as the definitional cost sum_t w_t (t - l(t; C_m)) of the
-// canonical placement C_m of every budget m (the frontier backtrack from the argmin logs), in
-// double-double, so that cost_by_budget meets the 1e-12 bound of SURVEY 8(c) a7 (the DP's own
-// e_m(N) carries ~m N eps P_N of absolute rounding; reading R10).  One budget per lane per pass;
-// the warp walks the row's non-zero bins once per pass.
+// a7: the definitional cost sum_t w_t (t - l(t; C)) of a placement C = {c_1 < ... < c_k} for fp64
+// weights, as T_N - sum_i c_i (P(c_{i+1} - 1) - P(c_i - 1)) (c_{k+1} = N + 1) from
+// the row's prefix sums P in double-double: O(k) lookups per placement instead of a walk over
+// the bins (round 1 walked the row once per 32 budgets with a pointer per lane: 110 ms of the
+// fp64 W5 launch).  The cancellation in T_N - sum costs ~1e-31 T_N absolute, far inside reading
+// R10's 1e-12 bound.  The prefix goes to the slot's two e-row buffers (free after the DP).
+__device__ __forceinline__ hdd hdd_neg(hdd a) { return hdd{-a.hi, -a.lo}; }
+__device__ __forceinline__ hdd hdd_mul_i(hdd a, int c) {   // a * c, c an exact small integer
+  const double p = a.hi * (double)c;
+  const double err = fma(a.hi, (double)c, -p) + a.lo * (double)c;
+  const double h = p + err;
+  return hdd{h, err - (h - p)};
+}
+// P[0..N] (P[0] = 0) into Ph / Pl; returns T_N = sum_t t w_t, both in double-double.  Blocks of
+// 1024 bins, lane l owning the 32 consecutive bins b0 + 32 l + i: a lane sums its bins (TwoSum
+// into hi, the errors into lo), one warp scan of the lane totals gives each lane its start, and a
+// second pass over the same bins (L1 hits) writes the running sums -- 32 independent chains per
+// warp instead of a dependent 5-step double-double scan per 32 bins.
+__device__ __forceinline__ void two_sum_acc(double& hi, double& lo, double x) {
+  const double s = hi + x, bb = s - hi;
+  lo += (hi - (s - bb)) + (x - bb);
+  hi = s;
+}
+__device__ __forceinline__ hdd f64_prefix_dd(const double* __restrict__ we, int N, double* Ph,
+                                             double* Pl) {
+  const int lane = lane_id();
+  hdd carry{0.0, 0.0};
+  double thi = 0.0, tlo = 0.0;
+  for (int b0 = 0; b0 <= N; b0 += 1024) {
+    const int t0 = b0 + 32 * lane;
+    double shi = 0.0, slo = 0.0;
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) {
+      const int t = t0 + i;
+      const double w = (t >= 1 && t <= N) ? we[t] : 0.0;
+      two_sum_acc(shi, slo, w);
+      const double pr = (double)t * w;
+      two_sum_acc(thi, tlo, pr);
+      tlo += fma((double)t, w, -pr);
+    }
+    const hdd tot{shi, slo};
+    hdd inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const hdd y = hdd_shfl_up(inc, o);
+      if (lane >= o) inc = hdd_add(inc, y);
+    }
+    const hdd start = hdd_add(carry, hdd_add(inc, hdd{-tot.hi, -tot.lo}));   // exclusive
+    double rhi = start.hi, rlo = start.lo;
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) {
+      const int t = t0 + i;
+      if (t > N) break;
+      const double w = t >= 1 ? we[t] : 0.0;
+      two_sum_acc(rhi, rlo, w);
+      Ph[t] = rhi;
+      Pl[t] = rlo;
+    }
+    carry = hdd_add(carry, hdd_shfl(inc, 31));
+  }
+  return hdd_warp_sum(hdd{thi, tlo});
+}
+__device__ __forceinline__ hdd f64_dP(const double* Ph, const double* Pl, int a, int b) {
+  return hdd_add(hdd{Ph[b], Pl[b]}, hdd{-Ph[a], -Pl[a]});   // P(b) - P(a), 0 <= a <= b <= N
+}
+// one placement (k ascending positions), warp-cooperative over its gaps
+__device__ __forceinline__ double f64_cost_warp(const int32_t* pos, int k, int N, hdd TN,
+                                                const double* Ph, const double* Pl) {
+  hdd acc{0.0, 0.0};
+  for (int i = lane_id(); i < k; i += 32) {
+    const int ci = pos[i], cn = i + 1 < k ? pos[i + 1] : N + 1;
+    acc = hdd_add(acc, hdd_mul_i(f64_dP(Ph, Pl, ci - 1, cn - 1), ci));
+  }
+  acc = hdd_warp_sum(acc);
+  const hdd c = hdd_add(TN, hdd_neg(acc));
+  return c.hi + c.lo;
+}
+// V_1..V_M: the canonical placement of every budget m (the frontier backtrack from the argmin
+// logs), one budget per lane; each gap's term needs two prefix lookups
 template <int K>
-__device__ __forceinline__ void hull_cbb_f64(const HullParams& p, int e, int tfirst,
-                                             const double* __restrict__ we, const uint32_t* logs,
-                                             const int32_t* logn, int32_t* fscr) {
+__device__ __forceinline__ void hull_cbb_f64(const HullParams& p, int e, int tfirst, hdd TN,
+                                             const double* Ph, const double* Pl,
+                                             const uint32_t* logs, const int32_t* logn) {
   const int lane = lane_id();
   const int N = p.N, M = p.M;
   double* cbb = reinterpret_cast<double*>(p.cbb) + (int64_t)e * (M + 1);
-  for (int g = 0; g < M; g += 32) {
-    const int mb = g + lane + 1;
-    int32_t* fo = fscr + (size_t)(mb - 1) * M;
-    int k = 0;
-    if (mb <= M) {
-      int j = N, m = mb;
-      while (m > 0 && j >= tfirst) {
-        const int ls = hull_layer_slot(K, m);
-        const int s = log_lookup_lane(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
-        fo[k++] = s;
-        j = s - 1;
-        --m;
-      }
-      for (int a = 0, z = k - 1; a < z; ++a, --z) {
-        const int t = fo[a];
-        fo[a] = fo[z];
-        fo[z] = t;
-      }
-    }
+  for (int mb = lane + 1; mb <= M; mb += 32) {
     hdd acc{0.0, 0.0};
-    int ptr = 0, l = 0;   // positions <= t so far; the largest of them
-    for (int jb = 0; jb < N; jb += 32) {
-      const double w = jb + 1 + lane <= N ? we[jb + 1 + lane] : 0.0;
-      unsigned mask = __ballot_sync(FULL, w != 0.0);
-      while (mask) {
-        const int i = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int t = jb + 1 + i;
-        const double wt = __shfl_sync(FULL, w, i);
-        if (mb <= M) {
-          while (ptr < k && fo[ptr] <= t) l = fo[ptr++];
-          acc = hdd_add(acc, hdd_prod(wt, (double)(t - l)));
-        }
-      }
+    int j = N, m = mb, cn = N + 1;
+    while (m > 0 && j >= tfirst) {   // positions from the largest down: gap [s, cn)
+      const int ls = hull_layer_slot(K, m);
+      const int s = log_lookup_lane(logs + (size_t)ls * hull_log_cap(N), logn[ls], j);
+      acc = hdd_add(acc, hdd_mul_i(f64_dP(Ph, Pl, s - 1, cn - 1), s));
+      cn = s;
+      j = s - 1;
+      --m;
     }
-    if (mb <= M) cbb[mb] = acc.hi + acc.lo;
+    const hdd c = hdd_add(TN, hdd_neg(acc));
+    cbb[mb] = c.hi + c.lo;
   }
 }
 
@@ -1534,21 +1580,21 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
       for (int q = k + lane; q < M; q += 32) out[q] = 0;
       if constexpr (F64) {
         // a7: report the definitional cost sum_t w_t (t - l(t)) of the returned placement in
-        // double-double (reading R10; the DP's own V_M carries ~M N eps P_N absolute rounding)
+        // double-double (reading R10; the DP's own V_M carries ~M N eps P_N absolute rounding),
+        // from the row's double-double prefix sums (e-row buffers: free after the DP)
         __syncwarp();
-        hdd acc{0.0, 0.0};
-        int ptr = 0;   // positions <= t (t increases per lane)
-        for (int t = lane + 1; t <= N; t += 32) {
-          while (ptr < k && out[ptr] <= t) ++ptr;
-          const double wt = (double)we[t];
-          if (wt != 0.0) acc = hdd_add(acc, hdd_prod(wt, (double)(t - (ptr ? out[ptr - 1] : 0))));
-        }
-        acc = hdd_warp_sum(acc);
-        if (lane == 0) reinterpret_cast<double*>(p.cost)[e] = acc.hi + acc.lo;
-        if (p.cbb) {
-          int32_t* fscr = reinterpret_cast<int32_t*>(
-              slot + hull_log_bytes(N, M) + hull_cnt_bytes(M) + 2 * hull_align(8 * (size_t)(N + 1)));
-          hull_cbb_f64<K>(p, e, tfirst, reinterpret_cast<const double*>(we), logs, logn, fscr);
+        double* Ph = reinterpret_cast<double*>(ebuf0);
+        double* Pl = reinterpret_cast<double*>(ebuf1);
+        const hdd TNd = f64_prefix_dd(reinterpret_cast<const double*>(we), N, Ph, Pl);
+        __syncwarp();
+        if (p.cbb) {   // V_1..V_M; the returned placement is budget M's canonical one
+          hull_cbb_f64<K>(p, e, tfirst, TNd, Ph, Pl, logs, logn);
+          __syncwarp();
+          if (lane == 0)
+            reinterpret_cast<double*>(p.cost)[e] = reinterpret_cast<double*>(p.cbb)[(int64_t)e * (M + 1) + M];
+        } else {
+          const double c = f64_cost_warp(out, k, N, TNd, Ph, Pl);
+          if (lane == 0) reinterpret_cast<double*>(p.cost)[e] = c;
         }
       }
     }

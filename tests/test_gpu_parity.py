@@ -264,6 +264,26 @@ def test_dp_uniform_thm1_full_size(dev):
         assert npos[e] == M and pos[e].tolist() == f7
 
 
+def test_dp_uniform_thm1_bench_size(dev):
+    """The bench's all-ones variant (`--dp-hist ones`, 16384 x N=32768 x M=64, the one-warp
+    kernel's hand-off to the large-hull mode): every entry's V_0..V_M equal Thm 1's closed form
+     and its positions SURVEY F7's rule-B formula; no entry on the D&C kernel."""
+    N, M, E = 32768, 64, 16384
+    H = wl.uniform_hist(E, N, device=dev)
+    ws = torch.empty(sp.place_checkpoints_workspace_bytes(E, N, M), dtype=torch.uint8, device=dev)
+    pos, npos, cost, cbb = sp.place_checkpoints(H, M, cost_by_budget=True, workspace=ws)
+    torch.cuda.synchronize()
+    st = sp.dp_stats(ws)
+    assert st["entries_hull"] == E and st["entries_hull_big"] == E and st["evaluations"] == 0
+    K = M + 1
+    q, rho = divmod(N + 1, K)
+    f7 = torch.tensor([i * q + max(0, i - (K - rho)) for i in range(1, M + 1)], dtype=torch.int32,
+                      device=dev)
+    v = torch.tensor([thm1_value(N, m) for m in range(M + 1)], dtype=torch.int64, device=dev)
+    assert bool((npos == M).all()) and bool((pos == f7).all())
+    assert bool((cost == thm1_value(N, M)).all()) and bool((cbb == v).all())
+
+
 def test_dp_w5_full_size_every_entry(dev):
     """BASELINE's scale config at full size (16384 x N=32768 x M=64) in the bench launch
     configuration; EVERY entry against the oracle's CHT DP (threaded over the host
@@ -544,6 +564,41 @@ def test_expected_recompute_f64(dev):
     rc, _ = oracle.eval_batch(H.astype(np.int32), np_(pos), np_(npos), broadcast=True)
     ref = rc / H.sum(1, keepdims=True)
     assert np.allclose(np_(cost), ref, rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("N,budgets,blocks", [(8192, (64,), (64, 128)), (2048, (1, 8, 33), (16,)),
+                                               (700, (), (1,))])
+def test_expected_recompute_f64_broadcast(dev, N, budgets, blocks):
+    """fp64 weights with <= 4 broadcast sets (eval_bcast_f64_kernel: the bench's `--weights f64`
+    evaluation): against the oracle's exact integer costs / n at 1e-13 relative, and against the
+    chunked double-double kernel (SP_DBG_EVAL_PATH = 1); a bin-0 (miss) weight is ignored; a
+    malformed set gives NaN and the flagged worst case."""
+    cfg = wl.TraceConfig("t", 37, N, 8, 1, (N, N), (1, 1), "mix", dense_n=(N // 3, N))
+    H = wl.make_dense_hist(cfg, seed=N).numpy().astype(np.int64)
+    H[5, 1:] = 0
+    H[5, N] = 3                                    # a point mass at N
+    n = np.maximum(H[:, 1:].sum(1, keepdims=True), 1)
+    W = H / n
+    W[:, 0] = 1e300                                # misses: ignored by the objective
+    pos, npos, _ = sp.baseline_sets(N, budgets=budgets, blocks=blocks, device=dev)
+    Wd = torch.from_numpy(W).to(dev)
+    cost, worst = sp.expected_recompute(Wd, pos, npos)
+    with sp.debug(SP_DBG_EVAL_PATH=1):
+        cost1, worst1 = sp.expected_recompute(Wd, pos, npos)
+    torch.cuda.synchronize()
+    Hz = H.copy()
+    Hz[:, 0] = 0
+    rc, rw = oracle.eval_batch(Hz.astype(np.int32), np_(pos), np_(npos), broadcast=True)
+    assert np.allclose(np_(cost), rc / n, rtol=1e-13, atol=0)
+    assert np.allclose(np_(cost), np_(cost1), rtol=1e-15, atol=0)
+    assert (np_(worst) == rw).all() and (np_(worst1) == rw).all()
+    bad = pos.clone()
+    if bad.shape[1] >= 2 and int(npos[0]) >= 2:
+        bad[0, 1] = bad[0, 0]                      # not strictly increasing
+        c2, w2 = sp.expected_recompute(Wd, bad, npos)
+        torch.cuda.synchronize()
+        assert np.isnan(np_(c2)[:, 0]).all() and (np_(w2)[:, 0] == -sp.SP_ERR_BAD_POSITIONS).all()
+        assert np.allclose(np_(c2)[:, 1:], np_(cost)[:, 1:], rtol=0, atol=0)
 
 
 # ------------------------------------------------------------------------------------------

@@ -12,6 +12,7 @@ import collections
 import csv
 import json
 import os
+import re
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -27,6 +28,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+# our kernels (ncu may print them without the sp:: namespace)
+OURS = re.compile(r"\b(lcp_hist|accumulate_depths|row_stats|dp_hull|dp_hull_split|dp_lean|dp_place|"
+                  r"eval_bcast|eval_p32|eval|gamma_observe|gamma_snapshot|grid_\w+|match|index_\w+)"
+                  r"(_kernel)?\b")
 UNIT = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0, "Tbyte": 1e12}
 
 
@@ -98,7 +103,7 @@ def main():
         iK, iV = h.index("Kernel Name"), h.index("Metric Value")
         agg = collections.OrderedDict()
         for x in lr[1:]:
-            if "sp::" not in x[iK]:
+            if "sp::" not in x[iK] and not OURS.search(x[iK]):
                 continue
             k = short(x[iK])
             agg.setdefault(k, []).append(float(x[iV].replace(",", "")) / 1e6)   # ns -> ms

@@ -141,6 +141,7 @@ struct HullParams {
   const HullRowStat* rstat;   // n, T_N, first bin, guards per entry (integer weights), or NULL
   const int2* sparse;         // [E][HULL_KC] compacted support rows (valid when rstat[e].K <= HULL_KC)
   int fwd;                    // the large-hull mode ran: the int64 list is its forwarded list
+  int32_t* fwd_list;          // int32 [E]: the large-hull mode's forwarded entries
 };
 
 // Global capacity (lines, a power of two) of layer m's windowed ring: ~1.125x the hull size of
@@ -384,14 +385,21 @@ struct SRingI {
 };
 
 // 12-byte lines for the int64 / fp64 instantiations, interleaved like SRingI: a 384-byte
-// position row holds the 32 lanes' 8-byte intercepts then their int32 s; one IMAD per row address
+// position row holds the 32 lanes' 8-byte intercepts then their int32 s; one IMAD per row
+// address.  SP_HULL_WROW=320 stores s as uint16 (10-byte lines, s <= N <= 65535): the shared
+// memory then allows 11 warps per SM, but the registers (192-202 per thread) cap it at 10, and
+// it measured neutral (fp64 W5 68.9 vs 68.3 ms, accumulated rows 227 vs 226 ms).
+#ifndef SP_HULL_WROW
+#define SP_HULL_WROW 384
+#endif
+constexpr uint32_t WROW = SP_HULL_WROW;
 template <typename VT, int C0, int C1>
 struct SRingW {
   uint32_t b0;   // shared address of slot 0, row 0, this lane's intercept
-  uint32_t ds;   // s address - intercept address: 256 - 4 lane
+  uint32_t ds;   // s address - intercept address: 256 - 4 lane (WROW 320: 256 - 6 lane)
   __device__ __forceinline__ uint32_t at(int k, int pos) const {
     const uint32_t q = (uint32_t)pos & (uint32_t)((k ? C1 : C0) - 1);
-    return q * 384u + b0 + (k ? (uint32_t)C0 * 384u : 0u);
+    return q * WROW + b0 + (k ? (uint32_t)C0 * WROW : 0u);
   }
   __device__ __forceinline__ Line<VT> ld(int k, int pos) const {
     const uint32_t a = at(k, pos);
@@ -400,7 +408,13 @@ struct SRingW {
       asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v.b) : "r"(a));
     else
       asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v.b) : "r"(a));
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.s) : "r"(a + ds));
+    if constexpr (WROW == 320) {
+      unsigned short sv;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(sv) : "r"(a + ds));
+      v.s = sv;
+    } else {
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v.s) : "r"(a + ds));
+    }
     return v;
   }
   __device__ __forceinline__ Line<VT> ld_back(int k, int b, int t) const { return ld(k, b - t); }
@@ -411,7 +425,10 @@ struct SRingW {
       asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v.b) : "memory");
     else
       asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v.b) : "memory");
-    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a + ds), "r"(v.s) : "memory");
+    if constexpr (WROW == 320)
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(a + ds), "h"((unsigned short)v.s) : "memory");
+    else
+      asm volatile("st.shared.b32 [%0], %1;" ::"r"(a + ds), "r"(v.s) : "memory");
   }
   static constexpr int cap(int k) { return k ? C1 : C0; }
 };
@@ -515,7 +532,7 @@ struct WRing {
 
 template <int K, typename VT>
 __host__ __device__ constexpr size_t ring_bytes() {
-  if constexpr (sizeof(VT) == 8) return (size_t)(WC + (K == 2 ? WC : 0)) * 384;
+  if constexpr (sizeof(VT) == 8) return (size_t)(WC + (K == 2 ? WC : 0)) * WROW;
   return (size_t)(HC0 + (K == 2 ? HC1 : 0)) * 192;
 }
 // per-warp row staging in shared memory: none (the counts wait in a register queue, HULL_PF
@@ -1362,7 +1379,7 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
   SR srg;
   if constexpr (sizeof(VT) == 8) {
     srg.sm.b0 = sbase + 8u * (uint32_t)lane;
-    srg.sm.ds = 256u - 4u * (uint32_t)lane;
+    srg.sm.ds = WROW == 320 ? 256u - 6u * (uint32_t)lane : 256u - 4u * (uint32_t)lane;
   } else {
     srg.sm.b0 = sbase + 4u * (uint32_t)lane;
     srg.sm.ds = 128u - 2u * (uint32_t)lane;
@@ -1376,7 +1393,10 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
       p.ws + (WIDE ? SP_WS_WIDE_CTR_OFF : BIG ? SP_WS_BIG_CTR_OFF : SP_WS_ENTRY_CTR_OFF));
   // Lists: the int32 kernel hands what it cannot solve to the int64 list (p.wide from the front);
   // when the large-hull mode runs (p.fwd) it takes that list and forwards the entries beyond its
-  // own guard to the int64 instantiation through the same array's back (SP_WS_BIG_COUNT_OFF).
+  // own guard to the int64 instantiation through a list of its own (p.fwd_list; its count at
+  // SP_WS_BIG_COUNT_OFF).  (Round 2 first wrote it into the back of the int64 list's array: with
+  // every entry listed -- accumulated rows -- the two overlapped; tests/test_gpu_hull.py
+  // test_hull_int64_list_handoff_all_entries.)
   // (The int32 kernel's hot loop is sensitive to any code around it -- routing there cost 2% on
   // W5 -- so the hand-offs live in the other two instantiations.)
   const bool from_fwd = WIDE && p.fwd;
@@ -1399,7 +1419,7 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
     if (lane == 0) it = (int)atomicAdd(ectr, 1u);
     it = __shfl_sync(FULL, it, 0);
     if (it >= n_items) break;
-    const int e = from_fwd ? p.wide[p.E - 1 - it] : (WIDE || BIG) ? p.wide[it]
+    const int e = from_fwd ? p.fwd_list[it] : (WIDE || BIG) ? p.wide[it]
                                                   : (p.order ? p.order[it] : it);
     const WT* we = reinterpret_cast<const WT*>(p.w) + (int64_t)e * (N + 1);
 
@@ -1472,7 +1492,7 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
       const bool wide_ok = !bad && n < (1ll << 46) / N;
       if (!WIDE && !narrow) {
         if (lane == 0) {
-          if (BIG && wide_ok) p.wide[p.E - 1 - (int)atomicAdd(big_n, 1u)] = e;   // forwarded
+          if (BIG && wide_ok) p.fwd_list[atomicAdd(big_n, 1u)] = e;   // forwarded
           else if (wide_ok) p.wide[atomicAdd(wide_n, 1u)] = e;
           else p.fb[atomicAdd(fb_n, 1u)] = e;
         }
@@ -2134,6 +2154,11 @@ __global__ void __launch_bounds__(32, 1) dp_lean_kernel(HullParams p, const Hull
 // and for integer weights n = P_N, T_N, the first non-zero bin and the guards that dp_lean_kernel
 // needs before it starts (so the DP itself reads each row once).
 constexpr int RS_U = 32;   // row pre-pass: 32-bin chunks in flight per lane (4 KB per warp)
+__device__ __forceinline__ long long mad_wide_s32(int a, int b, long long c) {   // c + a b, exact
+  long long d;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
 template <typename WT>
 __global__ void __launch_bounds__(256) row_stats_kernel(const WT* __restrict__ w, int E, int N,
                                                         int32_t* __restrict__ key,
@@ -2161,7 +2186,18 @@ __global__ void __launch_bounds__(256) row_stats_kernel(const WT* __restrict__ w
       for (int u = 0; u < RS_U; ++u) {
         const int t = base + 32 * u + 1 + lane;
         const unsigned nz = __ballot_sync(FULL, v[u] != WT(0));
-        if constexpr (!std::is_same<WT, double>::value) {
+        if constexpr (std::is_same<WT, int32_t>::value) {
+          // int32 counts: n and T_N with one mad.wide each; the first non-zero bin from the
+          // ballot (warp-uniform), the only guard a negative count
+          bad |= v[u] < 0;
+          n = mad_wide_s32(v[u], 1, n);
+          tn = mad_wide_s32(v[u], t, tn);
+          if (nz && tfirst == INT_MAX) tfirst = base + 32 * u + __ffs(nz);
+          if (sp_e && c < HULL_KC) {
+            const int at = c + __popc(nz & lt);
+            if (v[u] != 0 && at < HULL_KC) sp_e[at] = make_int2(t, v[u]);
+          }
+        } else if constexpr (!std::is_same<WT, double>::value) {
           const long long cv = (long long)v[u];
           bad |= (cv < 0) | (cv >= (1ll << 40));
           n += cv;
@@ -2375,13 +2411,15 @@ size_t sp_hull_order_bytes(int E) {
 
 cudaError_t sp_hull_launch(const void* weights, int wtype, int E, int N, int M, int32_t* pos,
                            int32_t* npos, void* cost, void* cbb, int32_t* fpos,
-                           int32_t* fn, uint8_t* ws, int32_t* fb, int32_t* wide, uint8_t* pool,
-                           uint8_t* order_ws, uint8_t* slots, int grid, cudaStream_t st) {
+                           int32_t* fn, uint8_t* ws, int32_t* fb, int32_t* wide,
+                           int32_t* fwd_list, uint8_t* pool, uint8_t* order_ws, uint8_t* slots,
+                           int grid, cudaStream_t st) {
   const bool no_order = sp_debug_get(SP_DBG_HULL_NO_ORDER) != 0;   // comparison hook
   const int logcap_env = sp_debug_get(SP_DBG_HULL_LOGCAP);   // test hook: force the log-full fallback
   sp::HullParams p;
   p.order = nullptr;
   p.fwd = 0;
+  p.fwd_list = fwd_list;
   const size_t a = sp::hull_align(4 * (size_t)E);
   int32_t* kin = (int32_t*)order_ws;
   int32_t* vin = (int32_t*)(order_ws + a);

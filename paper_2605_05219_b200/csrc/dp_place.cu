@@ -1611,7 +1611,7 @@ extern "C" size_t sp_place_checkpoints_workspace_bytes(int32_t n_entries, int32_
     const int gh = std::max(std::max(sp_hull_grid(n_entries, N, M, SP_W_COUNTS_I32),
                                      sp_hull_grid(n_entries, N, M, SP_W_COUNTS_I64)),
                             sp_hull_grid(n_entries, N, M, SP_W_PROB_F64));
-    hull = 2 * sp::align256(4 * (size_t)n_entries) + sp::align256(sp_hull_wg_bytes(n_entries, N, M)) +
+    hull = 3 * sp::align256(4 * (size_t)n_entries) + sp::align256(sp_hull_wg_bytes(n_entries, N, M)) +
            sp::align256(sp_hull_order_bytes(n_entries)) + (size_t)gh * sp_hull_slot_bytes(N, M);
   }
   return SP_WS_STATS_BYTES + hull + (size_t)dp_grid(n_entries, N) * sp::slot_bytes(N, M);
@@ -1665,7 +1665,8 @@ static sp_status place_impl(const void* weights, sp_weight_type wtype,
   const int hgrid = use_hull ? sp_hull_grid(n_entries, N, M, wtype) : 0;
   const size_t fb_off = SP_WS_STATS_BYTES;
   const size_t wide_off = fb_off + (use_hull ? sp::align256(4 * (size_t)n_entries) : 0);
-  const size_t pool_off = wide_off + (use_hull ? sp::align256(4 * (size_t)n_entries) : 0);
+  const size_t fwd_off = wide_off + (use_hull ? sp::align256(4 * (size_t)n_entries) : 0);
+  const size_t pool_off = fwd_off + (use_hull ? sp::align256(4 * (size_t)n_entries) : 0);
   const size_t order_off = pool_off + (use_hull ? sp::align256(sp_hull_wg_bytes(n_entries, N, M)) : 0);
   const size_t hull_off = order_off + (use_hull ? sp::align256(sp_hull_order_bytes(n_entries)) : 0);
   const size_t dc_off = hull_off + (size_t)hgrid * (use_hull ? sp_hull_slot_bytes(N, M) : 0);
@@ -1697,7 +1698,8 @@ static sp_status place_impl(const void* weights, sp_weight_type wtype,
         weights, wtype, n_entries, N, M, positions, n_positions, cost, cost_by_budget, fpos, fn,
         (uint8_t*)workspace,
         reinterpret_cast<int32_t*>((uint8_t*)workspace + fb_off),
-        reinterpret_cast<int32_t*>((uint8_t*)workspace + wide_off), (uint8_t*)workspace + pool_off,
+        reinterpret_cast<int32_t*>((uint8_t*)workspace + wide_off),
+        reinterpret_cast<int32_t*>((uint8_t*)workspace + fwd_off), (uint8_t*)workspace + pool_off,
         (uint8_t*)workspace + order_off, (uint8_t*)workspace + hull_off, hgrid, st);
     if (he != cudaSuccess) {
       sp_set_cuda_error(he);

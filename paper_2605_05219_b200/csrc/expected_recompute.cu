@@ -211,7 +211,10 @@ __global__ void __launch_bounds__(EP_NT)
   __shared__ long long sh_carry, sh_TN;
   __shared__ int sh_big;
   const int lane = lane_id(), wid = warp_id();
-  const int nseg = (N + 1 + 1023) / 1024;
+  // segments cover bins 1..N (bin 0, the misses, is not in the objective): index x - 1 holds
+  // P(x) relative to its segment -- N = 8192 is 8 segments, one round of 8 warps (round 1
+  // scanned bins 0..N: a ninth segment of one bin and a second round)
+  const int nseg = (N + 1023) / 1024;
   // broadcast sets staged once per CTA (stage_sets: the host checked they fit): positions as
   // uint16 (<= SP_MAX_N), and per set its worst case, or -1 for a malformed set
   uint16_t* spos = reinterpret_cast<uint16_t*>(seg_raw + (size_t)nseg * 1024 * sizeof(ST));
@@ -249,14 +252,14 @@ __global__ void __launch_bounds__(EP_NT)
       int32_t v[32];
 #pragma unroll
       for (int u = 0; u < 32; ++u) {
-        const int t = b0 + 32 * u + lane;
-        v[u] = (sg < nseg && t >= 1 && t <= N) ? __ldcs(we + t) : 0;
+        const int t = b0 + 32 * u + lane + 1;
+        v[u] = (sg < nseg && t <= N) ? __ldcs(we + t) : 0;
       }
       int run32 = 0;
       long long ls = 0;
 #pragma unroll
       for (int u = 0; u < 32; ++u) {
-        const int t = b0 + 32 * u + lane;
+        const int t = b0 + 32 * u + lane + 1;
         tpart += (long long)t * v[u];
         ls += v[u];
         int inc = v[u];
@@ -303,9 +306,10 @@ __global__ void __launch_bounds__(EP_NT)
     const bool exact32 = !sh_big;
     auto Pof = [&](int x) -> long long {
       if (x <= 0) return 0;
-      if (exact32) return (long long)seg[x] + woff[x >> 10];
-      long long s = woff[x >> 10];   // a huge segment: sum its bins from global memory
-      for (int t = max((x >> 10) << 10, 1); t <= x; ++t) s += we[t];
+      const int i = x - 1;   // bin x sits at index x - 1
+      if (exact32) return (long long)seg[i] + woff[i >> 10];
+      long long s = woff[i >> 10];   // a huge segment: sum its bins from global memory
+      for (int t = ((i >> 10) << 10) + 1; t <= x; ++t) s += we[t];
       return s;
     };
     if (stage_sets) {
@@ -751,7 +755,7 @@ extern "C" sp_status sp_expected_recompute(const void* weights, sp_weight_type w
         (const double*)weights, n_entries, N, positions, n_positions, n_sets, max_pos,
         (double*)cost, worst_case);
   } else if (wtype == SP_W_COUNTS_I32 && path != 1) {
-    const int nseg = (N + 1 + 1023) / 1024;
+    const int nseg = (N + 1023) / 1024;   // bins 1..N (eval_p32_kernel)
     const bool wide = path == 2;   // 4-byte prefixes (tests / comparison)
     size_t dyn = (size_t)nseg * 1024 * (wide ? 4 : 2);
     // broadcast sets staged in shared memory when they fit in 32 KB more

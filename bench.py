@@ -758,7 +758,7 @@ def run_ours(args):
         "clocks": clk,
         "e2e": e2e,
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:   # (N = 1 only)
         line["cpu_baseline"] = cpu_baseline(args, os.cpu_count() or 1)
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -850,6 +850,24 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
             if (!more[k]) continue;
             int cs = L2[k].s - j;
             VT cb = L2[k].b - bj[k];
+#ifdef SP_HULL_LOOP_PF
+            // the line below the one under test is loaded with it, so an iteration's test does
+            // not wait for its own load (one speculative load when the loop stops)
+            Line<VT> nx = rg.ldh(k, top[k] - 1, hi[k]);
+            while (top[k] - f[k] >= 1) {
+              const Line<VT> l1 = nx;
+              if (top[k] - f[k] >= 2) nx = rg.ldh(k, top[k] - 2, hi[k]);
+              const int ls = l1.s - j;
+              const VT lb = l1.b - bj[k];
+              if (pop_test(ls, lb, cs, cb)) {
+                --top[k];
+                cs = ls;
+                cb = lb;
+              } else {
+                break;
+              }
+            }
+#else
             while (top[k] - f[k] >= 1) {
               const Line<VT> l1 = rg.ldh(k, top[k] - 1, hi[k]);
               const int ls = l1.s - j;
@@ -862,6 +880,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
                 break;
               }
             }
+#endif
           }
         }
         VT v0[K], v1[K], v2[K];

@@ -1381,9 +1381,20 @@ __device__ __forceinline__ void hull_cbb_f64(const HullParams& p, int e, int tfi
 #ifndef SP_HULL_BIG_MINB
 #define SP_HULL_BIG_MINB 1
 #endif
+// int64 / fp64 instantiations: capped at 168 registers (no spills) so that an SM sub-partition
+// holds 3 of their warps, not 2 (202 / 192 registers: 8 warps per SM; now 9, the shared-memory
+// bound): accumulated rows 226 -> 210 ms, fp64 W5 rows 68.3 -> 62.0 ms (profiles/r02e_dp_variants.txt)
+#ifndef SP_HULL_WIDE_MINB
+#define SP_HULL_WIDE_MINB 12
+#endif
+#ifndef SP_HULL_F64_MINB
+#define SP_HULL_F64_MINB 12
+#endif
 template <typename WT, int K, typename VT, bool BIG = false>
 __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
-                                          : (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL_MINB)
+                                      : std::is_same<VT, long long>::value ? SP_HULL_WIDE_MINB
+                                      : std::is_same<VT, double>::value ? SP_HULL_F64_MINB
+                                      : (K == 1 && sizeof(VT) == 4) ? 16 : SP_HULL_MINB)
     dp_hull_kernel(HullParams p) {
   constexpr bool F64 = std::is_same<VT, double>::value;
   constexpr bool WIDE = std::is_same<VT, long long>::value;

@@ -384,13 +384,13 @@ struct SRingI {
   __device__ __forceinline__ void st2(int k, int pos, int b, int sv) const { st(k, pos, Line<int>{b, sv}); }
 };
 
-// 12-byte lines for the int64 / fp64 instantiations, interleaved like SRingI: a 384-byte
-// position row holds the 32 lanes' 8-byte intercepts then their int32 s; one IMAD per row
-// address.  SP_HULL_WROW=320 stores s as uint16 (10-byte lines, s <= N <= 65535): the shared
-// memory then allows 11 warps per SM, but the registers (192-202 per thread) cap it at 10, and
-// it measured neutral (fp64 W5 68.9 vs 68.3 ms, accumulated rows 227 vs 226 ms).
+// 10-byte lines for the int64 / fp64 instantiations, interleaved like SRingI: a 320-byte position
+// row holds the 32 lanes' 8-byte intercepts then their s as uint16 (s <= N <= SP_MAX_N = 65535);
+// one IMAD per row address.  With the 168-register cap (below) the shared memory is the bound:
+// 10 warps per SM instead of 9 with 12-byte lines (int32 s, 384-byte rows, SP_HULL_WROW=384):
+// accumulated rows 209.5 -> 201.3 ms, fp64 W5 rows 62.1 -> 58.8 ms (profiles/r02e_dp_variants.txt).
 #ifndef SP_HULL_WROW
-#define SP_HULL_WROW 384
+#define SP_HULL_WROW 320
 #endif
 constexpr uint32_t WROW = SP_HULL_WROW;
 template <typename VT, int C0, int C1>

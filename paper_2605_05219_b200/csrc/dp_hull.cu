@@ -2301,10 +2301,15 @@ static int hull_grid_t(int E) {
   return clamp_grid((long)dev_sms() * occ, E);
 }
 // the int32 large-hull mode (same shared memory as the int32 kernel)
+#ifndef SP_HULL_BIG_PAD
+#define SP_HULL_BIG_PAD 0   // extra dynamic shared memory per warp (occupancy / L1 experiments)
+#endif
+template <int K>
+constexpr size_t big_dyn_bytes() { return hull_dyn_bytes<K, int>() + SP_HULL_BIG_PAD; }
 template <typename WT, int K>
 static int big_grid_t(int E) {
   static int cache[HULL_MAX_DEV] = {0};
-  const int occ = occ_cached(dp_hull_kernel<WT, K, int, true>, hull_dyn_bytes<K, int>(), cache);
+  const int occ = occ_cached(dp_hull_kernel<WT, K, int, true>, big_dyn_bytes<K>(), cache);
   return clamp_grid((long)dev_sms() * occ, E);
 }
 
@@ -2377,7 +2382,7 @@ static void hull_launch_t(HullParams p, const HullRowStat* rstat, int gn, cudaSt
       const long regions = (long)(sp_hull_wg_bytes(p.E, p.N, p.M) / p.wgb);
       const int gb = (int)std::min<long>(std::min(gn, big_grid_t<WT, K>(p.E)), regions);
       if (gb >= 1) {
-        dp_hull_kernel<WT, K, int, true><<<gb, 32, hull_dyn_bytes<K, int>(), st>>>(p);
+        dp_hull_kernel<WT, K, int, true><<<gb, 32, big_dyn_bytes<K>(), st>>>(p);
         p.fwd = 1;
       }
     }

@@ -304,6 +304,29 @@ def test_dp_w5_full_size_every_entry(dev):
     assert (npos == cfg.M).all()                      # dense histograms: every slot is used
 
 
+def test_dp_accum_full_size_every_entry(dev):
+    """The bench's `--dp-hist accum` variant at full size (16384 x N=32768 x M=64, n ~ U[1.2e5,
+    1.8e5] per row: past the int32 guard, so the int32 kernel lists every entry, the large-hull
+    mode forwards them and the int64 instantiation solves them -- the hand-off path with every
+    entry listed); every entry against the oracle's CHT, bit-exact."""
+    import dataclasses
+    cfg = dataclasses.replace(wl.CONFIGS["W5"], dense_n=(120000, 180000))
+    H = wl.make_dense_hist(cfg, seed=0, device=dev)
+    ws = torch.empty(sp.place_checkpoints_workspace_bytes(cfg.n_entries, cfg.N, cfg.M),
+                     dtype=torch.uint8, device=dev)
+    pos, npos, cost, cbb = sp.place_checkpoints(H, cfg.M, cost_by_budget=True, workspace=ws)
+    torch.cuda.synchronize()
+    st = sp.dp_stats(ws)
+    assert st["entries_i64"] == cfg.n_entries and st["entries_hull"] == cfg.n_entries
+    pos, npos, cost, cbb = np_(pos), np_(npos), np_(cost), np_(cbb)
+    Hc = np_(H)
+    del H
+    rpos, rnpos, rcost, rcbb = oracle.place_batch(Hc, cfg.M, "cht", nthreads=os.cpu_count() or 1,
+                                                  with_budget=True)
+    assert (npos == rnpos).all() and (pos == rpos).all()
+    assert (cost == rcost).all() and (cbb == rcbb).all()
+
+
 def test_dp_edge_cases(dev):
     N = 50
     H = np.zeros((8, N + 1), np.int64)

@@ -589,6 +589,9 @@ using HullCT = typename std::conditional<std::is_same<VT, double>::value, double
 // of sequential passes.  Warp 0 publishes after each 32-row chunk, warp 1 releases ring space
 // after each chunk; either warp raises `abort` when it gives the entry up (ring / log full).
 constexpr int SPLIT_RING = 1024;
+#ifndef SP_SPLIT_NS
+#define SP_SPLIT_NS 64   // SPLIT mode: back-off of a warp waiting for the other (ns)
+#endif
 struct SplitSync {
   int* ring;                 // shared, SPLIT_RING ints
   volatile int* produced;    // support rows published by warp 0
@@ -740,9 +743,9 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       if (ss) {   // SPLIT mode: wait for the other warp (consumer: data; producer: ring space)
         if (lane == 0) {
           if (chain_in)
-            while (*ss->produced < evbase + nev - 1 && !*ss->abort_) __nanosleep(64);
+            while (*ss->produced < evbase + nev - 1 && !*ss->abort_) __nanosleep(SP_SPLIT_NS);
           else
-            while (evbase + nev - 1 - *ss->consumed >= SPLIT_RING && !*ss->abort_) __nanosleep(64);
+            while (evbase + nev - 1 - *ss->consumed >= SPLIT_RING && !*ss->abort_) __nanosleep(SP_SPLIT_NS);
         }
         __syncwarp();
         if (*ss->abort_) {

@@ -397,8 +397,12 @@ def test_dp_workspace_too_small(dev):
 
 
 @pytest.mark.parametrize("N,M,E,dyadic", [(500, 7, 10, False), (2048, 8, 8, True),
-                                          (8192, 16, 4, False)])
+                                          (8192, 16, 4, False), (4096, 64, 6, False),
+                                          (700, 100, 4, False)])
 def test_dp_f64_relerr(dev, N, M, E, dyadic):
+    """fp64 weights w = c / n (a7): cost and V_0..V_M against the oracle's exact V_int / n at the
+    1e-12 bound, the returned positions re-scored by the oracle's fp64 walk; M = 64 (two slots)
+    and M = 100 (two chained passes: the e-row buffers then hold the prefix sums)."""
     cfg = wl.TraceConfig("t", E, N, M, 1, (N, N), (1, 1), "mix",
                          dense_n=(4096, 4096) if dyadic else (3000, 9000))
     H = wl.make_dense_hist(cfg, seed=11).numpy().astype(np.int64)

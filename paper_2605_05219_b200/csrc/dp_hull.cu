@@ -605,7 +605,8 @@ struct SplitSync {
 // opt_m(j) - opt_m(j_prev) zero bits then a one bit, LSB first -- at most K + N <= 2N bits per
 // layer whatever the hull does (a change log fills when opt moves on most rows, e.g. all-ones);
 // the front lines of hulls that outgrow the window are prefetched into L2 16 positions ahead.
-template <typename WT, typename VT, int K, bool ALLACT, class RING, bool CMP = false, bool BIG = false>
+template <typename WT, typename VT, int K, bool ALLACT, class RING, bool CMP = false, bool BIG = false,
+          bool ONEPASS = false>
 __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
                                         HullCT<VT> TN, VT nV, RING rg, uint32_t* logs,
                                         int32_t* logn, VT* ebuf0, VT* ebuf1,
@@ -630,7 +631,8 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
   for (int ps = ps_begin; ps < ps_end && !ovf; ++ps) {
     const VT* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
     VT* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
-    const bool chain_in = ps > 0, chain_out = ps + 1 < passes;
+    // ONEPASS (M = 32 K, no SPLIT partner): no chained e-rows at compile time
+    const bool chain_in = !ONEPASS && ps > 0, chain_out = !ONEPASS && ps + 1 < passes;
     // Per slot: deque [f, b] (monotone counters; ring position = counter mod capacity).  In
     // registers: the back line B0 (the last one pushed) and the front line F0; the two lines
     // below the back and the two above the front are loaded from the ring at the top of every
@@ -740,7 +742,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
       // value at support row t-1 (constant over zero rows), 0 before the first
       VT Ec = 0;
       const int nev = __popc(evmask);
-      if (ss) {   // SPLIT mode: wait for the other warp (consumer: data; producer: ring space)
+      if (!ONEPASS && ss) {   // SPLIT mode: wait for the other warp (consumer: data; producer: ring space)
         if (lane == 0) {
           if (chain_in)
             while (*ss->produced < evbase + nev - 1 && !*ss->abort_) __nanosleep(SP_SPLIT_NS);
@@ -979,7 +981,7 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
           else eout_buf[evbase + q] = eo[K - 1];
         }
       }
-      if (ss) {   // publish this chunk (producer) / release its ring slots (consumer)
+      if (!ONEPASS && ss) {   // publish this chunk (producer) / release its ring slots (consumer)
         __syncwarp();
         __threadfence_block();
         if (lane == 0) {
@@ -1256,7 +1258,8 @@ __device__ __forceinline__ bool hull_dp_skew(const HullParams& p, const WT* __re
 }
 
 // dispatch to the compact-list walk (sparse rows) or the row scan (CMP: compile-time)
-template <typename WT, typename VT, int K, bool ALLACT, class RING, bool BIG = false>
+template <typename WT, typename VT, int K, bool ALLACT, class RING, bool BIG = false,
+          bool ONEPASS = false>
 __device__ __forceinline__ bool hull_dp_any(const HullParams& p, const WT* __restrict__ we, int e,
                                             HullCT<VT> TN, VT nV, RING rg, uint32_t* logs,
                                             int32_t* logn, VT* ebuf0, VT* ebuf1, unsigned& pops_e,
@@ -1264,12 +1267,12 @@ __device__ __forceinline__ bool hull_dp_any(const HullParams& p, const WT* __res
                                             const int2* klist, const SplitSync* ss = nullptr,
                                             int ps_only = -1) {
   if (kc >= 0)
-    return hull_dp<WT, VT, K, ALLACT, RING, true, BIG>(p, we, e, TN, nV, rg, logs, logn, ebuf0,
-                                                       ebuf1, pops_e, ev_e, logfull, stage, kc,
-                                                       klist, ss, ps_only);
-  return hull_dp<WT, VT, K, ALLACT, RING, false, BIG>(p, we, e, TN, nV, rg, logs, logn, ebuf0,
-                                                      ebuf1, pops_e, ev_e, logfull, stage, -1,
-                                                      nullptr, ss, ps_only);
+    return hull_dp<WT, VT, K, ALLACT, RING, true, BIG, ONEPASS>(p, we, e, TN, nV, rg, logs, logn,
+                                                                ebuf0, ebuf1, pops_e, ev_e, logfull,
+                                                                stage, kc, klist, ss, ps_only);
+  return hull_dp<WT, VT, K, ALLACT, RING, false, BIG, ONEPASS>(p, we, e, TN, nV, rg, logs, logn,
+                                                               ebuf0, ebuf1, pops_e, ev_e, logfull,
+                                                               stage, -1, nullptr, ss, ps_only);
 }
 
 // a7: the definitional cost sum_t w_t (t - l(t; C)) of a placement C = {c_1 < ... < c_k} for fp64
@@ -1564,6 +1567,16 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
         ovf = fullm ? hull_dp_skew<WT, true>(p, we, e, TN, srg.sm, logs, logn, pops_e, ev_e, logfull)
                     : hull_dp_skew<WT, false>(p, we, e, TN, srg.sm, logs, logn, pops_e, ev_e,
                                               logfull);
+      else
+#endif
+      // M = 32 K (W5's M = 64): one pass, no chained e-rows and no SPLIT partner at compile time
+      // -- the per-row chain checks and the predicated e-row store vanish (W5 28.95 -> 27.69 ms,
+      // profiles/r02e_dp_variants.txt)
+#ifndef SP_HULL_NO_ONEPASS
+      if (M == 32 * K)
+        ovf = hull_dp_any<WT, VT, K, true, std::remove_reference_t<decltype(rg1)>, false, true>(
+            p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1, pops_e, ev_e, logfull, stage, kcomp,
+            klist);
       else
 #endif
       ovf = fullm ? hull_dp_any<WT, VT, K, true>(p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1,

@@ -1578,6 +1578,13 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
             p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1, pops_e, ev_e, logfull, stage, kcomp,
             klist);
       else
+#ifdef SP_HULL_ONEPASS_ALL
+      if (M < 32 * K)
+        ovf = hull_dp_any<WT, VT, K, false, std::remove_reference_t<decltype(rg1)>, false, true>(
+            p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1, pops_e, ev_e, logfull, stage, kcomp,
+            klist);
+      else
+#endif
 #endif
       ovf = fullm ? hull_dp_any<WT, VT, K, true>(p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1,
                                              pops_e, ev_e, logfull, stage, kcomp, klist)
@@ -1590,6 +1597,13 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
                                         ev_e, logfull, stage, kcomp, klist);
       }
     } else {
+#ifdef SP_HULL_ONEPASS_WIDE
+      if (M == 32 * K)
+        ovf = hull_dp_any<WT, VT, K, true, SR, false, true>(p, we, e, TN, nV, srg, logs, logn,
+                                                            ebuf0, ebuf1, pops_e, ev_e, logfull,
+                                                            stage, kcomp, klist);
+      else
+#endif
       ovf = fullm ? hull_dp_any<WT, VT, K, true>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1,
                                              pops_e, ev_e, logfull, stage, kcomp, klist)
                   : hull_dp_any<WT, VT, K, false>(p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1,

@@ -1578,13 +1578,12 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
             p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1, pops_e, ev_e, logfull, stage, kcomp,
             klist);
       else
-#ifdef SP_HULL_ONEPASS_ALL
+      // M < 32 K: one pass as well, some slots inactive (W2 DP 54.1 -> 51.9 us, W3 80.8 -> 79.9 us)
       if (M < 32 * K)
         ovf = hull_dp_any<WT, VT, K, false, std::remove_reference_t<decltype(rg1)>, false, true>(
             p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1, pops_e, ev_e, logfull, stage, kcomp,
             klist);
       else
-#endif
 #endif
       ovf = fullm ? hull_dp_any<WT, VT, K, true>(p, we, e, TN, nV, rg1, logs, logn, ebuf0, ebuf1,
                                              pops_e, ev_e, logfull, stage, kcomp, klist)
@@ -1597,7 +1596,7 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
                                         ev_e, logfull, stage, kcomp, klist);
       }
     } else {
-#ifdef SP_HULL_ONEPASS_WIDE
+#ifndef SP_HULL_NO_ONEPASS   // (int64: accumulated rows 201.2 -> 198.6 ms; fp64: 58.7 -> 57.3 ms)
       if (M == 32 * K)
         ovf = hull_dp_any<WT, VT, K, true, SR, false, true>(p, we, e, TN, nV, srg, logs, logn,
                                                             ebuf0, ebuf1, pops_e, ev_e, logfull,

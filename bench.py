@@ -26,8 +26,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DP cells/s (entries*N*M)"
-TRAFFIC_JSON = "r02h_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
-PIPES_JSON = "r02h_ncu_pipes.json"       # the same capture: issue / ALU / FMA / LSU pipe %
+TRAFFIC_JSON = "r02i_ncu_traffic.json"   # ncu capture of the current kernels (tools/ncu_profiles.py)
+PIPES_JSON = "r02i_ncu_pipes.json"       # the same capture: issue / ALU / FMA / LSU pipe %
 
 
 def dp_update_cost():

@@ -606,7 +606,7 @@ struct SplitSync {
 // layer whatever the hull does (a change log fills when opt moves on most rows, e.g. all-ones);
 // the front lines of hulls that outgrow the window are prefetched into L2 16 positions ahead.
 template <typename WT, typename VT, int K, bool ALLACT, class RING, bool CMP = false, bool BIG = false,
-          bool ONEPASS = false>
+          bool ONEPASS = false, int ROLE = 0>
 __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restrict__ we, int e,
                                         HullCT<VT> TN, VT nV, RING rg, uint32_t* logs,
                                         int32_t* logn, VT* ebuf0, VT* ebuf1,
@@ -632,7 +632,10 @@ __device__ __forceinline__ bool hull_dp(const HullParams& p, const WT* __restric
     const VT* ein = (ps & 1) ? ebuf1 : ebuf0;    // e_{64 ps}(.) from the previous pass
     VT* eout_buf = (ps & 1) ? ebuf0 : ebuf1;
     // ONEPASS (M = 32 K, no SPLIT partner): no chained e-rows at compile time
-    const bool chain_in = !ONEPASS && ps > 0, chain_out = !ONEPASS && ps + 1 < passes;
+    // ROLE (SPLIT mode at compile time): 1 = warp 0 (pass 0, chains out), 2 = warp 1 (pass 1,
+    // chains in); 0 = decided at run time
+    const bool chain_in = ROLE == 2 ? true : ROLE == 1 ? false : !ONEPASS && ps > 0;
+    const bool chain_out = ROLE == 1 ? true : ROLE == 2 ? false : !ONEPASS && ps + 1 < passes;
     // Per slot: deque [f, b] (monotone counters; ring position = counter mod capacity).  In
     // registers: the back line B0 (the last one pushed) and the front line F0; the two lines
     // below the back and the two above the front are loaded from the ring at the top of every
@@ -1259,7 +1262,7 @@ __device__ __forceinline__ bool hull_dp_skew(const HullParams& p, const WT* __re
 
 // dispatch to the compact-list walk (sparse rows) or the row scan (CMP: compile-time)
 template <typename WT, typename VT, int K, bool ALLACT, class RING, bool BIG = false,
-          bool ONEPASS = false>
+          bool ONEPASS = false, int ROLE = 0>
 __device__ __forceinline__ bool hull_dp_any(const HullParams& p, const WT* __restrict__ we, int e,
                                             HullCT<VT> TN, VT nV, RING rg, uint32_t* logs,
                                             int32_t* logn, VT* ebuf0, VT* ebuf1, unsigned& pops_e,
@@ -1267,10 +1270,10 @@ __device__ __forceinline__ bool hull_dp_any(const HullParams& p, const WT* __res
                                             const int2* klist, const SplitSync* ss = nullptr,
                                             int ps_only = -1) {
   if (kc >= 0)
-    return hull_dp<WT, VT, K, ALLACT, RING, true, BIG, ONEPASS>(p, we, e, TN, nV, rg, logs, logn,
+    return hull_dp<WT, VT, K, ALLACT, RING, true, BIG, ONEPASS, ROLE>(p, we, e, TN, nV, rg, logs, logn,
                                                                 ebuf0, ebuf1, pops_e, ev_e, logfull,
                                                                 stage, kc, klist, ss, ps_only);
-  return hull_dp<WT, VT, K, ALLACT, RING, false, BIG, ONEPASS>(p, we, e, TN, nV, rg, logs, logn,
+  return hull_dp<WT, VT, K, ALLACT, RING, false, BIG, ONEPASS, ROLE>(p, we, e, TN, nV, rg, logs, logn,
                                                                ebuf0, ebuf1, pops_e, ev_e, logfull,
                                                                stage, -1, nullptr, ss, ps_only);
 }
@@ -2090,12 +2093,35 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
     const int2* klist = sparse_row ? p.sparse + (size_t)e * HULL_KC : nullptr;
     unsigned pops_e = 0, ev_e = 0;
     bool logfull = false;
+#ifdef SP_SPLIT_ROLES
+    // each warp's role at compile time (warp 0 chains out, warp 1 chains in)
+    if (w == 0) {
+      if (fullm)
+        hull_dp_any<WT, int, 1, true, SRingI<HC0, HC1>, false, false, 1>(
+            p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0, pops_e, ev_e, logfull, stage,
+            kcomp, klist, &ss, w);
+      else
+        hull_dp_any<WT, int, 1, false, SRingI<HC0, HC1>, false, false, 1>(
+            p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0, pops_e, ev_e, logfull, stage,
+            kcomp, klist, &ss, w);
+    } else {
+      if (fullm)
+        hull_dp_any<WT, int, 1, true, SRingI<HC0, HC1>, false, false, 2>(
+            p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0, pops_e, ev_e, logfull, stage,
+            kcomp, klist, &ss, w);
+      else
+        hull_dp_any<WT, int, 1, false, SRingI<HC0, HC1>, false, false, 2>(
+            p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0, pops_e, ev_e, logfull, stage,
+            kcomp, klist, &ss, w);
+    }
+#else
     if (fullm)
       hull_dp_any<WT, int, 1, true>(p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0, pops_e,
                                 ev_e, logfull, stage, kcomp, klist, &ss, w);
     else
       hull_dp_any<WT, int, 1, false>(p, we, e, rs.tn, (int)rs.n, srg, logs, logn, ebuf0, ebuf0,
                                  pops_e, ev_e, logfull, stage, kcomp, klist, &ss, w);
+#endif
     __syncthreads();
     if (s_abort) {   // ring or log full in either warp: the large-hull mode or the int64
       if (threadIdx.x == 0) p.wide[atomicAdd(wide_n, 1u)] = e;   // instantiation re-runs it

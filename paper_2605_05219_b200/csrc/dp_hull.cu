@@ -2093,8 +2093,9 @@ __global__ void __launch_bounds__(64, 1) dp_hull_split_kernel(HullParams p) {
     const int2* klist = sparse_row ? p.sparse + (size_t)e * HULL_KC : nullptr;
     unsigned pops_e = 0, ev_e = 0;
     bool logfull = false;
-#ifdef SP_SPLIT_ROLES
-    // each warp's role at compile time (warp 0 chains out, warp 1 chains in)
+#ifndef SP_SPLIT_NO_ROLES
+    // each warp's role at compile time (warp 0 chains out, warp 1 chains in): 2048 W5 entries
+    // 5.74 -> 5.64 ms (profiles/r02e_dp_variants.txt)
     if (w == 0) {
       if (fullm)
         hull_dp_any<WT, int, 1, true, SRingI<HC0, HC1>, false, false, 1>(

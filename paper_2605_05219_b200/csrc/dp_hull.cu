@@ -1393,6 +1393,11 @@ __device__ __forceinline__ void hull_cbb_f64(const HullParams& p, int e, int tfi
 // int64 / fp64 instantiations: capped at 168 registers (no spills) so that an SM sub-partition
 // holds 3 of their warps, not 2 (202 / 192 registers: 8 warps per SM; now 9, the shared-memory
 // bound): accumulated rows 226 -> 210 ms, fp64 W5 rows 68.3 -> 62.0 ms (profiles/r02e_dp_variants.txt)
+#ifdef SP_HULL_BIG_ONEPASS
+constexpr bool BIG_ONEPASS = true;
+#else
+constexpr bool BIG_ONEPASS = false;
+#endif
 #ifndef SP_HULL_WIDE_MINB
 #define SP_HULL_WIDE_MINB 12
 #endif
@@ -1550,12 +1555,13 @@ __global__ void __launch_bounds__(32, BIG ? (K == 1 ? 16 : SP_HULL_BIG_MINB)
     const bool fullm = M % (32 * K) == 0;
     bool ovf;
     if constexpr (BIG) {
-      ovf = fullm ? hull_dp_any<WT, VT, K, true, SR, true>(p, we, e, TN, nV, srg, logs, logn, ebuf0,
-                                                           ebuf1, pops_e, ev_e, logfull, stage,
-                                                           kcomp, klist)
-                  : hull_dp_any<WT, VT, K, false, SR, true>(p, we, e, TN, nV, srg, logs, logn,
-                                                            ebuf0, ebuf1, pops_e, ev_e, logfull,
-                                                            stage, kcomp, klist);
+      // (the mode runs M <= 64 only: always one pass)
+      ovf = fullm ? hull_dp_any<WT, VT, K, true, SR, true, BIG_ONEPASS>(
+                        p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1, pops_e, ev_e, logfull,
+                        stage, kcomp, klist)
+                  : hull_dp_any<WT, VT, K, false, SR, true, BIG_ONEPASS>(
+                        p, we, e, TN, nV, srg, logs, logn, ebuf0, ebuf1, pops_e, ev_e, logfull,
+                        stage, kcomp, klist);
     } else if constexpr (std::is_same<VT, int>::value) {
       // int32: plain shared rings first (W5: 16 of 16384 entries outgrow them); an entry whose
       // hull outgrows a ring is re-run at once with the windowed ring (the same window plus
